@@ -1,0 +1,88 @@
+"""Seeded synthetic inputs with the shapes of BASELINE.json's configs.
+
+The reference's own datasets (ORL Faces, V2D snapshots, Yale Faces; see
+``ref/PAPER.md:89-104``) are not available, so these generators stand in
+for them with the shapes, spectra and noise levels BASELINE.json states.
+Noise "N(0, x)" is read as variance x.
+
+* ``config1`` -- A = U diag(exp(-i/10)) V^T + N(0, 1e-6), m=2000, n=500,
+  U, V Haar (Q of QR of N(0,1)), numpy PCG64 from a seed; CPU-reproducible.
+* ``config2`` -- snapshot-like Fourier field: column t is
+  sum_{j=1..40} j^-2 cos(2 pi (kx_j x + ky_j y)/L + phi_{j,t}) on an L x L
+  grid flattened (L=512 -> m=262144), n=2000, + N(0, 1e-4), rows mean-centred
+  (``matcore.py:168-175`` semantics).  Built as A = B C with B the m x 80
+  cos/sin basis, so it is a GEMM on the device; ``side`` shrinks the grid
+  for proxies.
+
+Data generation is outside every timed region.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+CFG1 = dict(m=2000, n=500, k=10, r=30, c=50, tol=1e-8)
+CFG2 = dict(side=512, n=2000, k=20, r=60, c=100, tol=1e-8)
+
+
+def config1(seed=0, m=2000, n=500, noise_var=1e-6):
+    """BASELINE config 1 (CPU-runnable oracle case), float64 F-order."""
+    rng = np.random.default_rng(seed)
+    u = np.linalg.qr(rng.standard_normal((m, n)))[0]
+    v = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    s = np.exp(-np.arange(n) / 10.0)
+    a = (u * s) @ v.T + math.sqrt(noise_var) * rng.standard_normal((m, n))
+    return np.asfortranarray(a)
+
+
+def _fourier_modes(seed, nmodes=40, kmax=12):
+    rng = np.random.default_rng(seed)
+    ks = set()
+    out = []
+    while len(out) < nmodes:
+        kx, ky = (int(v) for v in rng.integers(-kmax, kmax + 1, size=2))
+        if (kx, ky) == (0, 0) or (kx, ky) in ks or (-kx, -ky) in ks:
+            continue
+        ks.add((kx, ky))
+        out.append((kx, ky))
+    return np.array(out, dtype=np.float64)
+
+
+def config2_torch(seed=0, side=512, n=2000, noise_var=1e-4, device="cpu",
+                  nmodes=40):
+    """BASELINE config 2 snapshot matrix as a column-major float64 torch
+    tensor of logical shape (m, n) (storage: n x m row-major, i.e. A^T
+    contiguous).  Deterministic for a (seed, device type) pair."""
+    import torch
+
+    m = side * side
+    modes = _fourier_modes(seed, nmodes)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(int(seed) * 7919 + 17)
+    dt = torch.float64
+    yy, xx = torch.meshgrid(torch.arange(side, dtype=dt, device=device),
+                            torch.arange(side, dtype=dt, device=device),
+                            indexing="ij")
+    x = xx.reshape(-1)
+    y = yy.reshape(-1)
+    kx = torch.tensor(modes[:, 0], dtype=dt, device=device)
+    ky = torch.tensor(modes[:, 1], dtype=dt, device=device)
+    theta = (2.0 * math.pi / side) * (x[:, None] * kx[None, :] + y[:, None] * ky[None, :])
+    basis = torch.cat([torch.cos(theta), torch.sin(theta)], dim=1)  # m x 2J
+    amp = torch.arange(1, nmodes + 1, dtype=dt, device=device) ** -2.0
+    phi = 2.0 * math.pi * torch.rand((nmodes, n), generator=gen, dtype=dt, device=device)
+    coef = torch.cat([amp[:, None] * torch.cos(phi), -amp[:, None] * torch.sin(phi)], dim=0)
+    at = (basis @ coef).T.contiguous()  # n x m storage == A column-major
+    del basis, theta
+    at.add_(torch.randn(at.shape, generator=gen, dtype=dt, device=device),
+            alpha=math.sqrt(noise_var))
+    at.sub_(at.mean(dim=0, keepdim=True))  # subtract each row's mean of A
+    return at  # A = at.T
+
+
+def config2(seed=0, side=512, n=2000, noise_var=1e-4):
+    """Host (numpy, F-order) copy of ``config2_torch`` generated on the CPU."""
+    at = config2_torch(seed, side, n, noise_var, device="cpu")
+    return np.asfortranarray(at.numpy().T)

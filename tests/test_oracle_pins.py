@@ -1,0 +1,104 @@
+"""Pin the CPU oracle (oracle/isma_oracle.py) to the reference's own outputs
+(tests/golden/*.npz, written by tests/golden/make_golden.py which runs the
+reference package) and to the reference test suite's known-answer vectors."""
+
+import numpy as np
+import pytest
+from conftest import load_golden
+
+from oracle import isma_oracle as orc
+from paper_1905_05107_b200 import workloads
+
+
+def _case_matrix(name):
+    if name.startswith("cfg1"):
+        return workloads.config1(seed=0)
+    if name.startswith("rank3"):
+        from conftest import make_low_rank
+        return make_low_rank(100, 60, 3, np.random.default_rng(7))
+    if name == "exhaustive_40x18":
+        return np.random.default_rng(13).standard_normal((40, 18))
+    if name == "cfg2proxy_l2n":
+        return workloads.config2(seed=1, side=64, n=300)
+    raise KeyError(name)
+
+
+CASES = ["cfg1_l2n_modes", "cfg1_unf_subspace", "cfg1_l2n_nofinal_keep11",
+         "rank3_unf", "rank3_l2n", "exhaustive_40x18", "cfg2proxy_l2n"]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_matches_reference_golden(name):
+    g = load_golden(name)
+    k, r, c, fin, keep = (int(x) for x in g["meta"])
+    a = _case_matrix(name)
+    out = orc.run(a, k, r=r, c=c, tau=float(g["tau"]), strategy=str(g["strategy"]),
+                  criterion=str(g["criterion"]), seed=int(g["seed"]),
+                  do_finalize=bool(fin), keep=None if keep < 0 else keep)
+    tr = out["trace"]
+    assert len(tr) == int(g["n_rounds"])
+    # per-round index sets and counts bit-exact
+    off = g["draw_off"]
+    for i, t in enumerate(tr):
+        np.testing.assert_array_equal(t["unique"], g["draw_idx"][off[i]:off[i + 1]])
+        np.testing.assert_array_equal(t["counts"], g["draw_cnt"][off[i]:off[i + 1]])
+        assert t["remaining"] == g["remaining"][i]
+    # same arithmetic in the same order: bit-identical on this machine
+    np.testing.assert_array_equal(out["sigma"], g["sigma"])
+    np.testing.assert_array_equal(out["u"], g["u"])
+    if fin:
+        np.testing.assert_array_equal(out["v"], g["v"])
+
+
+def test_merge_fixtures():
+    g = load_golden("merges")
+    for i in range(4):
+        u, s = orc.merge(g[f"m{i}_u1"], g[f"m{i}_s1"], g[f"m{i}_u2"], g[f"m{i}_s2"],
+                         int(g[f"m{i}_r"]))
+        np.testing.assert_array_equal(s, g[f"m{i}_s"])
+        np.testing.assert_array_equal(u, g[f"m{i}_u"])
+
+
+def test_incremental_fixture():
+    g = load_golden("incremental_t3")
+    a = workloads.config1(seed=int(g["seed"]), m=300, n=120)
+    out = orc.incremental(orc.column_blocks(a, 3), 4, c=20, tau=0.999, seed=9)
+    np.testing.assert_array_equal(out["sigma"], g["sigma"])
+    np.testing.assert_array_equal(out["u"], g["u"])
+    np.testing.assert_array_equal([t["remaining"] for t in out["trace"]], g["remaining"])
+
+
+def test_wedin_fixture():
+    g = load_golden("wedin_cfg1")
+    a = workloads.config1(seed=0)
+    rep = orc.wedin(a, g["u"], g["sigma"], g["v"], 10)
+    for key in ("r_norm", "s_norm", "omega_hat", "measure"):
+        assert rep[key] == float(g[key])
+
+
+def test_inverse_cdf_known_answer():
+    # reference tests/test_sampling.py:197-203
+    idx, cnt = orc.cdf_draw(np.array([3, 7, 9]), np.array([0.2, 0.3, 0.5]),
+                            np.array([0.05, 0.21, 0.45, 0.51, 0.99]))
+    np.testing.assert_array_equal(idx, [3, 7, 9])
+    np.testing.assert_array_equal(cnt, [1, 2, 2])
+
+
+def test_cdf_edge_trailing_zero_unreachable():
+    # reference tests/test_sampling.py:236-242
+    idx, _ = orc.cdf_draw(np.array([0, 1, 2]), np.array([0.5, 0.5, 0.0]),
+                          np.array([1.0 - 1e-16, 0.999999999]))
+    np.testing.assert_array_equal(idx, [1])
+
+
+def test_norm_ratio_weights():
+    # reference tests/test_sampling.py:75-78: column norms 1:2 -> weights 0.2, 0.8
+    a = np.array([[1.0, 2.0], [0.0, 0.0]])
+    w = orc.normalized_weights(orc.column_norms2(a))
+    np.testing.assert_allclose(w, [0.2, 0.8], rtol=1e-15)
+
+
+def test_budget_formula():
+    # reference tests/test_sampling.py:363-373 (acceptance 8): k=1, eps=1, delta=0.5
+    assert orc.ltsvd_count(10, 0.7, 0.6) == 746
+    assert orc.ltsvd_count(20, 0.7, 0.6) == 1491
