@@ -1,0 +1,148 @@
+/* podsketch-b200 C ABI -- the drop-in boundary for the ISMA hot path.
+ *
+ * The reference (podsketch 0.1.0) is a pure-Python package: its hot path
+ * sits behind a Python API, not an FFI.  Each entry point below replaces
+ * the numpy/LAPACK call site cited beside it; the Python host layer
+ * (paper_1905_05107_b200/) binds them with ctypes and keeps the reference's
+ * names, argument meaning and error behaviour.
+ *
+ * Conventions
+ *   - Matrices are column-major float64 with an explicit leading dimension
+ *     (the reference's Fortran-order storage, matcore.py:4-7).
+ *   - Every pointer argument is DEVICE memory owned by the caller, except
+ *     where noted.  Nothing allocates device memory; scratch is passed in
+ *     as (ws, ws_bytes) sized by the matching *_ws_bytes query.
+ *   - `stream` is a cudaStream_t; all work is enqueued asynchronously.
+ *   - Column index lists (`*cols`, int32) address a matrix's columns
+ *     indirectly, so a sampled block A[:, idx] is read in place.
+ *   - Return codes mirror the reference's error classes (errors.py:8-21):
+ *     POD_OK, POD_EPARAM (ParameterError, CLI exit 2), POD_EFORMAT
+ *     (FormatError, 3), POD_EDEGENERATE (DegenerateDistributionError, 4),
+ *     POD_ENOCONVERGE (scipy LinAlgError), POD_ECUDA; message text via
+ *     pod_last_error().
+ */
+#ifndef PODSKETCH_B200_H
+#define PODSKETCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POD_OK 0
+#define POD_EPARAM 2
+#define POD_EFORMAT 3
+#define POD_EDEGENERATE 4
+#define POD_ENOCONVERGE 5
+#define POD_ECUDA 6
+#define POD_ENCCL 7
+
+int pod_abi_version(void);
+/* Last error message of the calling thread ("" if none). */
+const char* pod_last_error(void);
+
+/* Squared column norms ||A[:, j]||^2 and a non-finite flag, one HBM pass.
+ * Replaces matcore.py:54 (isfinite), isma.py:260 and sampling.py:136
+ * (einsum "ij,ij->j").  nonfinite is set to 1 if any entry is NaN/Inf. */
+int pod_colnorms2_f64(const double* A, int64_t m, int64_t n, int64_t lda, double* norms2,
+                      int32_t* nonfinite, void* stream);
+
+/* Inverse-CDF draw with replacement + unique/counts + retirement.
+ * Replaces sampling.py:204-222 (sample_with_replacement) together with the
+ * distribution it samples -- mode 0: l2n over live columns, weights =
+ * raw norms2 normalised as sampling.py:55-65,34-53; mode 1: uniform over
+ * live columns (sampling.py:150-155); mode 2: explicit normalised weights
+ * over positions 0..n-1 (a Distribution's weights, no live mask) -- and the
+ * candidate-set update isma.py:164 (drawn columns cleared in `live`).
+ * `uniforms` holds the c variates of ONE rng.random(c) batch.
+ * Outputs: idx_out[0..g) ascending int32, cnt_out[0..g) int64,
+ * info[0] = g, info[1] = |S| after the draw, info[2] = status
+ * (0 ok, 1 empty S, 2 all weights zero -> DegenerateDistributionError). */
+size_t pod_draw_ws_bytes(int64_t n);
+int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n, const double* uniforms,
+             int64_t c, int32_t* idx_out, int64_t* cnt_out, void* ws, size_t ws_bytes,
+             int64_t* info, void* stream);
+
+/* C (p x q) = alpha X^T Y, X m x p, Y m x q, K = m split across CTAs with
+ * a fixed-order reduction (deterministic).  FP64 DMMA.8x8x4.
+ * Replaces: baselines.py:43 (D^T D), merge.py:65 (U1^T U2), merge.py:72/75
+ * (U1^T Q), isma.py:296 (A^T U), quality.py:104-105 partial products. */
+size_t pod_gemm_tn_ws_bytes(int64_t m, int64_t p, int64_t q);
+int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X, int64_t ldx,
+                    const int32_t* xcols, const double* Y, int64_t ldy, const int32_t* ycols,
+                    double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+
+/* Y (m x q) = alpha X T + beta Z, X m x p (optionally column-gathered),
+ * T p x q small.  FP64 DMMA.8x8x4.  Y may alias X when q <= 64.
+ * Replaces: baselines.py:62-63 (D V / sigma), merge.py:69 (U2 - U1 M),
+ * merge.py:86-88 ([U1 Q] U_E), isma.py:298-299 (U V_R, Q U_R). */
+int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X, int64_t ldx,
+                    const int32_t* xcols, const double* T, int64_t ldt, double beta,
+                    const double* Z, int64_t ldz, double* Y, int64_t ldy, void* stream);
+
+/* Workspace (bytes) sufficient for any small solve of dimension <= n. */
+size_t pod_small_ws_bytes(int64_t n);
+
+/* gram_spectrum + lift setup (baselines.py:35-65): eigen-decomposition of
+ * the PSD Gram G (g x g), descending, eigenvalue dust <= 1e-12 lambda_1
+ * zeroed (matcore.py:26), sigma = sqrt(lambda) into sigma[0..g);
+ * rank = #sigma > 1e-14 sigma_1 (matcore.py:20), keep = min(r, rank);
+ * T (g x r, ld ldt) = V[:, :keep] / sigma[:keep], zero columns beyond keep.
+ * info[0] = rank, info[1] = keep, info[2] = Jacobi sweeps. */
+int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r, double* sigma, double* T,
+                  int64_t ldt, int64_t* info, void* ws, size_t ws_bytes, void* stream);
+
+/* One CholeskyQR pass from the Gram G = W^T W (l x l) of an nrows x l
+ * block: R (upper) and Rinv such that Q = W Rinv has orthonormal columns
+ * and W = Q R.  Column-scaled, shifted on breakdown, exactly-zero columns
+ * dropped (zero R rows).  Replaces the Householder QR of merge.py:70,76 and
+ * matcore.py:209.  dinfo[0] = max |D^-1 G D^-1 - I| (input defect),
+ * dinfo[1] = shift attempts, dinfo[2] = dropped columns, dinfo[3] = shift. */
+int pod_cholqr_factor(const double* G, int64_t ldg, int64_t l, int64_t nrows, double* Rinv,
+                      int64_t ldri, double* R, int64_t ldr, double* dinfo, void* ws,
+                      size_t ws_bytes, void* stream);
+
+/* Merge core (merge.py:80-88): E = [[diag sig1, M diag sig2],[0, R diag sig2]],
+ * its SVD, keep = min(r, #sigma_E > 1e-14 max(sigma_E0, 1e-300)), and the
+ * rotation T ((rcap + l2) x tcols, ld ldt) mapping the stacked basis
+ * [U1 | 0-pad to rcap | Q] onto the merged left vectors.  info[0] = keep. */
+int pod_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
+                   int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
+                   int64_t ldt, int64_t tcols, double* sig_new, int64_t* info, void* ws,
+                   size_t ws_bytes, void* stream);
+
+/* Thin SVD of a small nr x nc matrix (nr >= nc) by one-sided Jacobi:
+ * sigma descending; if U and V are non-null, U (nr x nc) and V (nc x nc)
+ * with A = U diag(sigma) V^T.  Replaces matcore.py:178-184 (_svd) at
+ * isma.py:297 and np.linalg.svd at isma.py:198 / quality.py:56. */
+int pod_svd_small(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int64_t ldu,
+                  double* sigma, double* V, int64_t ldv, int64_t* info, void* ws, size_t ws_bytes,
+                  void* stream);
+
+/* C (p x q) = alpha op(A) B + beta C for small matrices (op = A or A^T). */
+int pod_small_gemm(int64_t p, int64_t q, int64_t k, double alpha, const double* A, int64_t lda,
+                   int transa, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                   void* stream);
+
+/* out[0] = max |A| over a p x q block (merge.py:72 leak test). */
+int pod_maxabs(const double* A, int64_t lda, int64_t p, int64_t q, double* out, void* stream);
+
+/* fix_signs (matcore.py:148-165): per column, the first entry of largest
+ * magnitude is made positive; V (n x l) flipped alongside when non-null.
+ * sign_out (l, optional) receives the +-1 factors. */
+size_t pod_colwise_ws_bytes(int64_t m, int64_t l);
+int pod_fix_signs(double* U, int64_t m, int64_t l, int64_t ldu, double* V, int64_t n, int64_t ldv,
+                  double* sign_out, void* ws, size_t ws_bytes, void* stream);
+
+/* out[j] = sum_i P[i, j] Q[i, j] for j < kk, 0 for kk <= j < k; with
+ * take_abs the |.| clipped to [0, 1] (convergence cosines, isma.py:195-201). */
+int pod_coldots(const double* P, int64_t ldp, const double* Q, int64_t ldq, int64_t m, int64_t k,
+                int64_t kk, int take_abs, double* out, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PODSKETCH_B200_H */

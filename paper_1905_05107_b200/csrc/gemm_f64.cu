@@ -1,0 +1,334 @@
+// FP64 tall-skinny GEMMs on the tensor pipe (DMMA.8x8x4) for sm_100a.
+//
+// Every m-length operand of the ISMA round is a column-major matrix whose
+// row count m is huge (rows of the data matrix) and whose column count is
+// small (sampled columns g, factor modes r).  Two shapes cover the round:
+//
+//   TN  C (p x q) = alpha X^T Y          K = m: Gram D^T D (baselines.py:43),
+//                                         U1^T U2 (merge.py:65), CholQR Grams,
+//                                         leak U1^T Q (merge.py:72), finalize
+//                                         A^T U (isma.py:296)
+//   NN  Y (m x q) = alpha X T + beta Z    lift D V / sigma (baselines.py:62-63),
+//                                         U2 - U1 M (merge.py:69), Q = W R^-1,
+//                                         [U1 Q] U_E (merge.py:86-88),
+//                                         finalize rotations (isma.py:298-299)
+//
+// X (and Y) may be addressed through a column index list, so the sampled
+// block D = A[:, idx] is never materialised (isma.py:163 gather fused into
+// the operand loads).  TN splits K=m across CTAs and reduces the partial
+// tiles in a fixed order (deterministic, no atomics).
+#include "common.cuh"
+
+namespace pod {
+
+// ---------------------------------------------------------------- TN ------
+namespace tn {
+constexpr int BP = 64, BQ = 64, BK = 32, LDS = BK + 4;  // LDS % 16 == 4: conflict-free frags
+constexpr int THREADS = 256;
+constexpr int STAGES = 3;
+constexpr int TILE_DBL = BP * LDS;  // doubles per operand tile
+constexpr size_t SMEM = size_t(STAGES) * 2 * TILE_DBL * sizeof(double);
+
+__device__ __forceinline__ const double* colptr(const double* base, int64_t ld,
+                                                const int32_t* cols, int c) {
+  return base + (cols ? (int64_t)cols[c] : (int64_t)c) * ld;
+}
+
+__global__ void __launch_bounds__(THREADS) partial_kernel(
+    int64_t m, int p, int q, const double* __restrict__ X, int64_t ldx,
+    const int32_t* __restrict__ xcols, const double* __restrict__ Y, int64_t ldy,
+    const int32_t* __restrict__ ycols, int64_t rows_per_split, double* __restrict__ ws) {
+  extern __shared__ __align__(16) double smem[];
+  const int tiles_p = (p + BP - 1) / BP;
+  const int tp = blockIdx.x % tiles_p, tq = blockIdx.x / tiles_p;
+  const int split = blockIdx.y;
+  const int64_t r0 = (int64_t)split * rows_per_split;
+  const int64_t r1 = min(m, r0 + rows_per_split);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  // Each thread loads row (r + lane) of 8 columns per operand per stage.
+  const double* xp[8];
+  const double* yp[8];
+  bool xv[8], yv[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int cx = tp * BP + warp + 8 * i;
+    int cy = tq * BQ + warp + 8 * i;
+    xv[i] = cx < p;
+    yv[i] = cy < q;
+    xp[i] = xv[i] ? colptr(X, ldx, xcols, cx) : X;
+    yp[i] = yv[i] ? colptr(Y, ldy, ycols, cy) : Y;
+  }
+  auto load_stage = [&](int st, int64_t rb) {
+    double* xs = smem + (size_t)st * 2 * TILE_DBL;
+    double* ys = xs + TILE_DBL;
+    const int64_t row = rb + lane;
+    const bool rv = row < r1;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int c = warp + 8 * i;
+      cp_async8(xs + c * LDS + lane, xv[i] && rv ? xp[i] + row : X, xv[i] && rv);
+      cp_async8(ys + c * LDS + lane, yv[i] && rv ? yp[i] + row : Y, yv[i] && rv);
+    }
+  };
+
+  const int wp = warp & 1, wq = warp >> 1;  // warp tile: 32 (p) x 16 (q)
+  double acc[4][2][2];
+#pragma unroll
+  for (int f = 0; f < 4; ++f)
+#pragma unroll
+    for (int g = 0; g < 2; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+
+  const int64_t nkb = (r1 > r0) ? (r1 - r0 + BK - 1) / BK : 0;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nkb) load_stage(s, r0 + (int64_t)s * BK);
+    cp_async_commit();
+  }
+  for (int64_t kb = 0; kb < nkb; ++kb) {
+    const int64_t nxt = kb + STAGES - 1;
+    if (nxt < nkb) load_stage((int)(nxt % STAGES), r0 + nxt * BK);
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    __syncthreads();
+    const double* xs = smem + (size_t)(kb % STAGES) * 2 * TILE_DBL;
+    const double* ys = xs + TILE_DBL;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double a[4], b[2];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+        a[f] = xs[(wp * 32 + f * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+#pragma unroll
+      for (int g = 0; g < 2; ++g)
+        b[g] = ys[(wq * 16 + g * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int g = 0; g < 2; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  double* out = ws + (size_t)split * p * q;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int i = tp * BP + wp * 32 + f * 8 + (lane >> 2);
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = tq * BQ + wq * 16 + g * 8 + 2 * (lane & 3) + e;
+        if (i < p && j < q) out[(size_t)j * p + i] = acc[f][g][e];
+      }
+  }
+}
+
+__global__ void reduce_kernel(int nsplit, int p, int q, double alpha, const double* __restrict__ ws,
+                              double* __restrict__ C, int64_t ldc) {
+  const int64_t total = (int64_t)p * q;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < nsplit; ++k) s += ws[(size_t)k * total + t];
+    const int64_t j = t / p, i = t - j * p;
+    C[i + j * ldc] = alpha * s;
+  }
+}
+
+struct Plan {
+  int tiles, splits;
+  int64_t rows_per_split;
+};
+
+inline Plan plan(int64_t m, int64_t p, int64_t q) {
+  Plan pl;
+  pl.tiles = (int)(ceil_div(p, BP) * ceil_div(q, BQ));
+  const int target = 2 * 148;
+  int64_t want = ceil_div(target, pl.tiles);
+  int64_t max_by_rows = std::max<int64_t>(1, ceil_div(m, 4 * BK));  // >= 4 k-blocks per CTA
+  int64_t splits = std::min<int64_t>(want, max_by_rows);
+  splits = std::max<int64_t>(1, std::min<int64_t>(splits, 65535));
+  pl.rows_per_split = ceil_div(ceil_div(m, splits), BK) * BK;
+  if (pl.rows_per_split == 0) pl.rows_per_split = BK;
+  pl.splits = (int)std::max<int64_t>(1, ceil_div(m, pl.rows_per_split));
+  return pl;
+}
+}  // namespace tn
+
+// ---------------------------------------------------------------- NN ------
+namespace nn {
+constexpr int BM = 128, BN = 64, BK = 16;
+constexpr int LDX = BM + 4;  // % 16 == 4
+constexpr int LDT = BK + 4;  // % 16 == 4
+constexpr int THREADS = 256;
+constexpr int STAGES = 3;
+constexpr int XT = BK * LDX, TT = BN * LDT;
+constexpr size_t SMEM = size_t(STAGES) * (XT + TT) * sizeof(double);
+
+__global__ void __launch_bounds__(THREADS) kernel(
+    int64_t m, int p, int q, double alpha, const double* __restrict__ X, int64_t ldx,
+    const int32_t* __restrict__ xcols, const double* __restrict__ T, int64_t ldt, double beta,
+    const double* Z, int64_t ldz, double* Y, int64_t ldy) {
+  extern __shared__ __align__(16) double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row0 = (int64_t)blockIdx.x * BM;
+  const int col0 = blockIdx.y * BN;
+  const int64_t lrow = row0 + (warp & 3) * 32 + lane;  // this thread's load row
+  const bool lrv = lrow < m;
+  const int lc0 = (warp >> 2) * 8;  // first of 8 columns this thread loads per stage
+
+  auto load_stage = [&](int st, int k0) {
+    double* xs = smem + (size_t)st * (XT + TT);
+    double* ts = xs + XT;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int c = k0 + lc0 + i;
+      const bool v = lrv && c < p;
+      const double* src = v ? X + (xcols ? (int64_t)xcols[c] : (int64_t)c) * ldx + lrow : X;
+      cp_async8(xs + (lc0 + i) * LDX + (warp & 3) * 32 + lane, src, v);
+    }
+    // T chunk: rows k0..k0+BK, cols col0..col0+BN; thread -> (j = tid/4, k = (tid%4)*4 + e)
+    const int j = threadIdx.x >> 2;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = (threadIdx.x & 3) * 4 + e;
+      const bool v = (col0 + j) < q && (k0 + k) < p;
+      const double* src = v ? T + (k0 + k) + (int64_t)(col0 + j) * ldt : T;
+      cp_async8(ts + j * LDT + k, src, v);
+    }
+  };
+
+  const int wm = warp & 3, wn = warp >> 2;  // warp tile: 32 rows x 32 cols
+  double acc[4][4][2];
+#pragma unroll
+  for (int f = 0; f < 4; ++f)
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+
+  const int nkb = (p + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nkb) load_stage(s, s * BK);
+    cp_async_commit();
+  }
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int nxt = kb + STAGES - 1;
+    if (nxt < nkb) load_stage(nxt % STAGES, nxt * BK);
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    __syncthreads();
+    const double* xs = smem + (size_t)(kb % STAGES) * (XT + TT);
+    const double* ts = xs + XT;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+        a[f] = xs[(kk * 4 + (lane & 3)) * LDX + wm * 32 + f * 8 + (lane >> 2)];
+#pragma unroll
+      for (int g = 0; g < 4; ++g)
+        b[g] = ts[(wn * 32 + g * 8 + (lane >> 2)) * LDT + kk * 4 + (lane & 3)];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t i = row0 + wm * 32 + f * 8 + (lane >> 2);
+    if (i >= m) continue;
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = col0 + wn * 32 + g * 8 + 2 * (lane & 3) + e;
+        if (j < q) {
+          double v = alpha * acc[f][g][e];
+          if (beta != 0.0) v += beta * Z[i + (int64_t)j * ldz];
+          Y[i + (int64_t)j * ldy] = v;
+        }
+      }
+  }
+}
+}  // namespace nn
+
+static bool g_attr_done = false;
+static int ensure_attrs() {
+  if (g_attr_done) return POD_OK;
+  cudaError_t e = cudaFuncSetAttribute(tn::partial_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tn::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "tn attr");
+  e = cudaFuncSetAttribute(nn::kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nn::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "nn attr");
+  g_attr_done = true;
+  return POD_OK;
+}
+
+}  // namespace pod
+
+using namespace pod;
+
+extern "C" size_t pod_gemm_tn_ws_bytes(int64_t m, int64_t p, int64_t q) {
+  if (m <= 0 || p <= 0 || q <= 0) return 0;
+  tn::Plan pl = tn::plan(m, p, q);
+  return (size_t)pl.splits * p * q * sizeof(double);
+}
+
+extern "C" int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
+                               int64_t ldx, const int32_t* xcols, const double* Y, int64_t ldy,
+                               const int32_t* ycols, double* C, int64_t ldc, void* ws,
+                               size_t ws_bytes, void* stream) {
+  POD_REQUIRE(m >= 0 && p >= 0 && q >= 0, "pod_gemm_tn_f64: negative size");
+  POD_REQUIRE(ldc >= p, "pod_gemm_tn_f64: ldc < p");
+  if (p == 0 || q == 0) return POD_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (m == 0) {
+    for (int64_t j = 0; j < q; ++j) {
+      cudaError_t e = cudaMemsetAsync(C + j * ldc, 0, p * sizeof(double), s);
+      if (e != cudaSuccess) return cuda_status(e, "tn memset");
+    }
+    return POD_OK;
+  }
+  int st = ensure_attrs();
+  if (st) return st;
+  tn::Plan pl = tn::plan(m, p, q);
+  POD_REQUIRE(ws_bytes >= (size_t)pl.splits * p * q * sizeof(double),
+              "pod_gemm_tn_f64: workspace too small (%zu < %zu)", ws_bytes,
+              (size_t)pl.splits * p * q * sizeof(double));
+  dim3 grid(pl.tiles, pl.splits);
+  tn::partial_kernel<<<grid, tn::THREADS, tn::SMEM, s>>>(m, (int)p, (int)q, X, ldx, xcols, Y, ldy,
+                                                         ycols, pl.rows_per_split, (double*)ws);
+  POD_CHECK_LAUNCH("tn partial");
+  int64_t tot = p * q;
+  int blocks = (int)std::min<int64_t>(ceil_div(tot, 256), 4 * 148);
+  tn::reduce_kernel<<<blocks, 256, 0, s>>>(pl.splits, (int)p, (int)q, alpha, (const double*)ws, C,
+                                           ldc);
+  POD_CHECK_LAUNCH("tn reduce");
+  return POD_OK;
+}
+
+extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
+                               int64_t ldx, const int32_t* xcols, const double* T, int64_t ldt,
+                               double beta, const double* Z, int64_t ldz, double* Y, int64_t ldy,
+                               void* stream) {
+  POD_REQUIRE(m >= 0 && p >= 0 && q >= 0, "pod_gemm_nn_f64: negative size");
+  if (m == 0 || q == 0) return POD_OK;
+  POD_REQUIRE(ldy >= m, "pod_gemm_nn_f64: ldy < m");
+  POD_REQUIRE(beta == 0.0 || Z != nullptr, "pod_gemm_nn_f64: beta != 0 needs Z");
+  const bool aliased = (Y == X) || (Y == Z && Z != nullptr && ldz != ldy);
+  POD_REQUIRE(!(Y == X && q > nn::BN), "pod_gemm_nn_f64: in-place needs q <= %d", nn::BN);
+  (void)aliased;
+  int st = ensure_attrs();
+  if (st) return st;
+  dim3 grid((unsigned)ceil_div(m, nn::BM), (unsigned)ceil_div(q, nn::BN));
+  nn::kernel<<<grid, nn::THREADS, nn::SMEM, (cudaStream_t)stream>>>(
+      m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy);
+  POD_CHECK_LAUNCH("nn");
+  return POD_OK;
+}

@@ -1,0 +1,210 @@
+"""Device plumbing: column-major device matrices, workspaces, and typed
+wrappers over the C ABI.  PyTorch provides memory, streams and the host
+side of collectives only; every numeric step below runs in
+libpodsketch_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import DeviceError
+
+try:  # torch is the memory/stream provider
+    import torch
+except ImportError as exc:  # pragma: no cover
+    raise DeviceError("PyTorch is required for device memory") from exc
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+class ColMat:
+    """A column-major float64 device matrix: storage is a torch tensor of
+    shape (cols, ld) whose row j is column j; m <= ld logical rows."""
+
+    __slots__ = ("t", "m", "ncols", "ld", "col0")
+
+    def __init__(self, t, m, ncols=None, col0=0):
+        self.t = t
+        self.ld = int(t.shape[1])
+        self.m = int(m)
+        self.ncols = int(t.shape[0] - col0) if ncols is None else int(ncols)
+        self.col0 = int(col0)
+
+    @classmethod
+    def zeros(cls, m, ncols, device, ld=None):
+        ld = int(m) if ld is None else int(ld)
+        return cls(torch.zeros((max(int(ncols), 1), ld), dtype=torch.float64, device=device), m,
+                   ncols)
+
+    def cols(self, a, b=None):
+        b = self.ncols if b is None else b
+        return ColMat(self.t, self.m, b - a, self.col0 + a)
+
+    @property
+    def ptr(self):
+        return ctypes.c_void_p(self.t.data_ptr() + 8 * self.ld * self.col0)
+
+    def to_numpy(self, ncols=None):
+        nc = self.ncols if ncols is None else ncols
+        blk = self.t[self.col0:self.col0 + nc, :self.m]
+        return np.asfortranarray(blk.cpu().numpy().T)
+
+
+class Ctx:
+    """Per-device execution context: stream handle, grow-only workspaces,
+    pinned mailboxes for the per-round scalars the host reads."""
+
+    def __init__(self, device=None):
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device available; the ISMA path runs on the GPU only")
+        _lib.load()
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        self._ws = {}
+        self.info = torch.zeros(16, dtype=torch.int64, device=self.device)
+        self.dinfo = torch.zeros(16, dtype=torch.float64, device=self.device)
+        self.h_info = torch.zeros(16, dtype=torch.int64).pin_memory()
+        self.h_dinfo = torch.zeros(16, dtype=torch.float64).pin_memory()
+
+    @property
+    def stream(self):
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def ws(self, key, nbytes):
+        nbytes = max(int(nbytes), 256)
+        buf = self._ws.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._ws[key] = buf
+        return buf
+
+    def read_info(self, n=4):
+        self.h_info[:n].copy_(self.info[:n], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return [int(x) for x in self.h_info[:n].tolist()]
+
+    def read_dinfo(self, n=4):
+        self.h_dinfo[:n].copy_(self.dinfo[:n], non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return [float(x) for x in self.h_dinfo[:n].tolist()]
+
+    # ------------------------------------------------------------ kernels
+    def colnorms2(self, A, out, flag):
+        _lib.call("pod_colnorms2_f64", A.ptr, A.m, A.ncols, A.ld, _ptr(out), _ptr(flag),
+                  self.stream)
+
+    def draw(self, mode, weights, live, n, uniforms, c, idx, cnt):
+        ws = self.ws("draw", _lib.load().pod_draw_ws_bytes(n))
+        _lib.call("pod_draw", mode, _ptr(weights), _ptr(live), n, _ptr(uniforms), c, _ptr(idx),
+                  _ptr(cnt), _ptr(ws), ws.numel(), _ptr(self.info), self.stream)
+
+    def tn(self, p, q, alpha, X, Y, C, ldc, xcols=None, ycols=None, m=None):
+        m = X.m if m is None else m
+        if p == 0 or q == 0:
+            return
+        need = _lib.load().pod_gemm_tn_ws_bytes(m, p, q)
+        ws = self.ws("tn", need)
+        _lib.call("pod_gemm_tn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), Y.ptr, Y.ld,
+                  _ptr(ycols), C, ldc, _ptr(ws), ws.numel(), self.stream)
+
+    def nn(self, p, q, alpha, X, T, ldt, Y, beta=0.0, Z=None, xcols=None, m=None):
+        m = X.m if m is None else m
+        if q == 0:
+            return
+        _lib.call("pod_gemm_nn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), T, ldt,
+                  float(beta), Z.ptr if Z is not None else ctypes.c_void_p(0),
+                  Z.ld if Z is not None else 1, Y.ptr, Y.ld, self.stream)
+
+    def small_ws(self, n):
+        return self.ws("small", _lib.load().pod_small_ws_bytes(n))
+
+    def gram_eigh(self, G, ldg, g, r, sigma, T, ldt):
+        ws = self.small_ws(g)
+        _lib.call("pod_gram_eigh", G, ldg, g, r, _ptr(sigma), T, ldt, _ptr(self.info), _ptr(ws),
+                  ws.numel(), self.stream)
+
+    def cholqr_factor(self, G, ldg, l, nrows, Rinv, ldri, R, ldr):
+        ws = self.small_ws(l)
+        _lib.call("pod_cholqr_factor", G, ldg, l, nrows, Rinv, ldri, R, ldr, _ptr(self.dinfo),
+                  _ptr(ws), ws.numel(), self.stream)
+
+    def merge_core(self, sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new):
+        ws = self.small_ws(l1 + l2)
+        _lib.call("pod_merge_core", sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols,
+                  sig_new, _ptr(self.info), _ptr(ws), ws.numel(), self.stream)
+
+    def svd_small(self, A, lda, nr, nc, U, ldu, sigma, V, ldv):
+        ws = self.small_ws(max(nr, nc))
+        _lib.call("pod_svd_small", A, lda, nr, nc, U, ldu, _ptr(sigma), V, ldv, _ptr(self.info),
+                  _ptr(ws), ws.numel(), self.stream)
+
+    def small_gemm(self, p, q, k, alpha, A, lda, transa, B, ldb, beta, C, ldc):
+        _lib.call("pod_small_gemm", p, q, k, float(alpha), A, lda, int(transa), B, ldb,
+                  float(beta), C, ldc, self.stream)
+
+    def maxabs(self, A, lda, p, q, out):
+        _lib.call("pod_maxabs", A, lda, p, q, out, self.stream)
+
+    def fix_signs(self, U, l, V=None, n=0):
+        ws = self.ws("colwise", _lib.load().pod_colwise_ws_bytes(U.m, max(l, 1)))
+        _lib.call("pod_fix_signs", U.ptr, U.m, l, U.ld, V.ptr if V is not None else None, n,
+                  V.ld if V is not None else 1, None, _ptr(ws), ws.numel(), self.stream)
+
+    def coldots(self, P, Q, k, kk, take_abs, out):
+        ws = self.ws("colwise", _lib.load().pod_colwise_ws_bytes(P.m, max(k, 1)))
+        _lib.call("pod_coldots", P.ptr, P.ld, Q.ptr, Q.ld, P.m, k, kk, int(take_abs), _ptr(out),
+                  _ptr(ws), ws.numel(), self.stream)
+
+
+def dptr(t, offset_elems=0):
+    """Raw pointer into a float64/int tensor (element offset)."""
+    return ctypes.c_void_p(t.data_ptr() + t.element_size() * int(offset_elems))
+
+
+_CTX = {}
+
+
+def get_ctx(device=None):
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device available; the ISMA path runs on the GPU only")
+    key = torch.cuda.current_device() if device is None else torch.device(device).index
+    ctx = _CTX.get(key)
+    if ctx is None:
+        ctx = Ctx(torch.device("cuda", key))
+        _CTX[key] = ctx
+    return ctx
+
+
+def to_device_colmajor(a, device):
+    """Host array / torch tensor -> ColMat (column-major float64 on device).
+
+    numpy input is made Fortran-ordered float64 (as_dense semantics,
+    matcore.py:49) and copied host->device; a CUDA tensor that is already
+    column-major float64 is used in place.
+    """
+    if isinstance(a, ColMat):
+        return a
+    if isinstance(a, torch.Tensor):
+        if a.ndim != 2:
+            from .errors import ParameterError
+
+            raise ParameterError(f"expected a 2-D matrix, got ndim={a.ndim}")
+        m, n = a.shape
+        t = a.to(device=device, dtype=torch.float64)
+        if t.stride(0) == 1 and t.stride(1) == max(m, 1):
+            st = t.T  # (n, m) contiguous view
+        else:
+            st = t.T.contiguous()
+        return ColMat(st, m, n)
+    arr = np.asarray(a)
+    m, n = arr.shape
+    arr = np.asarray(arr, dtype=np.float64, order="F")
+    host = torch.from_numpy(arr.T)  # (n, m) C-contiguous view of F-order data
+    return ColMat(host.to(device), m, n)

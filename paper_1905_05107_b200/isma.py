@@ -1,0 +1,234 @@
+"""Iterative sampling and merging on the GPU -- drop-in for the reference's
+``podsketch.isma`` (isma.py:1-303), column-sampling path.
+
+Same names, arguments, defaults, validation and error classes as the
+reference: ``IsmaConfig`` (isma.py:59-119), ``IterationTrace``
+(isma.py:122-141), ``isma_run`` (isma.py:225-303), ``get_update``
+(isma.py:144-178) and ``convergence_cosines`` (isma.py:181-201).  All
+numerics run in libpodsketch_b200.so (see engine.py); the caller's numpy
+Generator supplies the uniforms, one ``rng.random(c)`` batch per round,
+so sampled index sets follow the reference's stream.
+
+Not on this path (raise NotImplementedError rather than fall back):
+row sampling (``rows=True``, ICRS) and the ``ort`` strategy -- SURVEY.md
+section 8(f) ranks them next.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+from .errors import ParameterError
+from .sampling import ctsvd_sample_count, ltsvd_sample_count
+
+STRATEGIES = ("l2n", "unf", "ort", "ls")
+CRITERIA = ("modes", "subspace")
+
+
+@dataclasses.dataclass(frozen=True)
+class IsmaConfig:
+    """Parameters of an iterative run (isma.py:59-119); r defaults to 3k."""
+
+    k: int
+    r: int | None = None
+    epsilon: float = 0.7
+    delta: float = 0.6
+    tau: float = 0.99
+    strategy: str = "unf"
+    rows: bool = False
+    criterion: str = "modes"
+    seed: int = 0
+    finalize: bool = True
+    c: int | None = None
+    w: int | None = None
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise ParameterError("k must be >= 1")
+        r = 3 * self.k if self.r is None else self.r
+        if r < self.k:
+            raise ParameterError(f"r={r} must be >= k={self.k}")
+        if not self.epsilon > 0:
+            raise ParameterError("epsilon must be > 0")
+        if not 0 < self.delta < 1:
+            raise ParameterError("delta must lie strictly between 0 and 1")
+        if not 0 <= self.tau <= 1:
+            raise ParameterError("tau must lie in [0, 1]")
+        strategy = str(self.strategy).lower()
+        if strategy not in STRATEGIES:
+            raise ParameterError(f"strategy must be one of {STRATEGIES}")
+        criterion = str(self.criterion).lower()
+        if criterion not in CRITERIA:
+            raise ParameterError(f"criterion must be one of {CRITERIA}")
+        if strategy == "ls" and not self.rows:
+            raise ParameterError("strategy 'ls' samples rows; set rows=True")
+        if strategy == "l2n" and self.rows:
+            raise ParameterError("strategy 'l2n' is column-only; rows must be False")
+        for name, val in (("c", self.c), ("w", self.w)):
+            if val is not None and val < 1:
+                raise ParameterError(f"{name} override must be >= 1")
+        object.__setattr__(self, "r", r)
+        object.__setattr__(self, "strategy", strategy)
+        object.__setattr__(self, "criterion", criterion)
+
+    def column_budget(self):
+        if self.c is not None:
+            return int(self.c)
+        return ltsvd_sample_count(self.k, self.epsilon, self.delta)
+
+    def row_budget(self):
+        if self.w is not None:
+            return int(self.w)
+        return ctsvd_sample_count(self.k, self.epsilon, self.delta)
+
+
+@dataclasses.dataclass(frozen=True)
+class IterationTrace:
+    """Diagnostics of one update round (isma.py:122-141)."""
+
+    iteration: int
+    columns_sampled: int
+    rows_sampled: int
+    remaining: int
+    cosines: np.ndarray
+    wall_time: float
+
+    def __post_init__(self):
+        cos = np.asarray(self.cosines, dtype=np.float64)
+        if cos.size and (cos.min() < -1.0 or cos.max() > 1.0):
+            raise ParameterError("cosines must lie in [-1, 1]")
+        object.__setattr__(self, "cosines", cos)
+
+
+def _require_column_path(config):
+    if config.rows:
+        raise NotImplementedError("row sampling (rows=True) is not on the B200 path yet")
+    if config.strategy not in ("l2n", "unf"):
+        raise NotImplementedError(f"strategy {config.strategy!r} is not on the B200 path yet")
+
+
+def _validate_shape(a):
+    shape = getattr(a, "shape", None)
+    if shape is None:
+        a = np.asarray(a, dtype=np.float64)
+        shape = a.shape
+    if len(shape) != 2:
+        raise ParameterError(f"expected a 2-D matrix, got ndim={len(shape)}")
+    if shape[0] == 0 or shape[1] == 0:
+        raise ParameterError("matrix must have at least one row and column")
+    return a, int(shape[0]), int(shape[1])
+
+
+def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False):
+    """Run the full iteration (isma.py:225-303) on the GPU.
+
+    ``a`` may be a numpy array (copied host->device), a CUDA torch tensor
+    or a ``device.ColMat`` (used in place).  Returns ``(TruncatedFactor,
+    list[IterationTrace])`` exactly as the reference.
+    """
+    from .device import get_ctx, to_device_colmajor
+    from .engine import IsmaEngine
+    from .matcore import TruncatedFactor
+
+    _require_column_path(config)
+    a, m, n = _validate_shape(a)
+    k = config.k
+    if k > min(m, n):
+        raise ParameterError(f"k={k} exceeds min(m, n)={min(m, n)}")
+    keep = k if keep is None else int(keep)
+    if not 1 <= keep <= config.r:
+        raise ParameterError(f"keep={keep} outside 1..r={config.r}")
+    if rng is None:
+        rng = np.random.default_rng(config.seed)
+    ctx = get_ctx(device)
+    A = to_device_colmajor(a, ctx.device)
+    eng = IsmaEngine(ctx, A, k=k, r=config.r, c=config.column_budget(),
+                     criterion=config.criterion)
+    traces, v = eng.run(rng, strategy=config.strategy, tau=config.tau,
+                        finalize=config.finalize, keep=keep, trace_cls=IterationTrace)
+    u, s, vv = eng.result(keep, v)
+    factor = TruncatedFactor(u, s, vv)
+    if return_device:
+        return factor, traces, eng
+    return factor, traces
+
+
+def get_update(a, s, u_prev, dist, c, w, rows, rng, r):
+    """One sampling round (isma.py:144-178), column path, on the GPU.
+
+    Draws ``c`` indices from ``dist`` (one ``rng.random(c)`` batch), factors
+    the distinct sampled columns through their Gram matrix and returns
+    ``(factor, remaining, g, h)``; an empty candidate set returns
+    ``(None, s, 0, 0)``.
+    """
+    import torch
+
+    from .device import get_ctx, to_device_colmajor, dptr
+    from .engine import MODE_WEIGHTS
+    from .matcore import TruncatedFactor
+
+    s = np.asarray(s, dtype=np.int64)
+    if s.size == 0:
+        return None, s, 0, 0
+    if rows:
+        raise NotImplementedError("row sampling (rows=True) is not on the B200 path yet")
+    a, m, n = _validate_shape(a)
+    ctx = get_ctx()
+    A = to_device_colmajor(a, ctx.device)
+    dev = ctx.device
+    w_dev = torch.as_tensor(dist.weights, dtype=torch.float64, device=dev)
+    npos = dist.size
+    u = np.asarray(rng.random(int(c)), dtype=np.float64)
+    uni = torch.as_tensor(u, device=dev)
+    g_cap = min(int(c), npos)
+    pos = torch.empty(g_cap, dtype=torch.int32, device=dev)
+    cnt = torch.empty(g_cap, dtype=torch.int64, device=dev)
+    ctx.draw(MODE_WEIGHTS, w_dev, None, npos, uni, int(c), pos, cnt)
+    g, _, status = ctx.read_info(3)
+    picked = dist.indices[pos[:g].cpu().numpy().astype(np.int64)]
+    idx = torch.as_tensor(picked.astype(np.int32), device=dev)
+    remaining = np.setdiff1d(s, picked, assume_unique=True)
+    G = torch.empty(g * g, dtype=torch.float64, device=dev)
+    ctx.tn(g, g, 1.0, A, A, dptr(G), g, xcols=idx, ycols=idx)
+    sig = torch.empty(g, dtype=torch.float64, device=dev)
+    T = torch.empty(g * int(r), dtype=torch.float64, device=dev)
+    ctx.gram_eigh(dptr(G), g, g, int(r), sig, dptr(T), g)
+    _, keep, _ = ctx.read_info(3)
+    if keep == 0:
+        return TruncatedFactor.empty(m), remaining, g, 0
+    from .device import ColMat
+
+    U = ColMat.zeros(m, keep, dev)
+    ctx.nn(g, keep, 1.0, A, dptr(T), g, U, xcols=idx)
+    ctx.fix_signs(U, keep)
+    return TruncatedFactor(U.to_numpy(), sig[:keep].cpu().numpy()), remaining, g, 0
+
+
+def convergence_cosines(prev, next_, k, criterion):
+    """Cosines between successive top-k approximations (isma.py:181-201),
+    computed on the GPU."""
+    import torch
+
+    from .device import ColMat, dptr, get_ctx, to_device_colmajor
+
+    if criterion not in CRITERIA:
+        raise ParameterError(f"criterion must be one of {CRITERIA}")
+    kk = min(k, prev.nmodes, next_.nmodes)
+    xi = np.zeros(k)
+    if kk == 0:
+        return xi
+    ctx = get_ctx()
+    P = to_device_colmajor(np.asfortranarray(prev.u[:, :kk]), ctx.device)
+    Q = to_device_colmajor(np.asfortranarray(next_.u[:, :kk]), ctx.device)
+    if criterion == "modes":
+        out = torch.zeros(k, dtype=torch.float64, device=ctx.device)
+        ctx.coldots(P, Q, k, kk, True, out)
+        return out.cpu().numpy()
+    C = torch.empty(kk * kk, dtype=torch.float64, device=ctx.device)
+    ctx.tn(kk, kk, 1.0, P, Q, dptr(C), kk)
+    sv = torch.empty(kk, dtype=torch.float64, device=ctx.device)
+    ctx.svd_small(dptr(C), kk, kk, kk, None, 1, sv, None, 1)
+    xi[:kk] = sv.cpu().numpy()
+    return np.clip(xi, 0.0, 1.0)
