@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark: time to converged k POD modes on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], the largest config quoted for 1 GPU):
+the config-2 snapshot matrix, m = 262144 (512 x 512 field) x n = 2000,
+fp64, k = 20, r = 3k = 60, c = 100 draws per round, strategy l2n,
+criterion "modes", tau = 1 - tol with tol = 1e-8, seed 7,
+finalize on.  Synthetic data from ``workloads.config2_torch`` generated on
+the device (outside the timed region).  A step = one full ``isma_run``
+(norm pass, bootstrap, every update round, finalize) over the resident
+matrix; A is 4.2 GB >> 126 MB L2, so no L2 flush is needed between steps.
+
+Arms:
+  default           our CUDA path (value = device-resident run, e2e = the
+                    public API on pinned host memory incl. H2D of A)
+  --impl reference  the reference algorithm on the host CPU (the numpy /
+                    LAPACK oracle port, oracle/isma_oracle.py, all cores),
+                    each step a bounded sample extrapolated to the run.
+
+One JSON line on stdout (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time to converged k POD modes (s) & achieved HBM GB/s, 1/2/4/8 B200 vs CPU ref"
+WORKLOAD = dict(side=512, n=2000, k=20, r=60, c=100, tol=1e-8, strategy="l2n",
+                criterion="modes", seed=7, data_seed=0)
+CPU_SAMPLE_ROUNDS = 3
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+FP64_DMMA_TFLOPS = 37.17  # tools/fp64_peak.cu on this pool's B200 (profiles/fp64_peak.txt)
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) during the timed region."""
+
+    def __init__(self, index=0, period=0.1):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._th = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover
+            self.nv = None
+        self.period = period
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown",
+                                               0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._th:
+            self._th.join()
+
+    def result(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_reference_sample(a_host, steps, warmup, n_rounds_full):
+    """The reference algorithm (oracle port) on the host: bootstrap + the
+    first CPU_SAMPLE_ROUNDS update rounds + finalize on the full matrix,
+    extrapolated to the full round count with the mean sampled round."""
+    from oracle import isma_oracle as orc
+
+    w = WORKLOAD
+    est = []
+    for i in range(warmup + steps):
+        out = orc.run(a_host, w["k"], r=w["r"], c=w["c"], tau=1 - w["tol"],
+                      strategy=w["strategy"], criterion=w["criterion"], seed=w["seed"],
+                      max_rounds=CPU_SAMPLE_ROUNDS)
+        tr = out["trace"]
+        t_boot = tr[0]["wall_time"]
+        rounds = [t["wall_time"] for t in tr[1:]]
+        per_round = sum(rounds) / max(len(rounds), 1)
+        full = (out["timings"]["norms"] + t_boot + per_round * (n_rounds_full - 1)
+                + out["timings"]["finalize"])
+        if i >= warmup:
+            est.append(full)
+    try:
+        from threadpoolctl import threadpool_info
+
+        threads = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    return statistics.mean(est), threads
+
+
+def run_reference_arm(args):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return 0
+    import torch
+
+    from paper_1905_05107_b200 import workloads
+
+    w = WORKLOAD
+    at = workloads.config2_torch(w["data_seed"], w["side"], w["n"], device="cpu")
+    a_host = at.numpy().T  # F-order view
+    # full round count: the l2n index stream does not depend on the factor,
+    # so replay the draws alone (cheap) to learn it
+    from oracle import isma_oracle as orc
+
+    norms2 = orc.column_norms2(a_host)
+    rng = np.random.default_rng(w["seed"])
+    s = np.arange(w["n"])
+    n_rounds = 0
+    while s.size:
+        idx, _ = orc.cdf_draw(s, orc.normalized_weights(norms2[s]), rng.random(w["c"]))
+        s = np.setdiff1d(s, idx, assume_unique=True)
+        n_rounds += 1
+    value, threads = cpu_reference_sample(a_host, args.steps, args.warmup, n_rounds)
+    del torch
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_dict(n_rounds),
+        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port",
+                         "sample": f"oracle port of podsketch isma_run on the full config-2 "
+                                   f"matrix: norm pass + bootstrap + {CPU_SAMPLE_ROUNDS} update "
+                                   f"rounds + finalize, extrapolated to {n_rounds} rounds"},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config_dict(n_rounds=None):
+    w = WORKLOAD
+    d = {"workload": "config2 snapshot field 512x512 -> m=262144, n=2000, fp64; k=20, r=60, "
+                     "c=100, l2n, modes, tau=1-1e-8, finalize",
+         "m": w["side"] ** 2, "n": w["n"], "k": w["k"], "r": w["r"], "c": w["c"],
+         "tau": 1 - w["tol"], "strategy": w["strategy"], "criterion": w["criterion"],
+         "seed": w["seed"], "l2_policy": "A is 4.2 GB >> 126 MB L2 (no flush needed)"}
+    if n_rounds is not None:
+        d["rounds"] = n_rounds
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+
+    import paper_1905_05107_b200 as pod
+    from paper_1905_05107_b200 import workloads
+    from paper_1905_05107_b200.device import KernelProfile, get_ctx, to_device_colmajor
+
+    ws, rank, local = _dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    w = WORKLOAD
+    ctx = get_ctx()
+    dev = ctx.device
+    at = workloads.config2_torch(w["data_seed"], w["side"], w["n"], device=dev)
+    m, n = at.shape[1], at.shape[0]
+    A = to_device_colmajor(at.T, dev)
+    cfg = pod.IsmaConfig(k=w["k"], r=w["r"], c=w["c"], tau=1 - w["tol"], strategy=w["strategy"],
+                         criterion=w["criterion"], seed=w["seed"])
+    stream = torch.cuda.current_stream(dev)
+
+    def one_run():
+        return pod.isma_run(A, cfg)
+
+    for _ in range(args.warmup):
+        factor, traces = one_run()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    prof = KernelProfile()
+    ctx.prof = prof
+    launches0 = ctx.launches
+    times = []
+    with ClockSampler(index=torch.cuda.current_device()) as clk:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            factor, traces = one_run()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    ctx.prof = None
+    launches = ctx.launches - launches0
+    step_s = statistics.mean(times)
+    if ws > 1:
+        t = torch.tensor([step_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_s = float(t.item())
+    kern = prof.summary()
+    n_rounds = len(traces)
+
+    # roofline of the dominant kernel (by total device time)
+    dom_name, dom = max(kern.items(), key=lambda kv: kv[1]["ms"])
+    peaks = _peaks()
+    per_launch_s = dom["ms"] / 1e3 / dom["calls"]
+    if dom["flops"] > 0 and dom_name.startswith("gemm"):
+        ach = dom["flops"] / dom["calls"] / per_launch_s / 1e12
+        roof = {"kernel": dom_name, "bound": "tensor", "achieved": ach,
+                "peak": FP64_DMMA_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_DMMA_TFLOPS,
+                "peak_source": "measured FP64 DMMA.8x8x4 peak (tools/fp64_peak.cu)"}
+    else:
+        ach = dom["bytes"] / dom["calls"] / per_launch_s / 1e9
+        pk = peaks.get("hbm_gbs", 6650.0)
+        roof = {"kernel": dom_name, "bound": "hbm", "achieved": ach, "peak": pk, "unit": "GB/s",
+                "frac": ach / pk,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks
+                else "fallback 6650 GB/s"}
+    roof["traffic"] = None
+    norm = kern.get("colnorms2")
+    hbm_norm = (norm["bytes"] / (norm["ms"] / 1e3)) / 1e9 if norm else None
+    breakdown = {k: {"ms_per_step": v["ms"] / args.steps, "calls_per_step": v["calls"] / args.steps,
+                     "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["flops"] else None,
+                     "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["bytes"] else None}
+                 for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["ms"])}
+
+    line = {
+        "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config-2 Fourier snapshot generator, on device)",
+        "config": _config_dict(n_rounds),
+        "hbm_gbs_norm_pass": hbm_norm,
+        "roofline": roof,
+        "kernels": breakdown,
+        "gpu_launches": launches,
+        "clocks": clk.result(),
+        "sigma_top3": [float(x) for x in factor.sigma[:3]],
+        "engine_stats": {k: (v if not isinstance(v, list) else
+                             {"mean": sum(v) / max(len(v), 1), "max": max(v) if v else 0})
+                         for k, v in __import__("paper_1905_05107_b200.isma", fromlist=["x"])
+                         .LAST_STATS.items()},
+    }
+
+    if rank == 0 and not args.no_e2e:
+        # public API with HOST buffers: H2D of A and D2H of the factor inside the timed region
+        host = torch.empty((n, m), dtype=torch.float64).pin_memory()
+        host.copy_(at)
+        a_host = host.numpy().T  # F-order numpy view of pinned memory
+        del at
+        torch.cuda.empty_cache()
+        e2e = []
+        for i in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            f_h, tr_h = pod.isma_run(a_host, cfg)
+            torch.cuda.synchronize()
+            if i:
+                e2e.append(time.perf_counter() - t0)
+        h2d = m * n * 8 + len(tr_h) * w["c"] * 8
+        d2h = (f_h.u.size + f_h.sigma.size + (f_h.v.size if f_h.v is not None else 0)) * 8
+        line["e2e"] = {"value": statistics.mean(e2e), "unit": "s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h}
+        if not args.no_cpu_baseline:
+            cpu_s, threads = cpu_reference_sample(a_host, 1, 0, n_rounds)
+            line["cpu_baseline"] = {
+                "value": cpu_s, "unit": "s", "cores": threads, "kind": "port",
+                "sample": f"oracle port (numpy/LAPACK) of podsketch isma_run, full config-2 "
+                          f"matrix: norm pass + bootstrap + {CPU_SAMPLE_ROUNDS} update rounds + "
+                          f"finalize, extrapolated to {n_rounds} rounds"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

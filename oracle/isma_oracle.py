@@ -232,11 +232,12 @@ def finalize(a, u):
 # --------------------------------------------------------------------------
 
 def run(a, k, *, r=None, c, tau, strategy="l2n", criterion="modes", seed=0,
-        rng=None, do_finalize=True, keep=None, monitor=False):
+        rng=None, do_finalize=True, keep=None, monitor=False, max_rounds=None):
     """isma.py:225-303 restricted to the column-only path (rows=False) with
     strategies l2n / unf.  Returns a dict with u, sigma, v (or None), and a
     per-round trace list of dicts (iteration, unique, counts, remaining,
-    cosines, wall_time[, margin])."""
+    cosines, wall_time[, margin]) plus phase timings.  ``max_rounds`` stops
+    after that many update rounds (a bounded CPU-timing sample only)."""
     if strategy not in ("l2n", "unf"):
         raise OracleParamError("oracle covers strategies l2n and unf")
     a = dense_f64(a)
@@ -249,7 +250,9 @@ def run(a, k, *, r=None, c, tau, strategy="l2n", criterion="modes", seed=0,
         raise OracleParamError("keep outside 1..r")
     if rng is None:
         rng = np.random.default_rng(seed)
+    t_start = time.perf_counter()
     norms2 = column_norms2(a)
+    t_norm = time.perf_counter() - t_start
     trace = []
 
     def one_round(s, weights):
@@ -273,6 +276,8 @@ def run(a, k, *, r=None, c, tau, strategy="l2n", criterion="modes", seed=0,
     xi = np.zeros(k)
     it = 0
     while s.size and (it == 0 or bool(np.any(xi < tau))):
+        if max_rounds is not None and it >= max_rounds:
+            break
         it += 1
         if strategy == "l2n":
             try:
@@ -289,12 +294,16 @@ def run(a, k, *, r=None, c, tau, strategy="l2n", criterion="modes", seed=0,
                     wall_time=time.perf_counter() - info.pop("t0"))
         trace.append(info)
     v = None
+    t0 = time.perf_counter()
     if do_finalize and sig.size:
         u, sig, v = finalize(a, u)
+    t_fin = time.perf_counter() - t0
     if keep < sig.size:
         u, sig = u[:, :keep].copy(), sig[:keep].copy()
         v = None if v is None else v[:, :keep].copy()
-    return {"u": u, "sigma": sig, "v": v, "trace": trace}
+    return {"u": u, "sigma": sig, "v": v, "trace": trace,
+            "timings": {"norms": t_norm, "finalize": t_fin,
+                        "total": time.perf_counter() - t_start}}
 
 
 def wedin(a, u, sigma, v, k):

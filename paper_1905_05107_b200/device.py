@@ -72,6 +72,24 @@ class Ctx:
         self.dinfo = torch.zeros(16, dtype=torch.float64, device=self.device)
         self.h_info = torch.zeros(16, dtype=torch.int64).pin_memory()
         self.h_dinfo = torch.zeros(16, dtype=torch.float64).pin_memory()
+        self.launches = 0      # kernels launched through this context
+        self.prof = None       # KernelProfile when instrumenting
+
+    def _call(self, name, nlaunch, flops, nbytes, fn, *args):
+        """Invoke one ABI entry point; count its kernel launches and, when a
+        profile is active, bracket it with CUDA events on the launch stream."""
+        self.launches += nlaunch
+        prof = self.prof
+        if prof is None:
+            _lib.call(fn, *args)
+            return
+        st = torch.cuda.current_stream(self.device)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        _lib.call(fn, *args)
+        e1.record(st)
+        prof.add(name, e0, e1, flops, nbytes, nlaunch)
 
     @property
     def stream(self):
@@ -97,12 +115,12 @@ class Ctx:
 
     # ------------------------------------------------------------ kernels
     def colnorms2(self, A, out, flag):
-        _lib.call("pod_colnorms2_f64", A.ptr, A.m, A.ncols, A.ld, _ptr(out), _ptr(flag),
+        self._call("colnorms2", 1, 2.0 * A.m * A.ncols, 8.0 * A.m * A.ncols, "pod_colnorms2_f64", A.ptr, A.m, A.ncols, A.ld, _ptr(out), _ptr(flag),
                   self.stream)
 
     def draw(self, mode, weights, live, n, uniforms, c, idx, cnt):
         ws = self.ws("draw", _lib.load().pod_draw_ws_bytes(n))
-        _lib.call("pod_draw", mode, _ptr(weights), _ptr(live), n, _ptr(uniforms), c, _ptr(idx),
+        self._call("draw", 1, 0.0, 24.0 * n + 8.0 * c, "pod_draw", mode, _ptr(weights), _ptr(live), n, _ptr(uniforms), c, _ptr(idx),
                   _ptr(cnt), _ptr(ws), ws.numel(), _ptr(self.info), self.stream)
 
     def tn(self, p, q, alpha, X, Y, C, ldc, xcols=None, ycols=None, m=None):
@@ -111,14 +129,18 @@ class Ctx:
             return
         need = _lib.load().pod_gemm_tn_ws_bytes(m, p, q)
         ws = self.ws("tn", need)
-        _lib.call("pod_gemm_tn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), Y.ptr, Y.ld,
+        sym = X.ptr.value == Y.ptr.value and (xcols is ycols)
+        flops = float(m) * p * (p + 1) if sym else 2.0 * m * p * q
+        nbytes = 8.0 * m * (p if sym else p + q)
+        self._call("gemm_tn", 2, flops, nbytes, "pod_gemm_tn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), Y.ptr, Y.ld,
                   _ptr(ycols), C, ldc, _ptr(ws), ws.numel(), self.stream)
 
     def nn(self, p, q, alpha, X, T, ldt, Y, beta=0.0, Z=None, xcols=None, m=None):
         m = X.m if m is None else m
         if q == 0:
             return
-        _lib.call("pod_gemm_nn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), T, ldt,
+        nbytes = 8.0 * m * (p + q + (q if beta != 0.0 else 0))
+        self._call("gemm_nn", 1, 2.0 * m * p * q, nbytes, "pod_gemm_nn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), T, ldt,
                   float(beta), Z.ptr if Z is not None else ctypes.c_void_p(0),
                   Z.ld if Z is not None else 1, Y.ptr, Y.ld, self.stream)
 
@@ -127,40 +149,63 @@ class Ctx:
 
     def gram_eigh(self, G, ldg, g, r, sigma, T, ldt):
         ws = self.small_ws(g)
-        _lib.call("pod_gram_eigh", G, ldg, g, r, _ptr(sigma), T, ldt, _ptr(self.info), _ptr(ws),
+        self._call("gram_eigh", 1, 0.0, 8.0 * g * g, "pod_gram_eigh", G, ldg, g, r, _ptr(sigma), T, ldt, _ptr(self.info), _ptr(ws),
                   ws.numel(), self.stream)
 
     def cholqr_factor(self, G, ldg, l, nrows, Rinv, ldri, R, ldr):
         ws = self.small_ws(l)
-        _lib.call("pod_cholqr_factor", G, ldg, l, nrows, Rinv, ldri, R, ldr, _ptr(self.dinfo),
+        self._call("cholqr_factor", 1, 0.0, 8.0 * l * l, "pod_cholqr_factor", G, ldg, l, nrows, Rinv, ldri, R, ldr, _ptr(self.dinfo),
                   _ptr(ws), ws.numel(), self.stream)
 
     def merge_core(self, sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new):
         ws = self.small_ws(l1 + l2)
-        _lib.call("pod_merge_core", sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols,
+        self._call("merge_core", 1, 0.0, 8.0 * (l1 + l2) ** 2, "pod_merge_core", sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols,
                   sig_new, _ptr(self.info), _ptr(ws), ws.numel(), self.stream)
 
     def svd_small(self, A, lda, nr, nc, U, ldu, sigma, V, ldv):
         ws = self.small_ws(max(nr, nc))
-        _lib.call("pod_svd_small", A, lda, nr, nc, U, ldu, _ptr(sigma), V, ldv, _ptr(self.info),
+        self._call("svd_small", 1, 0.0, 8.0 * nr * nc, "pod_svd_small", A, lda, nr, nc, U, ldu, _ptr(sigma), V, ldv, _ptr(self.info),
                   _ptr(ws), ws.numel(), self.stream)
 
     def small_gemm(self, p, q, k, alpha, A, lda, transa, B, ldb, beta, C, ldc):
-        _lib.call("pod_small_gemm", p, q, k, float(alpha), A, lda, int(transa), B, ldb,
+        self._call("small_gemm", 1, 2.0 * p * q * k, 0.0, "pod_small_gemm", p, q, k, float(alpha), A, lda, int(transa), B, ldb,
                   float(beta), C, ldc, self.stream)
 
     def maxabs(self, A, lda, p, q, out):
-        _lib.call("pod_maxabs", A, lda, p, q, out, self.stream)
+        self._call("maxabs", 1, 0.0, 8.0 * p * q, "pod_maxabs", A, lda, p, q, out, self.stream)
 
     def fix_signs(self, U, l, V=None, n=0):
         ws = self.ws("colwise", _lib.load().pod_colwise_ws_bytes(U.m, max(l, 1)))
-        _lib.call("pod_fix_signs", U.ptr, U.m, l, U.ld, V.ptr if V is not None else None, n,
+        self._call("fix_signs", 4 if V is not None else 3, 0.0, 16.0 * U.m * l, "pod_fix_signs", U.ptr, U.m, l, U.ld, V.ptr if V is not None else None, n,
                   V.ld if V is not None else 1, None, _ptr(ws), ws.numel(), self.stream)
 
     def coldots(self, P, Q, k, kk, take_abs, out):
         ws = self.ws("colwise", _lib.load().pod_colwise_ws_bytes(P.m, max(k, 1)))
-        _lib.call("pod_coldots", P.ptr, P.ld, Q.ptr, Q.ld, P.m, k, kk, int(take_abs), _ptr(out),
+        self._call("coldots", 2, 2.0 * P.m * kk, 16.0 * P.m * kk, "pod_coldots", P.ptr, P.ld, Q.ptr, Q.ld, P.m, k, kk, int(take_abs), _ptr(out),
                   _ptr(ws), ws.numel(), self.stream)
+
+
+class KernelProfile:
+    """Per-kernel CUDA-event timings with algorithmic flop/byte counts."""
+
+    def __init__(self):
+        self.events = []
+
+    def add(self, name, e0, e1, flops, nbytes, nlaunch):
+        self.events.append((name, e0, e1, float(flops), float(nbytes), int(nlaunch)))
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for name, e0, e1, fl, by, nl in self.events:
+            d = out.setdefault(name, {"calls": 0, "launches": 0, "ms": 0.0, "flops": 0.0,
+                                      "bytes": 0.0})
+            d["calls"] += 1
+            d["launches"] += nl
+            d["ms"] += e0.elapsed_time(e1)
+            d["flops"] += fl
+            d["bytes"] += by
+        return out
 
 
 def dptr(t, offset_elems=0):

@@ -142,7 +142,8 @@ class MergeWorkspace:
         ctx.merge_core(dptr(self.sig[self.cur]), l1, dptr(self.M), r, dptr(self.Rt), r,
                        dptr(self.sig_upd), l2, r, r, dptr(self.Tm), 2 * r, r,
                        dptr(self.sig[nxt]))                               # merge.py:80-85
-        keep = ctx.read_info(2)[0]
+        keep, sweeps = ctx.read_info(2)
+        self.stats.setdefault("merge_sweeps", []).append(sweeps)
         ctx.nn(r + l2, keep, 1.0, S, dptr(self.Tm), 2 * r, Snext.cols(0, keep))  # merge.py:86-88
         return nxt, keep
 
@@ -213,7 +214,8 @@ class IsmaEngine(MergeWorkspace):
         ctx, A = self.ctx, self.A
         ctx.tn(g, g, 1.0, A, A, dptr(self.G), g, xcols=self.idx, ycols=self.idx)
         ctx.gram_eigh(dptr(self.G), g, g, self.r, self.sig_upd, dptr(self.Tl), g)
-        rank, keep, _ = ctx.read_info(3)
+        rank, keep, sweeps = ctx.read_info(3)
+        self.stats.setdefault("eigh_sweeps", []).append(sweeps)
         if keep > 0:
             ctx.nn(g, keep, 1.0, A, dptr(self.Tl), g, dest, xcols=self.idx)
         return g, rem, keep

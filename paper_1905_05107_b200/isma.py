@@ -24,6 +24,7 @@ from .errors import ParameterError
 from .sampling import ctsvd_sample_count, ltsvd_sample_count
 
 STRATEGIES = ("l2n", "unf", "ort", "ls")
+LAST_STATS = {}  # engine statistics of the most recent isma_run (diagnostics)
 CRITERIA = ("modes", "subspace")
 
 
@@ -110,6 +111,12 @@ def _require_column_path(config):
 
 
 def _validate_shape(a):
+    from .device import ColMat
+
+    if isinstance(a, ColMat):
+        if a.m == 0 or a.ncols == 0:
+            raise ParameterError("matrix must have at least one row and column")
+        return a, a.m, a.ncols
     shape = getattr(a, "shape", None)
     if shape is None:
         a = np.asarray(a, dtype=np.float64)
@@ -150,6 +157,8 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
                         finalize=config.finalize, keep=keep, trace_cls=IterationTrace)
     u, s, vv = eng.result(keep, v)
     factor = TruncatedFactor(u, s, vv)
+    global LAST_STATS
+    LAST_STATS = eng.stats
     if return_device:
         return factor, traces, eng
     return factor, traces
