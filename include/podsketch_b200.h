@@ -57,30 +57,41 @@ int pod_colnorms2_f64(const double* A, int64_t m, int64_t n, int64_t lda, double
  * over positions 0..n-1 (a Distribution's weights, no live mask) -- and the
  * candidate-set update isma.py:164 (drawn columns cleared in `live`).
  * `uniforms` holds the c variates of ONE rng.random(c) batch.
- * Outputs: idx_out[0..g) ascending int32, cnt_out[0..g) int64,
+ * Outputs: idx_out[0..g) ascending int32 (idx_out[g..cap) = -1: zero-column
+ * padding for the gathered GEMMs), cnt_out[0..g) int64,
  * info[0] = g, info[1] = |S| after the draw, info[2] = status
  * (0 ok, 1 empty S, 2 all weights zero -> DegenerateDistributionError). */
 size_t pod_draw_ws_bytes(int64_t n);
 int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n, const double* uniforms,
-             int64_t c, int32_t* idx_out, int64_t* cnt_out, void* ws, size_t ws_bytes,
-             int64_t* info, void* stream);
+             int64_t c, int32_t* idx_out, int64_t* cnt_out, int64_t cap, void* ws,
+             size_t ws_bytes, int64_t* info, void* stream);
 
-/* C (p x q) = alpha X^T Y, X m x p, Y m x q, K = m split across CTAs with
+/* Gates: every compute entry point below that takes `gate` (device int32,
+ * nullable) does nothing when *gate == 0, so a round's launch sequence is
+ * static (capturable in a CUDA graph) while data-dependent branches of the
+ * reference -- extra CholeskyQR passes, the merge.py:73 second projection --
+ * are decided on the device.  Column index -1 in a gather list denotes a
+ * zero column (capacity padding of the sampled block).
+ *
+ * C (p x q) = alpha X^T Y, X m x p, Y m x q, K = m split across CTAs with
  * a fixed-order reduction (deterministic).  FP64 DMMA.8x8x4.
  * Replaces: baselines.py:43 (D^T D), merge.py:65 (U1^T U2), merge.py:72/75
  * (U1^T Q), isma.py:296 (A^T U), quality.py:104-105 partial products. */
 size_t pod_gemm_tn_ws_bytes(int64_t m, int64_t p, int64_t q);
 int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X, int64_t ldx,
                     const int32_t* xcols, const double* Y, int64_t ldy, const int32_t* ycols,
-                    double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+                    double* C, int64_t ldc, void* ws, size_t ws_bytes, const int32_t* gate,
+                    void* stream);
 
 /* Y (m x q) = alpha X T + beta Z, X m x p (optionally column-gathered),
- * T p x q small.  FP64 DMMA.8x8x4.  Y may alias X when q <= 64.
+ * T p x q small, q <= 192.  FP64 DMMA.8x8x4.  One CTA owns all q output
+ * columns of its rows, so Y may alias X or Z (in-place updates).
  * Replaces: baselines.py:62-63 (D V / sigma), merge.py:69 (U2 - U1 M),
  * merge.py:86-88 ([U1 Q] U_E), isma.py:298-299 (U V_R, Q U_R). */
 int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X, int64_t ldx,
                     const int32_t* xcols, const double* T, int64_t ldt, double beta,
-                    const double* Z, int64_t ldz, double* Y, int64_t ldy, void* stream);
+                    const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* gate,
+                    void* stream);
 
 /* Workspace (bytes) sufficient for any small solve of dimension <= n. */
 size_t pod_small_ws_bytes(int64_t n);
@@ -99,15 +110,20 @@ int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r, double* si
  * and W = Q R.  Column-scaled, shifted on breakdown, exactly-zero columns
  * dropped (zero R rows).  Replaces the Householder QR of merge.py:70,76 and
  * matcore.py:209.  dinfo[0] = max |D^-1 G D^-1 - I| (input defect),
- * dinfo[1] = shift attempts, dinfo[2] = dropped columns, dinfo[3] = shift. */
+ * dinfo[1] = shift attempts, dinfo[2] = dropped columns, dinfo[3] = shift.
+ * Runs iff gate_in is null or *gate_in != 0; gate_out (nullable) receives
+ * whether ANOTHER pass is needed: 1 after a first pass, else
+ * (ran && (defect > 1e-4 || shifted)). */
 int pod_cholqr_factor(const double* G, int64_t ldg, int64_t l, int64_t nrows, double* Rinv,
                       int64_t ldri, double* R, int64_t ldr, double* dinfo, void* ws,
-                      size_t ws_bytes, void* stream);
+                      size_t ws_bytes, const int32_t* gate_in, int32_t* gate_out, int first_pass,
+                      void* stream);
 
 /* Merge core (merge.py:80-88): E = [[diag sig1, M diag sig2],[0, R diag sig2]],
  * its SVD, keep = min(r, #sigma_E > 1e-14 max(sigma_E0, 1e-300)), and the
  * rotation T ((rcap + l2) x tcols, ld ldt) mapping the stacked basis
- * [U1 | 0-pad to rcap | Q] onto the merged left vectors.  info[0] = keep. */
+ * [U1 | 0-pad to rcap | Q] onto the merged left vectors.  info[0] = keep,
+ * info[1] = Jacobi sweeps; sig_new[0..rcap) = merged sigma, zero beyond keep. */
 int pod_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
                    int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
                    int64_t ldt, int64_t tcols, double* sig_new, int64_t* info, void* ws,
@@ -121,13 +137,20 @@ int pod_svd_small(const double* A, int64_t lda, int64_t nr, int64_t nc, double* 
                   double* sigma, double* V, int64_t ldv, int64_t* info, void* ws, size_t ws_bytes,
                   void* stream);
 
-/* C (p x q) = alpha op(A) B + beta C for small matrices (op = A or A^T). */
+/* C (p x q) = alpha op(A) B + beta C for small matrices (op = A or A^T).
+ * C must not alias A or B. */
 int pod_small_gemm(int64_t p, int64_t q, int64_t k, double alpha, const double* A, int64_t lda,
                    int transa, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
-                   void* stream);
+                   const int32_t* gate, void* stream);
 
-/* out[0] = max |A| over a p x q block (merge.py:72 leak test). */
-int pod_maxabs(const double* A, int64_t lda, int64_t p, int64_t q, double* out, void* stream);
+/* Copy a p x q block (ld_src -> ld_dst), gated. */
+int pod_small_copy(int64_t p, int64_t q, const double* src, int64_t lds, double* dst, int64_t ldd,
+                   const int32_t* gate, void* stream);
+
+/* out[0] = max |A| over a p x q block and gate_out = (max > thr)
+ * (merge.py:72 leak test with thr = 1e-8). */
+int pod_maxabs(const double* A, int64_t lda, int64_t p, int64_t q, double thr, double* out,
+               int32_t* gate_out, void* stream);
 
 /* fix_signs (matcore.py:148-165): per column, the first entry of largest
  * magnitude is made positive; V (n x l) flipped alongside when non-null.

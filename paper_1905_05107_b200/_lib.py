@@ -35,21 +35,23 @@ SIGNATURES = {
     "pod_last_error": (ctypes.c_char_p, []),
     "pod_colnorms2_f64": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "pod_draw_ws_bytes": (_sz, [_i64]),
-    "pod_draw": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "pod_draw": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp, _vp]),
     "pod_gemm_tn_ws_bytes": (_sz, [_i64, _i64, _i64]),
     "pod_gemm_tn_f64": (_i32, [_i64, _i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
-                               _vp, _sz, _vp]),
+                               _vp, _sz, _vp, _vp]),
     "pod_gemm_nn_f64": (_i32, [_i64, _i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _f64, _vp, _i64,
-                               _vp, _i64, _vp]),
+                               _vp, _i64, _vp, _vp]),
     "pod_small_ws_bytes": (_sz, [_i64]),
     "pod_gram_eigh": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
-    "pod_cholqr_factor": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp]),
+    "pod_cholqr_factor": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp,
+                                 _vp, _i32, _vp]),
     "pod_merge_core": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64,
                               _i64, _vp, _vp, _vp, _sz, _vp]),
     "pod_svd_small": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "pod_small_gemm": (_i32, [_i64, _i64, _i64, _f64, _vp, _i64, _i32, _vp, _i64, _f64, _vp, _i64,
-                              _vp]),
-    "pod_maxabs": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp]),
+                              _vp, _vp]),
+    "pod_small_copy": (_i32, [_i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
+    "pod_maxabs": (_i32, [_vp, _i64, _i64, _i64, _f64, _vp, _vp, _vp]),
     "pod_colwise_ws_bytes": (_sz, [_i64, _i64]),
     "pod_fix_signs": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
     "pod_coldots": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _sz, _vp]),

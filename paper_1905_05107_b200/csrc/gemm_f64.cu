@@ -37,7 +37,9 @@ __device__ __forceinline__ const double* colptr(const double* base, int64_t ld,
 __global__ void __launch_bounds__(THREADS) partial_kernel(
     int64_t m, int p, int q, const double* __restrict__ X, int64_t ldx,
     const int32_t* __restrict__ xcols, const double* __restrict__ Y, int64_t ldy,
-    const int32_t* __restrict__ ycols, int64_t rows_per_split, double* __restrict__ ws) {
+    const int32_t* __restrict__ ycols, int64_t rows_per_split, double* __restrict__ ws,
+    const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   extern __shared__ __align__(16) double smem[];
   const int tiles_p = (p + BP - 1) / BP;
   const int tp = blockIdx.x % tiles_p, tq = blockIdx.x / tiles_p;
@@ -54,8 +56,8 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
   for (int i = 0; i < 8; ++i) {
     int cx = tp * BP + warp + 8 * i;
     int cy = tq * BQ + warp + 8 * i;
-    xv[i] = cx < p;
-    yv[i] = cy < q;
+    xv[i] = cx < p && (!xcols || xcols[cx] >= 0);  // index -1: zero column (padding)
+    yv[i] = cy < q && (!ycols || ycols[cy] >= 0);
     xp[i] = xv[i] ? colptr(X, ldx, xcols, cx) : X;
     yp[i] = yv[i] ? colptr(Y, ldy, ycols, cy) : Y;
   }
@@ -126,7 +128,8 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
 }
 
 __global__ void reduce_kernel(int nsplit, int p, int q, double alpha, const double* __restrict__ ws,
-                              double* __restrict__ C, int64_t ldc) {
+                              double* __restrict__ C, int64_t ldc, const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   const int64_t total = (int64_t)p * q;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -158,54 +161,73 @@ inline Plan plan(int64_t m, int64_t p, int64_t q) {
 }  // namespace tn
 
 // ---------------------------------------------------------------- NN ------
+// One CTA owns BM rows x ALL q (<= BN) output columns, so Y may alias X or Z
+// (each CTA reads its own rows completely before writing them).
 namespace nn {
-constexpr int BM = 128, BN = 64, BK = 16;
-constexpr int LDX = BM + 4;  // % 16 == 4
+constexpr int BK = 16;
 constexpr int LDT = BK + 4;  // % 16 == 4
 constexpr int THREADS = 256;
 constexpr int STAGES = 3;
-constexpr int XT = BK * LDX, TT = BN * LDT;
-constexpr size_t SMEM = size_t(STAGES) * (XT + TT) * sizeof(double);
 
+template <int BN>
+struct Cfg {
+  static constexpr int BM = (BN == 64) ? 128 : 64;
+  static constexpr int WM = BM / 32;         // warps along M (32 rows each)
+  static constexpr int WN = 8 / WM;          // warps along N
+  static constexpr int FN = BN / WN / 8;     // 8-col fragments per warp
+  static constexpr int LDX = BM + 4;         // % 16 == 4
+  static constexpr int XT = BK * LDX, TT = BN * LDT;
+  static constexpr size_t SMEM = size_t(STAGES) * (XT + TT) * sizeof(double);
+};
+
+template <int BN>
 __global__ void __launch_bounds__(THREADS) kernel(
-    int64_t m, int p, int q, double alpha, const double* __restrict__ X, int64_t ldx,
+    int64_t m, int p, int q, double alpha, const double* X, int64_t ldx,
     const int32_t* __restrict__ xcols, const double* __restrict__ T, int64_t ldt, double beta,
-    const double* Z, int64_t ldz, double* Y, int64_t ldy) {
+    const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* __restrict__ gate) {
+  using C = Cfg<BN>;
+  if (gate && *gate == 0) return;
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row0 = (int64_t)blockIdx.x * BM;
-  const int col0 = blockIdx.y * BN;
-  const int64_t lrow = row0 + (warp & 3) * 32 + lane;  // this thread's load row
+  const int64_t row0 = (int64_t)blockIdx.x * C::BM;
+  // loader: 256 threads cover BM rows x BK cols of X
+  constexpr int RGROUPS = C::BM / 32;          // row groups of 32
+  constexpr int CPT = BK / (8 / RGROUPS);      // columns per thread
+  const int lrg = warp % RGROUPS, lcg = warp / RGROUPS;
+  const int64_t lrow = row0 + lrg * 32 + lane;
   const bool lrv = lrow < m;
-  const int lc0 = (warp >> 2) * 8;  // first of 8 columns this thread loads per stage
 
   auto load_stage = [&](int st, int k0) {
-    double* xs = smem + (size_t)st * (XT + TT);
-    double* ts = xs + XT;
+    double* xs = smem + (size_t)st * (C::XT + C::TT);
+    double* ts = xs + C::XT;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int c = k0 + lc0 + i;
-      const bool v = lrv && c < p;
-      const double* src = v ? X + (xcols ? (int64_t)xcols[c] : (int64_t)c) * ldx + lrow : X;
-      cp_async8(xs + (lc0 + i) * LDX + (warp & 3) * 32 + lane, src, v);
+    for (int i = 0; i < CPT; ++i) {
+      const int cl = lcg * CPT + i;
+      const int c = k0 + cl;
+      bool v = lrv && c < p;
+      int64_t col = c;
+      if (v && xcols) {
+        col = xcols[c];
+        v = col >= 0;  // index -1: zero column
+      }
+      const double* src = v ? X + col * ldx + lrow : X;
+      cp_async8(xs + cl * C::LDX + lrg * 32 + lane, src, v);
     }
-    // T chunk: rows k0..k0+BK, cols col0..col0+BN; thread -> (j = tid/4, k = (tid%4)*4 + e)
-    const int j = threadIdx.x >> 2;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int k = (threadIdx.x & 3) * 4 + e;
-      const bool v = (col0 + j) < q && (k0 + k) < p;
-      const double* src = v ? T + (k0 + k) + (int64_t)(col0 + j) * ldt : T;
+    // T chunk: rows k0..k0+BK, cols 0..BN
+    for (int e = threadIdx.x; e < BN * BK; e += THREADS) {
+      const int j = e / BK, k = e % BK;
+      const bool v = j < q && (k0 + k) < p;
+      const double* src = v ? T + (k0 + k) + (int64_t)j * ldt : T;
       cp_async8(ts + j * LDT + k, src, v);
     }
   };
 
-  const int wm = warp & 3, wn = warp >> 2;  // warp tile: 32 rows x 32 cols
-  double acc[4][4][2];
+  const int wm = warp % C::WM, wn = warp / C::WM;
+  double acc[4][C::FN][2];
 #pragma unroll
   for (int f = 0; f < 4; ++f)
 #pragma unroll
-    for (int g = 0; g < 4; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+    for (int g = 0; g < C::FN; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
 
   const int nkb = (p + BK - 1) / BK;
 #pragma unroll
@@ -219,21 +241,21 @@ __global__ void __launch_bounds__(THREADS) kernel(
     cp_async_commit();
     cp_async_wait<STAGES - 1>();
     __syncthreads();
-    const double* xs = smem + (size_t)(kb % STAGES) * (XT + TT);
-    const double* ts = xs + XT;
+    const double* xs = smem + (size_t)(kb % STAGES) * (C::XT + C::TT);
+    const double* ts = xs + C::XT;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
-      double a[4], b[4];
+      double a[4], b[C::FN];
 #pragma unroll
       for (int f = 0; f < 4; ++f)
-        a[f] = xs[(kk * 4 + (lane & 3)) * LDX + wm * 32 + f * 8 + (lane >> 2)];
+        a[f] = xs[(kk * 4 + (lane & 3)) * C::LDX + wm * 32 + f * 8 + (lane >> 2)];
 #pragma unroll
-      for (int g = 0; g < 4; ++g)
-        b[g] = ts[(wn * 32 + g * 8 + (lane >> 2)) * LDT + kk * 4 + (lane & 3)];
+      for (int g = 0; g < C::FN; ++g)
+        b[g] = ts[(wn * (BN / C::WN) + g * 8 + (lane >> 2)) * LDT + kk * 4 + (lane & 3)];
 #pragma unroll
       for (int f = 0; f < 4; ++f)
 #pragma unroll
-        for (int g = 0; g < 4; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
+        for (int g = 0; g < C::FN; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
     }
     __syncthreads();
   }
@@ -244,10 +266,10 @@ __global__ void __launch_bounds__(THREADS) kernel(
     const int64_t i = row0 + wm * 32 + f * 8 + (lane >> 2);
     if (i >= m) continue;
 #pragma unroll
-    for (int g = 0; g < 4; ++g)
+    for (int g = 0; g < C::FN; ++g)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int j = col0 + wn * 32 + g * 8 + 2 * (lane & 3) + e;
+        const int j = wn * (BN / C::WN) + g * 8 + 2 * (lane & 3) + e;
         if (j < q) {
           double v = alpha * acc[f][g][e];
           if (beta != 0.0) v += beta * Z[i + (int64_t)j * ldz];
@@ -264,7 +286,14 @@ static int ensure_attrs() {
   cudaError_t e = cudaFuncSetAttribute(tn::partial_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tn::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "tn attr");
-  e = cudaFuncSetAttribute(nn::kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nn::SMEM);
+  e = cudaFuncSetAttribute(nn::kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)nn::Cfg<64>::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "nn attr");
+  e = cudaFuncSetAttribute(nn::kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)nn::Cfg<128>::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "nn attr");
+  e = cudaFuncSetAttribute(nn::kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)nn::Cfg<192>::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "nn attr");
   g_attr_done = true;
   return POD_OK;
@@ -283,18 +312,12 @@ extern "C" size_t pod_gemm_tn_ws_bytes(int64_t m, int64_t p, int64_t q) {
 extern "C" int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
                                int64_t ldx, const int32_t* xcols, const double* Y, int64_t ldy,
                                const int32_t* ycols, double* C, int64_t ldc, void* ws,
-                               size_t ws_bytes, void* stream) {
+                               size_t ws_bytes, const int32_t* gate, void* stream) {
   POD_REQUIRE(m >= 0 && p >= 0 && q >= 0, "pod_gemm_tn_f64: negative size");
   POD_REQUIRE(ldc >= p, "pod_gemm_tn_f64: ldc < p");
   if (p == 0 || q == 0) return POD_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (m == 0) {
-    for (int64_t j = 0; j < q; ++j) {
-      cudaError_t e = cudaMemsetAsync(C + j * ldc, 0, p * sizeof(double), s);
-      if (e != cudaSuccess) return cuda_status(e, "tn memset");
-    }
-    return POD_OK;
-  }
+  POD_REQUIRE(m > 0, "pod_gemm_tn_f64: m must be >= 1");
   int st = ensure_attrs();
   if (st) return st;
   tn::Plan pl = tn::plan(m, p, q);
@@ -303,12 +326,13 @@ extern "C" int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
               (size_t)pl.splits * p * q * sizeof(double));
   dim3 grid(pl.tiles, pl.splits);
   tn::partial_kernel<<<grid, tn::THREADS, tn::SMEM, s>>>(m, (int)p, (int)q, X, ldx, xcols, Y, ldy,
-                                                         ycols, pl.rows_per_split, (double*)ws);
+                                                         ycols, pl.rows_per_split, (double*)ws,
+                                                         gate);
   POD_CHECK_LAUNCH("tn partial");
   int64_t tot = p * q;
   int blocks = (int)std::min<int64_t>(ceil_div(tot, 256), 4 * 148);
   tn::reduce_kernel<<<blocks, 256, 0, s>>>(pl.splits, (int)p, (int)q, alpha, (const double*)ws, C,
-                                           ldc);
+                                           ldc, gate);
   POD_CHECK_LAUNCH("tn reduce");
   return POD_OK;
 }
@@ -316,19 +340,29 @@ extern "C" int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
 extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
                                int64_t ldx, const int32_t* xcols, const double* T, int64_t ldt,
                                double beta, const double* Z, int64_t ldz, double* Y, int64_t ldy,
-                               void* stream) {
+                               const int32_t* gate, void* stream) {
   POD_REQUIRE(m >= 0 && p >= 0 && q >= 0, "pod_gemm_nn_f64: negative size");
   if (m == 0 || q == 0) return POD_OK;
   POD_REQUIRE(ldy >= m, "pod_gemm_nn_f64: ldy < m");
+  POD_REQUIRE(q <= 192, "pod_gemm_nn_f64: q=%lld > 192 output columns", (long long)q);
   POD_REQUIRE(beta == 0.0 || Z != nullptr, "pod_gemm_nn_f64: beta != 0 needs Z");
-  const bool aliased = (Y == X) || (Y == Z && Z != nullptr && ldz != ldy);
-  POD_REQUIRE(!(Y == X && q > nn::BN), "pod_gemm_nn_f64: in-place needs q <= %d", nn::BN);
-  (void)aliased;
   int st = ensure_attrs();
   if (st) return st;
-  dim3 grid((unsigned)ceil_div(m, nn::BM), (unsigned)ceil_div(q, nn::BN));
-  nn::kernel<<<grid, nn::THREADS, nn::SMEM, (cudaStream_t)stream>>>(
-      m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (q <= 64) {
+    dim3 grid((unsigned)ceil_div(m, nn::Cfg<64>::BM));
+    nn::kernel<64><<<grid, nn::THREADS, nn::Cfg<64>::SMEM, s>>>(m, (int)p, (int)q, alpha, X, ldx,
+                                                               xcols, T, ldt, beta, Z, ldz, Y, ldy,
+                                                               gate);
+  } else if (q <= 128) {
+    dim3 grid((unsigned)ceil_div(m, nn::Cfg<128>::BM));
+    nn::kernel<128><<<grid, nn::THREADS, nn::Cfg<128>::SMEM, s>>>(
+        m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate);
+  } else {
+    dim3 grid((unsigned)ceil_div(m, nn::Cfg<192>::BM));
+    nn::kernel<192><<<grid, nn::THREADS, nn::Cfg<192>::SMEM, s>>>(
+        m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate);
+  }
   POD_CHECK_LAUNCH("nn");
   return POD_OK;
 }

@@ -126,8 +126,8 @@ __device__ int64_t block_excl_scan_i64(int64_t v, int64_t* sh, int64_t* total) {
 __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
     int mode, const double* __restrict__ raw, uint8_t* __restrict__ live, int64_t n,
     const double* __restrict__ uni, int64_t c, int32_t* __restrict__ idx_out,
-    int64_t* __restrict__ cnt_out, double* __restrict__ cum, int32_t* __restrict__ counts,
-    int64_t* __restrict__ info) {
+    int64_t* __restrict__ cnt_out, int64_t cap, double* __restrict__ cum,
+    int32_t* __restrict__ counts, int64_t* __restrict__ info) {
   __shared__ double shd[DRAW_THREADS + 1];
   __shared__ int64_t shi[DRAW_THREADS + 1];
   __shared__ double red[32];
@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
   int64_t nlive = 0;
   (void)block_excl_scan_i64(nlive_local, shi, &nlive);
   if (nlive == 0) {
+    for (int64_t j = t; j < cap; j += DRAW_THREADS) idx_out[j] = -1;
     if (t == 0) { info[0] = 0; info[1] = 0; info[2] = 1; }  // status 1: empty S
     return;
   }
@@ -156,8 +157,10 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
     loc += w;
   }
   double total = block_sum(loc, red);
+  if (mode == 2) total = 1.0;  // a Distribution's weights are used as given (sampling.py:214)
   if (mode == 0) {
     if (!(total > 0.0)) {
+      for (int64_t j = t; j < cap; j += DRAW_THREADS) idx_out[j] = -1;
       if (t == 0) { info[0] = 0; info[1] = nlive; info[2] = 2; }  // status 2: degenerate
       return;
     }
@@ -212,6 +215,7 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
       if (mode != 2) live[j] = 0;
     }
   }
+  for (int64_t j = g + t; j < cap; j += DRAW_THREADS) idx_out[j] = -1;  // zero-column padding
   if (t == 0) { info[0] = g; info[1] = nlive - g; info[2] = 0; }
 }
 
@@ -247,17 +251,20 @@ extern "C" size_t pod_draw_ws_bytes(int64_t n) {
 
 extern "C" int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n,
                         const double* uniforms, int64_t c, int32_t* idx_out, int64_t* cnt_out,
-                        void* ws, size_t ws_bytes, int64_t* info, void* stream) {
+                        int64_t cap, void* ws, size_t ws_bytes, int64_t* info, void* stream) {
   POD_REQUIRE(mode >= 0 && mode <= 2, "pod_draw: bad mode %d", mode);
   POD_REQUIRE(n > 0 && n < (int64_t)INT32_MAX, "pod_draw: bad n");
   POD_REQUIRE(c >= 1, "sample count must be >= 1");
   POD_REQUIRE(ws_bytes >= pod_draw_ws_bytes(n), "pod_draw: workspace too small");
+  POD_REQUIRE(cap >= std::min<int64_t>(c, n), "pod_draw: output capacity %lld < min(c, n)",
+              (long long)cap);
   POD_REQUIRE(mode == 1 || weights != nullptr, "pod_draw: weights required");
   POD_REQUIRE(mode == 2 || live != nullptr, "pod_draw: live mask required");
   double* cum = (double*)ws;
   int32_t* counts = (int32_t*)(cum + n);
   draw_kernel<<<1, DRAW_THREADS, 0, (cudaStream_t)stream>>>(mode, weights, live, n, uniforms, c,
-                                                              idx_out, cnt_out, cum, counts, info);
+                                                              idx_out, cnt_out, cap, cum, counts,
+                                                              info);
   POD_CHECK_LAUNCH("draw");
   return POD_OK;
 }

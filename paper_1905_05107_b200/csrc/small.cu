@@ -438,7 +438,12 @@ template <bool SMEM>
 __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
     const double* __restrict__ G, int64_t ldg, int l, double nrows, double* __restrict__ Rinv,
     int64_t ldri, double* __restrict__ R, int64_t ldr, double* __restrict__ dinfo, double* gws,
-    int use_smem) {
+    int use_smem, const int32_t* __restrict__ gate_in, int32_t* __restrict__ gate_out,
+    int first_pass) {
+  if (gate_in && *gate_in == 0) {
+    if (gate_out && threadIdx.x == 0) *gate_out = 0;
+    return;
+  }
   extern __shared__ __align__(16) double sm[];
   double* H = SMEM ? sm : gws;        // scaled Gram (l x l)
   double* C = H + (size_t)l * l;       // Cholesky factor workspace
@@ -533,6 +538,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
     dinfo[1] = (double)attempt;
     dinfo[2] = (double)ndead;
     dinfo[3] = shift;
+    if (gate_out) *gate_out = first_pass ? 1 : ((s_defect > 1e-4 || attempt > 0) ? 1 : 0);
   }
 }
 
@@ -579,7 +585,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) merge_core_kernel(
   }
   __syncthreads();
   const int keep = s_keep;
-  for (int k = threadIdx.x; k < keep; k += blockDim.x) sig_new[k] = nrm[perm[k]];
+  for (int k = threadIdx.x; k < rcap; k += blockDim.x) sig_new[k] = (k < keep) ? nrm[perm[k]] : 0.0;
   // T rows follow the stack layout [U1 (rcap cols) | Q (l2 cols)]
   const int trows = rcap + l2;
   for (int64_t t = threadIdx.x; t < (int64_t)trows * tcols; t += blockDim.x) {
@@ -640,7 +646,9 @@ __global__ void __launch_bounds__(SMALL_THREADS) svd_small_kernel(
 // C (p x q) = alpha * op(A) B + beta * C, op(A) = A (p x k) or A^T (A is k x p)
 __global__ void small_gemm_kernel(int p, int q, int k, double alpha, const double* __restrict__ A,
                                   int64_t lda, int transa, const double* __restrict__ B,
-                                  int64_t ldb, double beta, double* C, int64_t ldc) {
+                                  int64_t ldb, double beta, double* C, int64_t ldc,
+                                  const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   const int64_t tot = (int64_t)p * q;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -656,8 +664,20 @@ __global__ void small_gemm_kernel(int p, int q, int k, double alpha, const doubl
   }
 }
 
-__global__ void maxabs_kernel(const double* __restrict__ A, int64_t lda, int p, int q,
-                              double* __restrict__ out) {
+__global__ void small_copy_kernel(int p, int q, const double* __restrict__ src, int64_t lds,
+                                  double* __restrict__ dst, int64_t ldd,
+                                  const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
+  const int64_t tot = (int64_t)p * q;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(t / p), i = (int)(t - (int64_t)j * p);
+    dst[i + (int64_t)j * ldd] = src[i + (int64_t)j * lds];
+  }
+}
+
+__global__ void maxabs_kernel(const double* __restrict__ A, int64_t lda, int p, int q, double thr,
+                              double* __restrict__ out, int32_t* __restrict__ gate_out) {
   __shared__ double red[32];
   double v = 0.0;
   for (int64_t t = threadIdx.x; t < (int64_t)p * q; t += blockDim.x) {
@@ -670,13 +690,30 @@ __global__ void maxabs_kernel(const double* __restrict__ A, int64_t lda, int p, 
   if (threadIdx.x < 32) {
     v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
     v = warp_max(v);
-    if (threadIdx.x == 0) out[0] = v;
+    if (threadIdx.x == 0) {
+      if (out) out[0] = v;
+      if (gate_out) *gate_out = (v > thr) ? 1 : 0;
+    }
   }
 }
 
+// Raise a kernel's dynamic shared-memory limit once to the maximum any call
+// needs (kept host-side so launches inside CUDA-graph capture make no
+// attribute calls).
 static int set_smem(const void* fn, size_t bytes) {
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  return e == cudaSuccess ? POD_OK : cuda_status(e, "small smem attr");
+  static const void* fns[16];
+  static size_t done[16];
+  static int nf = 0;
+  int i = 0;
+  for (; i < nf; ++i)
+    if (fns[i] == fn) break;
+  if (i < nf && done[i] >= bytes) return POD_OK;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)SMALL_SMEM_CAP);
+  if (e != cudaSuccess) return cuda_status(e, "small smem attr");
+  if (i == nf && nf < 16) { fns[nf] = fn; ++nf; }
+  if (i < 16) done[i] = SMALL_SMEM_CAP;
+  return POD_OK;
 }
 
 }  // namespace pod
@@ -720,7 +757,8 @@ extern "C" int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r,
 
 extern "C" int pod_cholqr_factor(const double* G, int64_t ldg, int64_t l, int64_t nrows,
                                  double* Rinv, int64_t ldri, double* R, int64_t ldr, double* dinfo,
-                                 void* ws, size_t ws_bytes, void* stream) {
+                                 void* ws, size_t ws_bytes, const int32_t* gate_in,
+                                 int32_t* gate_out, int first_pass, void* stream) {
   POD_REQUIRE(l >= 1 && ldg >= l && ldri >= l && ldr >= l, "pod_cholqr_factor: bad shape");
   const size_t bytes = cholqr_bytes(l);
   const int use_smem = bytes <= SMALL_SMEM_CAP;
@@ -728,10 +766,12 @@ extern "C" int pod_cholqr_factor(const double* G, int64_t ldg, int64_t l, int64_
   if (use_smem) { int st = set_smem((const void*)cholqr_kernel<true>, bytes); if (st) return st; }
   if (use_smem)
     cholqr_kernel<true><<<1, SMALL_THREADS, use_smem ? bytes : 0, (cudaStream_t)stream>>>(
-      G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr, dinfo, (double*)ws, use_smem);
+      G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr, dinfo, (double*)ws, use_smem, gate_in,
+      gate_out, first_pass);
   else
     cholqr_kernel<false><<<1, SMALL_THREADS, use_smem ? bytes : 0, (cudaStream_t)stream>>>(
-      G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr, dinfo, (double*)ws, use_smem);
+      G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr, dinfo, (double*)ws, use_smem, gate_in,
+      gate_out, first_pass);
   POD_CHECK_LAUNCH("cholqr");
   return POD_OK;
 }
@@ -783,20 +823,32 @@ extern "C" int pod_svd_small(const double* A, int64_t lda, int64_t nr, int64_t n
 
 extern "C" int pod_small_gemm(int64_t p, int64_t q, int64_t k, double alpha, const double* A,
                               int64_t lda, int transa, const double* B, int64_t ldb, double beta,
-                              double* C, int64_t ldc, void* stream) {
+                              double* C, int64_t ldc, const int32_t* gate, void* stream) {
   POD_REQUIRE(p >= 0 && q >= 0 && k >= 0, "pod_small_gemm: bad shape");
   if (p == 0 || q == 0) return POD_OK;
   int blocks = (int)std::min<int64_t>(ceil_div(p * q, 256), 1024);
   small_gemm_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((int)p, (int)q, (int)k, alpha, A,
-                                                                lda, transa, B, ldb, beta, C, ldc);
+                                                                lda, transa, B, ldb, beta, C, ldc,
+                                                                gate);
   POD_CHECK_LAUNCH("small_gemm");
   return POD_OK;
 }
 
-extern "C" int pod_maxabs(const double* A, int64_t lda, int64_t p, int64_t q, double* out,
-                          void* stream) {
+extern "C" int pod_small_copy(int64_t p, int64_t q, const double* src, int64_t lds, double* dst,
+                              int64_t ldd, const int32_t* gate, void* stream) {
+  POD_REQUIRE(p >= 0 && q >= 0, "pod_small_copy: bad shape");
+  if (p == 0 || q == 0) return POD_OK;
+  int blocks = (int)std::min<int64_t>(ceil_div(p * q, 256), 1024);
+  small_copy_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((int)p, (int)q, src, lds, dst, ldd,
+                                                                gate);
+  POD_CHECK_LAUNCH("small_copy");
+  return POD_OK;
+}
+
+extern "C" int pod_maxabs(const double* A, int64_t lda, int64_t p, int64_t q, double thr,
+                          double* out, int32_t* gate_out, void* stream) {
   POD_REQUIRE(p >= 0 && q >= 0, "pod_maxabs: bad shape");
-  maxabs_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(A, lda, (int)p, (int)q, out);
+  maxabs_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(A, lda, (int)p, (int)q, thr, out, gate_out);
   POD_CHECK_LAUNCH("maxabs");
   return POD_OK;
 }

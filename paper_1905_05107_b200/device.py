@@ -23,6 +23,15 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
 
+def _gp(g):
+    """Gate argument: None, a raw c_void_p, or an int32 tensor element."""
+    if g is None:
+        return ctypes.c_void_p(0)
+    if isinstance(g, ctypes.c_void_p):
+        return g
+    return ctypes.c_void_p(g.data_ptr())
+
+
 class ColMat:
     """A column-major float64 device matrix: storage is a torch tensor of
     shape (cols, ld) whose row j is column j; m <= ld logical rows."""
@@ -118,12 +127,14 @@ class Ctx:
         self._call("colnorms2", 1, 2.0 * A.m * A.ncols, 8.0 * A.m * A.ncols, "pod_colnorms2_f64", A.ptr, A.m, A.ncols, A.ld, _ptr(out), _ptr(flag),
                   self.stream)
 
-    def draw(self, mode, weights, live, n, uniforms, c, idx, cnt):
+    def draw(self, mode, weights, live, n, uniforms, c, idx, cnt, info=None):
         ws = self.ws("draw", _lib.load().pod_draw_ws_bytes(n))
-        self._call("draw", 1, 0.0, 24.0 * n + 8.0 * c, "pod_draw", mode, _ptr(weights), _ptr(live), n, _ptr(uniforms), c, _ptr(idx),
-                  _ptr(cnt), _ptr(ws), ws.numel(), _ptr(self.info), self.stream)
+        self._call("draw", 1, 0.0, 24.0 * n + 8.0 * c, "pod_draw", mode, _ptr(weights),
+                   _ptr(live), n, _ptr(uniforms), c, _ptr(idx), _ptr(cnt), idx.numel(), _ptr(ws),
+                   ws.numel(), _ptr(self.info if info is None else info), self.stream)
 
-    def tn(self, p, q, alpha, X, Y, C, ldc, xcols=None, ycols=None, m=None):
+    def tn(self, p, q, alpha, X, Y, C, ldc, xcols=None, ycols=None, m=None, gate=None,
+           tag="gemm_tn"):
         m = X.m if m is None else m
         if p == 0 or q == 0:
             return
@@ -132,47 +143,59 @@ class Ctx:
         sym = X.ptr.value == Y.ptr.value and (xcols is ycols)
         flops = float(m) * p * (p + 1) if sym else 2.0 * m * p * q
         nbytes = 8.0 * m * (p if sym else p + q)
-        self._call("gemm_tn", 2, flops, nbytes, "pod_gemm_tn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), Y.ptr, Y.ld,
-                  _ptr(ycols), C, ldc, _ptr(ws), ws.numel(), self.stream)
+        self._call(tag if gate is None else tag + "[gated]", 2, flops, nbytes,
+                   "pod_gemm_tn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), Y.ptr, Y.ld,
+                  _ptr(ycols), C, ldc, _ptr(ws), ws.numel(), _gp(gate), self.stream)
 
-    def nn(self, p, q, alpha, X, T, ldt, Y, beta=0.0, Z=None, xcols=None, m=None):
+    def nn(self, p, q, alpha, X, T, ldt, Y, beta=0.0, Z=None, xcols=None, m=None, gate=None,
+           tag="gemm_nn"):
         m = X.m if m is None else m
         if q == 0:
             return
         nbytes = 8.0 * m * (p + q + (q if beta != 0.0 else 0))
-        self._call("gemm_nn", 1, 2.0 * m * p * q, nbytes, "pod_gemm_nn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), T, ldt,
+        self._call(tag if gate is None else tag + "[gated]", 1, 2.0 * m * p * q, nbytes,
+                   "pod_gemm_nn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), T, ldt,
                   float(beta), Z.ptr if Z is not None else ctypes.c_void_p(0),
-                  Z.ld if Z is not None else 1, Y.ptr, Y.ld, self.stream)
+                  Z.ld if Z is not None else 1, Y.ptr, Y.ld, _gp(gate), self.stream)
 
     def small_ws(self, n):
         return self.ws("small", _lib.load().pod_small_ws_bytes(n))
 
-    def gram_eigh(self, G, ldg, g, r, sigma, T, ldt):
+    def gram_eigh(self, G, ldg, g, r, sigma, T, ldt, info=None):
         ws = self.small_ws(g)
-        self._call("gram_eigh", 1, 0.0, 8.0 * g * g, "pod_gram_eigh", G, ldg, g, r, _ptr(sigma), T, ldt, _ptr(self.info), _ptr(ws),
+        self._call("gram_eigh", 1, 0.0, 8.0 * g * g, "pod_gram_eigh", G, ldg, g, r, _ptr(sigma), T, ldt,
+                   _ptr(self.info if info is None else info), _ptr(ws),
                   ws.numel(), self.stream)
 
-    def cholqr_factor(self, G, ldg, l, nrows, Rinv, ldri, R, ldr):
+    def cholqr_factor(self, G, ldg, l, nrows, Rinv, ldri, R, ldr, gate_in=None, gate_out=None,
+                      first_pass=0):
         ws = self.small_ws(l)
         self._call("cholqr_factor", 1, 0.0, 8.0 * l * l, "pod_cholqr_factor", G, ldg, l, nrows, Rinv, ldri, R, ldr, _ptr(self.dinfo),
-                  _ptr(ws), ws.numel(), self.stream)
+                  _ptr(ws), ws.numel(), _gp(gate_in), _gp(gate_out), int(first_pass), self.stream)
 
-    def merge_core(self, sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new):
+    def merge_core(self, sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new,
+                   info=None):
         ws = self.small_ws(l1 + l2)
         self._call("merge_core", 1, 0.0, 8.0 * (l1 + l2) ** 2, "pod_merge_core", sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols,
-                  sig_new, _ptr(self.info), _ptr(ws), ws.numel(), self.stream)
+                  sig_new, _ptr(self.info if info is None else info), _ptr(ws), ws.numel(),
+                  self.stream)
 
     def svd_small(self, A, lda, nr, nc, U, ldu, sigma, V, ldv):
         ws = self.small_ws(max(nr, nc))
         self._call("svd_small", 1, 0.0, 8.0 * nr * nc, "pod_svd_small", A, lda, nr, nc, U, ldu, _ptr(sigma), V, ldv, _ptr(self.info),
                   _ptr(ws), ws.numel(), self.stream)
 
-    def small_gemm(self, p, q, k, alpha, A, lda, transa, B, ldb, beta, C, ldc):
+    def small_gemm(self, p, q, k, alpha, A, lda, transa, B, ldb, beta, C, ldc, gate=None):
         self._call("small_gemm", 1, 2.0 * p * q * k, 0.0, "pod_small_gemm", p, q, k, float(alpha), A, lda, int(transa), B, ldb,
-                  float(beta), C, ldc, self.stream)
+                  float(beta), C, ldc, _gp(gate), self.stream)
 
-    def maxabs(self, A, lda, p, q, out):
-        self._call("maxabs", 1, 0.0, 8.0 * p * q, "pod_maxabs", A, lda, p, q, out, self.stream)
+    def small_copy(self, p, q, src, lds, dst, ldd, gate=None):
+        self._call("small_copy", 1, 0.0, 16.0 * p * q, "pod_small_copy", p, q, src, lds, dst, ldd,
+                   _gp(gate), self.stream)
+
+    def maxabs(self, A, lda, p, q, out, thr=0.0, gate_out=None):
+        self._call("maxabs", 1, 0.0, 8.0 * p * q, "pod_maxabs", A, lda, p, q, float(thr), out,
+                   _gp(gate_out), self.stream)
 
     def fix_signs(self, U, l, V=None, n=0):
         ws = self.ws("colwise", _lib.load().pod_colwise_ws_bytes(U.m, max(l, 1)))

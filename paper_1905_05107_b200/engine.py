@@ -1,20 +1,33 @@
 """Device-resident ISMA engine (column-sampling path).
 
-One ``IsmaEngine`` owns every buffer of a run on one GPU.  The data matrix
-A stays in HBM (column-major, ld = m); the running factor lives in one of
-two "stacks" S0/S1 of 2r columns each: columns [0, r) hold the current
-basis U (zero-padded beyond its l modes), columns [r, r + l2) receive the
-merge's orthogonal complement Q, so the merged basis [U1 Q] U_E is one
-GEMM over a contiguous operand (no hstack copy, merge.py:86).
+Layout in HBM (one engine per run and GPU):
+  A          m x n column-major, ld = m (the data matrix, read in place)
+  S0, S1     m x 2r "stacks": columns [0, r) hold the current basis U (zero
+             beyond its l modes), columns [r, 2r) receive the merge's
+             orthogonal complement Q, so the merged basis [U1 Q] U_E is ONE
+             GEMM over a contiguous operand (no hstack, merge.py:86)
+  Uupd, W    m x r: the lifted update U2 and the projection residual
+  small      r x r matrices (M, C, Grams, R factors), 2r x r rotation T
 
-Per round (isma.py:276-293) the host issues:
-  draw (pod_draw)  -> Gram of A[:, idx] (TN, gathered)  -> eigh (Jacobi)
-  -> lift A[:, idx] T (NN, gathered)                     [get_update]
-  -> M = U1^T U2 -> W = U2 - U1 M -> CholeskyQR passes   [block_merge]
-  -> leak test / second projection -> E-SVD -> [U1 Q] T
-  -> cosines                                             [convergence]
-and reads back a handful of scalars (g, |S|, keep, CholQR defect, leak,
-cosines): the round's only host synchronisation points.
+Every kernel of a round runs at CAPACITY (g = min(c, n) sampled columns,
+l = r modes) on zero-padded operands: padded sample slots carry gather
+index -1 (a zero column), padded modes are zero columns with sigma = 0.
+Zero columns add only zero singular values and never pass the reference's
+rank cuts, so results equal the reference's on the active part.  Data-
+dependent branches of the reference -- the number of CholeskyQR passes
+and the second projection of merge.py:73-79 -- are device-side gates
+(int32 flags) read by the kernels themselves.  A round is therefore a
+static launch sequence with no host synchronisation: the host uploads the
+round's uniforms, launches (or replays a captured CUDA graph), and reads
+back one small record (g, |S|, ranks, keep) plus the k cosines.
+
+Per round (isma.py:276-293):
+  draw -> Gram of A[:, idx] (TN, gathered) -> eigh (pivoted Cholesky +
+  Jacobi) -> lift A[:, idx] T (NN, gathered)                 [get_update]
+  M = U1^T U2 -> W = U2 - U1 M -> CholeskyQR (<= 4 gated passes)
+  -> leak gate -> gated second projection -> E-SVD (Jacobi)
+  -> [U1 Q] T                                                [block_merge]
+  -> cosines                                                 [convergence]
 """
 
 from __future__ import annotations
@@ -25,19 +38,30 @@ import numpy as np
 import torch
 
 from .device import ColMat, dptr
-from .errors import DegenerateDistributionError
+from .errors import DegenerateDistributionError, ParameterError
 
-REORTH_TOL = 1e-8          # merge.py:34
-CHOLQR_STOP_DEFECT = 1e-4  # input defect below which one more CholQR pass is exact to eps
+REORTH_TOL = 1e-8  # merge.py:34
+CHOLQR_PASSES = 4  # pass 0 always; passes 1..3 gated on the previous pass
 
 MODE_L2N, MODE_UNIFORM, MODE_WEIGHTS = 0, 1, 2
 
+# round record slots (int64)
+REC_G, REC_REM, REC_STATUS, REC_RANK, REC_KEEP_UPD, REC_EIGH_SWEEPS, REC_KEEP, REC_MERGE_SWEEPS = \
+    range(8)
+REC_LEN = 8
+
+# gate slots (int32)
+G_QR = 0            # main CholeskyQR passes: slots 0..4
+G_LEAK = 5          # merge.py:73 second projection
+G_RQR = 6           # second-projection CholeskyQR passes: slots 6..10
+G_FQR = 11          # finalize CholeskyQR passes: 11..15
+N_GATES = 16
+
 
 class MergeWorkspace:
-    """Buffers + steps of BLOCK MERGE at rank r for m-row factors: the two
-    basis stacks, the update slot, the residual block and the small
-    r x r matrices.  Used by the ISMA engine, block_merge and the
-    out-of-core driver."""
+    """Buffers and launch sequences of BLOCK MERGE at rank r for m-row
+    factors (used by the ISMA engine, block_merge and the one-pass
+    incremental driver)."""
 
     def __init__(self, ctx, m, r, *, k=1, criterion="modes", upd_cap=None):
         self.ctx = ctx
@@ -61,110 +85,123 @@ class MergeWorkspace:
         self.Rtmp = torch.zeros(sq, **f64)
         self.Tm = torch.zeros(2 * r * r, **f64)
         self.sig = [torch.zeros(r, **f64), torch.zeros(r, **f64)]
-        self.xi = torch.zeros(max(self.k, 1), **f64)
-        self.Ck = torch.zeros(max(self.k, 1) ** 2, **f64)
+        kk = max(self.k, 1)
+        self.xi = torch.zeros(kk, **f64)
+        self.Ck = torch.zeros(kk * kk, **f64)
+        self.gates = torch.ones(N_GATES, dtype=torch.int32, device=dev)
+        self.rec = torch.zeros(REC_LEN, dtype=torch.int64, device=dev)
+        self.h_rec = torch.zeros(REC_LEN, dtype=torch.int64).pin_memory()
+        self.h_xi = torch.zeros(kk, dtype=torch.float64).pin_memory()
+        self.leak = torch.zeros(1, **f64)
         self.cur = 0
         self.l = 0
-        self.stats = {"cholqr_passes": 0, "reorth": 0, "rounds": 0}
+        self.stats = {"rounds": 0}
+
+    # ------------------------------------------------------------ helpers --
+    def gate(self, i):
+        return self.gates[i:i + 1]
 
     def load_factor(self, which, u, sigma):
-        """Host factor -> stack `which` (cols 0..l) or the update slot."""
+        """Host factor -> stack `which` (cols 0..l) or the update slot; the
+        padding columns and sigmas are zeroed."""
         l = int(sigma.shape[0])
         ut = torch.as_tensor(np.ascontiguousarray(np.asarray(u, dtype=np.float64).T))
         if which == "upd":
+            self.Uupd.t[:self.r, :self.m].zero_()
             self.Uupd.t[:l, :self.m].copy_(ut)
+            self.sig_upd.zero_()
             self.sig_upd[:l].copy_(torch.as_tensor(sigma, dtype=torch.float64))
         else:
+            self.S[which].t[:self.r, :self.m].zero_()
             self.S[which].t[:l, :self.m].copy_(ut)
+            self.sig[which].zero_()
             self.sig[which][:l].copy_(torch.as_tensor(sigma, dtype=torch.float64))
         return l
 
-    # ---------------------------------------------------------- pieces ---
-    def cholqr(self, W, l, dest, Rout):
-        """Orthonormalise the m x l block W into dest (Q) with W = Q Rout.
-        CholeskyQR2 with column scaling; more passes while a pass's input
-        was not already orthonormal to CHOLQR_STOP_DEFECT."""
+    # ------------------------------------------------------- launch pieces --
+    def cholqr_ops(self, Wsrc, Q, l, Rout, gate_base, first_gate=None):
+        """Q = orthonormal factor of Wsrc (m x l) with Wsrc = Q Rout (the
+        Householder QR of merge.py:70/76, matcore.py:209 replaced by gated
+        CholeskyQR passes).  Pass 0 runs when first_gate is null or set;
+        pass p >= 1 runs when pass p-1 asked for it (slot gate_base + p)."""
         ctx, r = self.ctx, self.r
-        src = W
-        for pas in range(6):
-            ctx.tn(l, l, 1.0, src, src, dptr(self.Gq), r)
-            ctx.cholqr_factor(dptr(self.Gq), r, l, src.m, dptr(self.Rinv), r, dptr(self.Rk), r)
-            defect, attempts, _, _ = ctx.read_dinfo(4)
-            if src is dest and l <= 64:
-                out = dest
-            else:
-                out = dest if src is not dest else W
-            ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, out)
-            if pas == 0:
-                Rout.copy_(self.Rk)
-            else:
-                ctx.small_gemm(l, l, l, 1.0, dptr(self.Rk), r, 0, dptr(Rout), r, 0.0,
-                               dptr(self.Rtmp), r)
-                Rout.copy_(self.Rtmp)
-            self.stats["cholqr_passes"] += 1
-            src = out
-            if pas >= 1 and defect <= CHOLQR_STOP_DEFECT and attempts == 0:
-                break
-        if src is not dest:
-            dest.t[dest.col0:dest.col0 + l, :dest.m].copy_(src.t[src.col0:src.col0 + l, :src.m])
-        return dest
+        g0 = first_gate
+        ctx.tn(l, l, 1.0, Wsrc, Wsrc, dptr(self.Gq), r, gate=g0, tag="tn_cholqr_gram")
+        ctx.cholqr_factor(dptr(self.Gq), r, l, Wsrc.m, dptr(self.Rinv), r, dptr(self.Rk), r,
+                          gate_in=g0, gate_out=self.gate(gate_base + 1), first_pass=1)
+        ctx.nn(l, l, 1.0, Wsrc, dptr(self.Rinv), r, Q, gate=g0, tag="nn_cholqr_apply")
+        ctx.small_copy(l, l, dptr(self.Rk), r, dptr(Rout), r, gate=g0)
+        for p in range(1, CHOLQR_PASSES):
+            gp = self.gate(gate_base + p)
+            ctx.tn(l, l, 1.0, Q, Q, dptr(self.Gq), r, gate=gp, tag="tn_cholqr_gram")
+            ctx.cholqr_factor(dptr(self.Gq), r, l, Q.m, dptr(self.Rinv), r, dptr(self.Rk), r,
+                              gate_in=gp, gate_out=self.gate(gate_base + p + 1), first_pass=0)
+            ctx.nn(l, l, 1.0, Q, dptr(self.Rinv), r, Q, gate=gp, tag="nn_cholqr_apply")
+            ctx.small_gemm(l, l, l, 1.0, dptr(self.Rk), r, 0, dptr(Rout), r, 0.0,
+                           dptr(self.Rtmp), r, gate=gp)
+            ctx.small_copy(l, l, dptr(self.Rtmp), r, dptr(Rout), r, gate=gp)
 
-    def merge(self, l1, l2):
-        """block_merge (merge.py:37-91) of the current factor (stack cur,
-        l1 modes) with the update in Uupd (l2 modes) into the other stack."""
+    def merge_ops(self, cur):
+        """block_merge (merge.py:37-91) of stack `cur` (U1, sig[cur]) with the
+        update slot (Uupd, sig_upd) into stack 1 - cur, all at capacity r."""
         ctx, r = self.ctx, self.r
-        S, Snext = self.S[self.cur], self.S[1 - self.cur]
-        if l2 == 0:  # empty update: identity (merge.py:57-58)
-            return self.cur, l1
-        if l1 == 0:  # empty accumulator: the update is the merge (merge.py:55-56)
-            Snext.t[:l2, :self.m].copy_(self.Uupd.t[:l2, :self.m])
-            self.sig[1 - self.cur][:l2].copy_(self.sig_upd[:l2])
-            return 1 - self.cur, l2
-        U1 = S.cols(0, l1)
-        U2 = self.Uupd.cols(0, l2)
-        ctx.tn(l1, l2, 1.0, U1, U2, dptr(self.M), r)                       # merge.py:65
-        ctx.nn(l1, l2, -1.0, U1, dptr(self.M), r, self.W, beta=1.0, Z=U2)  # merge.py:69
-        Q = S.cols(r, r + l2)
-        self.cholqr(self.W.cols(0, l2), l2, Q, self.Rt)                    # merge.py:70
-        ctx.tn(l1, l2, 1.0, U1, Q, dptr(self.C), r)                        # merge.py:72
-        ctx.maxabs(dptr(self.C), r, l1, l2, dptr(ctx.dinfo, 8))
-        leak = ctx.read_dinfo(9)[8]
-        if leak > REORTH_TOL:                                              # merge.py:73-79
-            self.stats["reorth"] += 1
-            ctx.nn(l1, l2, -1.0, U1, dptr(self.C), r, self.W, beta=1.0, Z=Q)
-            self.cholqr(self.W.cols(0, l2), l2, Q, self.Rt2)
-            ctx.small_gemm(l1, l2, l2, 1.0, dptr(self.C), r, 0, dptr(self.Rt), r, 1.0,
-                           dptr(self.M), r)
-            ctx.small_gemm(l2, l2, l2, 1.0, dptr(self.Rt2), r, 0, dptr(self.Rt), r, 0.0,
-                           dptr(self.Rtmp), r)
-            self.Rt.copy_(self.Rtmp)
-        nxt = 1 - self.cur
-        ctx.merge_core(dptr(self.sig[self.cur]), l1, dptr(self.M), r, dptr(self.Rt), r,
-                       dptr(self.sig_upd), l2, r, r, dptr(self.Tm), 2 * r, r,
-                       dptr(self.sig[nxt]))                               # merge.py:80-85
-        keep, sweeps = ctx.read_info(2)
-        self.stats.setdefault("merge_sweeps", []).append(sweeps)
-        ctx.nn(r + l2, keep, 1.0, S, dptr(self.Tm), 2 * r, Snext.cols(0, keep))  # merge.py:86-88
-        return nxt, keep
+        S, Snext = self.S[cur], self.S[1 - cur]
+        U1 = S.cols(0, r)
+        U2 = self.Uupd.cols(0, r)
+        Q = S.cols(r, 2 * r)
+        ctx.tn(r, r, 1.0, U1, U2, dptr(self.M), r, tag="tn_merge_proj")       # merge.py:65
+        ctx.nn(r, r, -1.0, U1, dptr(self.M), r, self.W, beta=1.0, Z=U2,
+               tag="nn_merge_resid")                                         # merge.py:69
+        self.cholqr_ops(self.W, Q, r, self.Rt, G_QR)                         # merge.py:70
+        ctx.tn(r, r, 1.0, U1, Q, dptr(self.C), r, tag="tn_merge_leak")       # merge.py:72
+        ctx.maxabs(dptr(self.C), r, r, r, dptr(self.leak), thr=REORTH_TOL,
+                   gate_out=self.gate(G_LEAK))
+        gl = self.gate(G_LEAK)                                               # merge.py:73-79
+        ctx.nn(r, r, -1.0, U1, dptr(self.C), r, self.W, beta=1.0, Z=Q, gate=gl,
+               tag="nn_merge_resid")
+        self.cholqr_ops(self.W, Q, r, self.Rt2, G_RQR, first_gate=gl)
+        ctx.small_gemm(r, r, r, 1.0, dptr(self.C), r, 0, dptr(self.Rt), r, 1.0, dptr(self.M), r,
+                       gate=gl)
+        ctx.small_gemm(r, r, r, 1.0, dptr(self.Rt2), r, 0, dptr(self.Rt), r, 0.0,
+                       dptr(self.Rtmp), r, gate=gl)
+        ctx.small_copy(r, r, dptr(self.Rtmp), r, dptr(self.Rt), r, gate=gl)
+        ctx.merge_core(dptr(self.sig[cur]), r, dptr(self.M), r, dptr(self.Rt), r,
+                       dptr(self.sig_upd), r, r, r, dptr(self.Tm), 2 * r, r,
+                       dptr(self.sig[1 - cur]), info=self.rec[REC_KEEP:])    # merge.py:80-85
+        ctx.nn(2 * r, r, 1.0, S, dptr(self.Tm), 2 * r, Snext.cols(0, r),
+               tag="nn_merge_rotate")                                        # merge.py:86-88
 
-    def cosines(self, old, l_old, new, l_new):
-        """convergence_cosines (isma.py:181-201)."""
+    def cosines_ops(self, old, new):
+        """convergence_cosines (isma.py:181-201) into self.xi (length k);
+        padded (missing) modes are zero columns and contribute 0."""
         ctx, k = self.ctx, self.k
-        kk = min(k, l_old, l_new)
-        P, Qn = self.S[old].cols(0, max(kk, 1)), self.S[new].cols(0, max(kk, 1))
+        P, Qn = self.S[old].cols(0, k), self.S[new].cols(0, k)
         if self.criterion == "modes":
-            ctx.coldots(P, Qn, k, kk, True, self.xi)
-            return self.xi[:k].cpu().numpy().copy()
-        xi = np.zeros(k)
-        if kk:
-            ctx.tn(kk, kk, 1.0, P, Qn, dptr(self.Ck), kk)
-            sv = torch.empty(kk, dtype=torch.float64, device=ctx.device)
-            ctx.svd_small(dptr(self.Ck), kk, kk, kk, None, 1, sv, None, 1)
-            xi[:kk] = sv.cpu().numpy()
-        return np.clip(xi, 0.0, 1.0)
+            ctx.coldots(P, Qn, k, k, True, self.xi)
+        else:
+            ctx.tn(k, k, 1.0, P, Qn, dptr(self.Ck), k, tag="tn_cosines")
+            ctx.svd_small(dptr(self.Ck), k, k, k, None, 1, self.xi, None, 1)
+
+    def readback(self):
+        self.h_rec.copy_(self.rec, non_blocking=True)
+        self.h_xi.copy_(self.xi, non_blocking=True)
+
+    def read_record(self):
+        torch.cuda.current_stream(self.ctx.device).synchronize()
+        rec = [int(x) for x in self.h_rec.tolist()]
+        xi = np.clip(self.h_xi.numpy().astype(np.float64), 0.0, 1.0)
+        return rec, xi
+
+    def merge_now(self, cur):
+        """Standalone merge (block_merge): returns (next stack, keep)."""
+        self.merge_ops(cur)
+        self.readback()
+        rec, _ = self.read_record()
+        return 1 - cur, rec[REC_KEEP]
+
 
 class IsmaEngine(MergeWorkspace):
-    def __init__(self, ctx, A, *, k, r, c, criterion="modes"):
+    def __init__(self, ctx, A, *, k, r, c, criterion="modes", use_graphs=True):
         self.A = A
         self.n = A.ncols
         self.c = int(c)
@@ -184,76 +221,126 @@ class IsmaEngine(MergeWorkspace):
         self.G = torch.empty(g * g, **f64)
         self.Tl = torch.empty(g * r, **f64)
         self.npos = 0
+        self.use_graphs = use_graphs
+        self.graphs = {}
+        self.graph_launches = {}
 
+    def reset(self):
+        """Per-run state (the captured graphs and buffers are reused)."""
+        self.live.fill_(1)
+        self.cur = 0
+        self.l = 0
+        self.npos = 0
+        self.stats = {"rounds": 0}
+
+    # ------------------------------------------------------------ pieces --
     def norm_pass(self):
         """Fused validate + column norms (matcore.py:54, isma.py:260)."""
         self.ctx.colnorms2(self.A, self.norms2, self.nonfinite)
         flag = int(self.nonfinite.item())
         if flag:
-            from .errors import ParameterError
-
             raise ParameterError("matrix contains non-finite entries")
         self.npos = int((self.norms2 > 0).sum().item())
         if self.npos == 0:
             raise DegenerateDistributionError("all candidate column weights are zero")
 
-    def draw(self, mode, rng):
-        u = np.asarray(rng.random(int(self.c)), dtype=np.float64)  # one batch (sampling.py:213)
-        self.h_uni.numpy()[:] = u
+    def update_ops(self, mode, dest):
+        """get_update (isma.py:144-178), column path, at capacity."""
+        ctx, A, g, r = self.ctx, self.A, self.gcap, self.r
         self.uni.copy_(self.h_uni, non_blocking=True)
-        self.ctx.draw(mode, self.norms2 if mode == MODE_L2N else None, self.live, self.n, self.uni,
-                      self.c, self.idx, self.cnt)
-        g, rem, status = self.ctx.read_info(3)
-        return g, rem, status
+        ctx.draw(mode, self.norms2 if mode == MODE_L2N else None, self.live, self.n, self.uni,
+                 self.c, self.idx, self.cnt, info=self.rec[REC_G:])
+        ctx.tn(g, g, 1.0, A, A, dptr(self.G), g, xcols=self.idx, ycols=self.idx,
+               tag="tn_gram_gather")                                         # baselines.py:43
+        ctx.gram_eigh(dptr(self.G), g, g, r, self.sig_upd, dptr(self.Tl), g,
+                      info=self.rec[REC_RANK:])                                   # baselines:44-48
+        ctx.nn(g, r, 1.0, A, dptr(self.Tl), g, dest, xcols=self.idx,
+               tag="nn_lift_gather")                                         # baselines.py:62-63
 
-    def update(self, mode, rng, dest):
-        """get_update (isma.py:144-178), column path: returns (g, |S|, keep)."""
-        g, rem, status = self.draw(mode, rng)
-        if status != 0:
-            raise RuntimeError(f"pod_draw status {status}")
-        ctx, A = self.ctx, self.A
-        ctx.tn(g, g, 1.0, A, A, dptr(self.G), g, xcols=self.idx, ycols=self.idx)
-        ctx.gram_eigh(dptr(self.G), g, g, self.r, self.sig_upd, dptr(self.Tl), g)
-        rank, keep, sweeps = ctx.read_info(3)
-        self.stats.setdefault("eigh_sweeps", []).append(sweeps)
-        if keep > 0:
-            ctx.nn(g, keep, 1.0, A, dptr(self.Tl), g, dest, xcols=self.idx)
-        return g, rem, keep
+    def round_ops(self, mode, cur):
+        self.update_ops(mode, self.Uupd)
+        self.merge_ops(cur)
+        self.cosines_ops(cur, 1 - cur)
+        self.readback()
+
+    def launch_round(self, mode, cur):
+        if not self.use_graphs or self.ctx.prof is not None:
+            self.round_ops(mode, cur)
+            return
+        key = (mode, cur)
+        gr = self.graphs.get(key)
+        if gr is None:
+            dev = self.ctx.device
+            # eager warm-up (grows every workspace) on a side stream, state restored
+            saved = [t.clone() for t in (self.live, self.rec, self.Uupd.t, self.S[1 - cur].t,
+                                         self.S[cur].t, self.sig[1 - cur], self.sig_upd)]
+            st = torch.cuda.Stream(dev)
+            st.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(st):
+                self.round_ops(mode, cur)
+            torch.cuda.current_stream(dev).wait_stream(st)
+            torch.cuda.synchronize(dev)
+            for dst, src in zip((self.live, self.rec, self.Uupd.t, self.S[1 - cur].t,
+                                 self.S[cur].t, self.sig[1 - cur], self.sig_upd), saved):
+                dst.copy_(src)
+            torch.cuda.synchronize(dev)
+            gr = torch.cuda.CUDAGraph()
+            l0 = self.ctx.launches
+            with torch.cuda.graph(gr, stream=st):
+                self.round_ops(mode, cur)
+            self.graph_launches[key] = self.ctx.launches - l0
+            self.graphs[key] = gr
+            torch.cuda.synchronize(dev)
+        gr.replay()
+        self.ctx.launches += self.graph_launches[key]
 
     def finalize(self):
         """isma.py:295-301: Q, R = QR(A^T U); SVD(R); U V_R, Q U_R; signs."""
-        ctx, r, n, l = self.ctx, self.r, self.n, self.l
+        ctx, r, n = self.ctx, self.r, self.n
         dev = ctx.device
-        U = self.S[self.cur].cols(0, l)
-        Cm = ColMat.zeros(n, l, dev)
-        ctx.tn(n, l, 1.0, self.A, U, Cm.ptr, n)                            # A^T U
-        Qc = ColMat.zeros(n, l, dev)
+        U = self.S[self.cur].cols(0, r)
+        Cm = ColMat.zeros(n, r, dev)
+        ctx.tn(n, r, 1.0, self.A, U, Cm.ptr, n, tag="tn_finalize_AtU")      # A^T U
+        Qc = ColMat.zeros(n, r, dev)
         Rc = torch.zeros(r * r, dtype=torch.float64, device=dev)
-        self.cholqr(Cm, l, Qc, Rc)
-        Ur = torch.zeros(l * l, dtype=torch.float64, device=dev)
-        Vr = torch.zeros(l * l, dtype=torch.float64, device=dev)
-        sr = torch.zeros(l, dtype=torch.float64, device=dev)
-        ctx.svd_small(dptr(Rc), r, l, l, dptr(Ur), l, sr, dptr(Vr), l)     # _svd(rr)
+        self.cholqr_ops(Cm, Qc, r, Rc, G_FQR)
+        Ur = torch.zeros(r * r, dtype=torch.float64, device=dev)
+        Vr = torch.zeros(r * r, dtype=torch.float64, device=dev)
+        sr = torch.zeros(r, dtype=torch.float64, device=dev)
+        ctx.svd_small(dptr(Rc), r, r, r, dptr(Ur), r, sr, dptr(Vr), r)       # _svd(rr)
         nxt = 1 - self.cur
-        Unew = self.S[nxt].cols(0, l)
-        ctx.nn(l, l, 1.0, U, dptr(Vr), l, Unew)                            # u @ vrt.T
-        Vnew = ColMat.zeros(n, l, dev)
-        ctx.nn(l, l, 1.0, Qc, dptr(Ur), l, Vnew)                           # q @ ur
-        ctx.fix_signs(Unew, l, Vnew, n)
-        self.sig[nxt][:l].copy_(sr)
+        Unew = self.S[nxt].cols(0, r)
+        ctx.nn(r, r, 1.0, U, dptr(Vr), r, Unew, tag="nn_finalize_rot")      # u @ vrt.T
+        Vnew = ColMat.zeros(n, r, dev)
+        ctx.nn(r, r, 1.0, Qc, dptr(Ur), r, Vnew, tag="nn_finalize_rot")     # q @ ur
+        ctx.fix_signs(Unew, r, Vnew, n)
+        self.sig[nxt].copy_(sr)
         self.cur = nxt
         return Vnew
 
     # ------------------------------------------------------------ driver ---
+    def _stage_uniforms(self, rng):
+        u = np.asarray(rng.random(int(self.c)), dtype=np.float64)  # one batch (sampling.py:213)
+        if u.shape != (self.c,):
+            raise ParameterError("generator returned a batch of the wrong shape")
+        self.h_uni.numpy()[:] = u
+
     def run(self, rng, *, strategy, tau, finalize, keep, trace_cls):
         """isma_run main loop (isma.py:258-303) on the device."""
         self.norm_pass()
         traces = []
         t0 = time.perf_counter()
-        g, rem, l = self.update(MODE_L2N, rng, self.S[self.cur])
+        cur = self.cur
+        r = self.r
+        self._stage_uniforms(rng)
+        self.update_ops(MODE_L2N, self.S[cur].cols(0, r))                    # bootstrap
+        self.sig[cur].copy_(self.sig_upd[:r])
+        self.readback()
+        rec, _ = self.read_record()
+        g, rem, keep0 = rec[REC_G], rec[REC_REM], rec[REC_KEEP_UPD]
         self.npos -= g
-        self.sig[self.cur][:l].copy_(self.sig_upd[:l])
-        self.l = l
+        self.sig[cur][keep0:].zero_()  # the basis carries keep0 modes; zero sigma padding
+        self.l = keep0
         traces.append(trace_cls(0, g, 0, rem, np.zeros(0), time.perf_counter() - t0))
         xi = np.zeros(self.k)
         it = 0
@@ -263,15 +350,19 @@ class IsmaEngine(MergeWorkspace):
             t0 = time.perf_counter()
             if mode == MODE_L2N and self.npos <= 0:
                 break  # l2n over only zero-norm columns (isma.py:211-215, 280-281)
-            g, rem, l2 = self.update(mode, rng, self.Uupd)
+            self._stage_uniforms(rng)
+            self.launch_round(mode, cur)
+            rec, xi = self.read_record()
+            g, rem = rec[REC_G], rec[REC_REM]
             if mode == MODE_L2N:
                 self.npos -= g
-            old, l_old = self.cur, self.l
-            nxt, l_new = self.merge(l_old, l2)
-            xi = self.cosines(old, l_old, nxt, l_new)
-            self.cur, self.l = nxt, l_new
+            cur = 1 - cur
+            self.l = rec[REC_KEEP]
             self.stats["rounds"] += 1
+            self.stats.setdefault("eigh_sweeps", []).append(rec[REC_EIGH_SWEEPS])
+            self.stats.setdefault("merge_sweeps", []).append(rec[REC_MERGE_SWEEPS])
             traces.append(trace_cls(it, g, 0, rem, xi.copy(), time.perf_counter() - t0))
+        self.cur = cur
         v = None
         if finalize and self.l:
             v = self.finalize()
@@ -285,3 +376,25 @@ class IsmaEngine(MergeWorkspace):
         s = self.sig[self.cur][:l].cpu().numpy().copy()
         vv = None if v is None else (v.to_numpy(l) if l else np.zeros((self.n, 0)))
         return u, s, vv
+
+
+_ENGINE_CACHE = {}
+
+
+def get_engine(ctx, A, *, k, r, c, criterion, use_graphs):
+    """Reuse the engine (buffers + captured round graphs) of the previous run
+    when the matrix buffer, shape and configuration match; one engine is
+    cached per device.  Graph replay reads A and the staged uniforms at
+    replay time, so a reused engine is valid for new contents of A."""
+    key = (A.t.data_ptr() + 8 * A.ld * A.col0, A.m, A.ncols, A.ld, int(k), int(r), int(c),
+           criterion, bool(use_graphs), ctx.device.index)
+    eng = _ENGINE_CACHE.get(ctx.device.index)
+    if eng is not None and eng.key == key:
+        eng.A = A
+        eng.reset()
+        return eng
+    _ENGINE_CACHE.pop(ctx.device.index, None)
+    eng = IsmaEngine(ctx, A, k=k, r=r, c=c, criterion=criterion, use_graphs=use_graphs)
+    eng.key = key
+    _ENGINE_CACHE[ctx.device.index] = eng
+    return eng

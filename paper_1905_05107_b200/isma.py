@@ -128,7 +128,8 @@ def _validate_shape(a):
     return a, int(shape[0]), int(shape[1])
 
 
-def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False):
+def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False,
+             use_graphs=True):
     """Run the full iteration (isma.py:225-303) on the GPU.
 
     ``a`` may be a numpy array (copied host->device), a CUDA torch tensor
@@ -136,7 +137,7 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
     list[IterationTrace])`` exactly as the reference.
     """
     from .device import get_ctx, to_device_colmajor
-    from .engine import IsmaEngine
+    from .engine import get_engine
     from .matcore import TruncatedFactor
 
     _require_column_path(config)
@@ -151,11 +152,12 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
         rng = np.random.default_rng(config.seed)
     ctx = get_ctx(device)
     A = to_device_colmajor(a, ctx.device)
-    eng = IsmaEngine(ctx, A, k=k, r=config.r, c=config.column_budget(),
-                     criterion=config.criterion)
+    eng = get_engine(ctx, A, k=k, r=config.r, c=config.column_budget(),
+                     criterion=config.criterion, use_graphs=use_graphs)
     traces, v = eng.run(rng, strategy=config.strategy, tau=config.tau,
                         finalize=config.finalize, keep=keep, trace_cls=IterationTrace)
     u, s, vv = eng.result(keep, v)
+    eng.A = None  # the cached engine must not keep the caller's matrix alive
     factor = TruncatedFactor(u, s, vv)
     global LAST_STATS
     LAST_STATS = eng.stats

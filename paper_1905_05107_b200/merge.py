@@ -37,9 +37,9 @@ def block_merge(f1, f2, r):
         raise ParameterError(f"factors live in different row spaces ({m1} vs {m2})")
     ctx = get_ctx()
     ws = MergeWorkspace(ctx, m1, r)
-    l1 = ws.load_factor(0, f1.u, f1.sigma)
-    l2 = ws.load_factor("upd", f2.u, f2.sigma)
-    nxt, keep = ws.merge(l1, l2)
+    ws.load_factor(0, f1.u, f1.sigma)
+    ws.load_factor("upd", f2.u, f2.sigma)
+    nxt, keep = ws.merge_now(0)
     ws.cur, ws.l = nxt, keep
     if keep:
         ctx.fix_signs(ws.S[nxt].cols(0, keep), keep)

@@ -228,3 +228,28 @@ def test_sample_with_replacement_known_answer():
     dr = pod.sample_with_replacement(d, 5, Q([[0.05, 0.21, 0.45, 0.51, 0.99]]))
     np.testing.assert_array_equal(dr.unique_indices, [3, 7, 9])
     np.testing.assert_array_equal(dr.counts, [1, 2, 2])
+
+
+def test_graph_replay_matches_eager_bitwise():
+    """The CUDA-graph round and the eager launch sequence are the same
+    kernels on the same data: identical results bit for bit."""
+    a = workloads.config1(seed=0)
+    cfg = pod.IsmaConfig(k=10, r=30, c=50, tau=1 - 1e-8, strategy="l2n", seed=7)
+    f1, t1 = pod.isma_run(a, cfg, use_graphs=True)
+    f2, t2 = pod.isma_run(a, cfg, use_graphs=False)
+    assert np.array_equal(f1.u, f2.u) and np.array_equal(f1.sigma, f2.sigma)
+    assert [t.remaining for t in t1] == [t.remaining for t in t2]
+    for a1, a2 in zip(t1, t2):
+        assert np.array_equal(a1.cosines, a2.cosines)
+
+
+def test_large_rank_capacity_paths():
+    """r > 64 exercises the 128/192-column NN tiles and Jacobi on >128 columns."""
+    a = workloads.config1(seed=3, m=3000, n=400)
+    for k, r in ((30, 90), (40, 160)):
+        cfg = pod.IsmaConfig(k=k, r=r, c=150, tau=0.999, strategy="l2n", seed=2)
+        f, tr = pod.isma_run(a, cfg)
+        o = orc.run(a, k, r=r, c=150, tau=0.999, strategy="l2n", seed=2)
+        assert [t.remaining for t in tr] == [t["remaining"] for t in o["trace"]]
+        assert sigma_relerr(f.sigma, o["sigma"]) <= SIGMA_RTOL
+        assert principal_angles_sin(f.u, o["u"]).max() <= ANGLE_TOL_RAD
