@@ -147,8 +147,9 @@ __device__ void cj_norms(cg::cluster_group& cl, const CJScratch& s, const double
 // One-sided cyclic Jacobi (round-robin pairs) on W distributed by rows.
 // Wl: this CTA's nrl rows (ld ldl) of all nc columns; Jl (nullable): this
 // CTA's njl rows (ld ldj) of the nc x nc accumulator.  Returns sweeps.
-__device__ int cj_jacobi(cg::cluster_group& cl, const CJScratch& s, double* Wl, int ldl, int nrl, int nc,
-                         double* Jl, int ldj, int njl, double tol, int max_sweeps) {
+template <int RPL>
+__device__ int cj_jacobi_t(cg::cluster_group& cl, const CJScratch& s, double* Wl, int ldl, int nrl,
+                           int nc, double* Jl, int ldj, int njl, double tol, int max_sweeps) {
   const int me = (int)cl.block_rank();
   const int N = nc + (nc & 1);
   const int M1 = N - 1;
@@ -156,7 +157,17 @@ __device__ int cj_jacobi(cg::cluster_group& cl, const CJScratch& s, double* Wl, 
   const double tol2 = tol * tol;
   // threads per pair for the partial dots (power of two, <= 32)
   int tpp = 1;
-  while (tpp * 2 * npairs <= (int)blockDim.x && tpp < 32) tpp *= 2;
+  while (tpp * 2 * npairs <= (int)blockDim.x && tpp < 16) tpp *= 2;
+  // DSMEM addresses of every CTA's receive buffers and mbarriers (fixed)
+  uint32_t rpart[CL], rmbar[CL];
+  {
+    const uint32_t lp = smem_u32(s.part), lm = smem_u32(s.mbar);
+#pragma unroll
+    for (int c = 0; c < CL; ++c) {
+      rpart[c] = cluster_map(lp, c);
+      rmbar[c] = cluster_map(lm, c);
+    }
+  }
   const int grp = threadIdx.x / tpp, gl = threadIdx.x % tpp;
   int sweep = 0;
   int parity = 0;
@@ -200,14 +211,25 @@ __device__ int cj_jacobi(cg::cluster_group& cl, const CJScratch& s, double* Wl, 
       double* wb = Wl + (int64_t)b * ldl;
       // 1. partial dot over the local rows -> every CTA's receive slot
       double g = 0.0;
-      if (live)
+      double xa[RPL > 0 ? RPL : 1], xb[RPL > 0 ? RPL : 1];
+      if (RPL > 0) {
+#pragma unroll
+        for (int k = 0; k < (RPL > 0 ? RPL : 1); ++k) {
+          const int i = gl + k * tpp;
+          const bool ok = live && i < nrl;
+          xa[k] = ok ? wa[i] : 0.0;
+          xb[k] = ok ? wb[i] : 0.0;
+          g = fma(xa[k], xb[k], g);
+        }
+      } else if (live) {
         for (int i = gl; i < nrl; i += tpp) g = fma(wa[i], wb[i], g);
+      }
       for (int o = tpp / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o, tpp);
       if (valid && gl == 0) {
-        const uint32_t slot = smem_u32(&s.part[(parity * CL + me) * npairs + pr]);
-        const uint32_t mb = smem_u32(&s.mbar[parity]);
+        const uint32_t off = (uint32_t)(((parity * CL + me) * npairs + pr) * sizeof(double));
+        const uint32_t moff = (uint32_t)(parity * sizeof(uint64_t));
 #pragma unroll
-        for (int c = 0; c < CL; ++c) st_async_f64(cluster_map(slot, c), g, cluster_map(mb, c));
+        for (int c = 0; c < CL; ++c) st_async_f64(rpart[c] + off, g, rmbar[c] + moff);
       }
       mbar_wait(&s.mbar[parity], (gstep >> 1) & 1u);
       // 2. full gamma (rank-ordered sum: identical in every CTA) and the
@@ -227,18 +249,29 @@ __device__ int cj_jacobi(cg::cluster_group& cl, const CJScratch& s, double* Wl, 
           const double ic = rsqrt_nr2(x);
           const double c_ = x * ic;
           const double s_ = copysign(fabs(gg) * rh * ic, d * gg);
-          for (int i = gl; i < nrl; i += tpp) {
-            const double xa = wa[i], yb = wb[i];
-            wa[i] = fma(c_, xa, -s_ * yb);
-            wb[i] = fma(s_, xa, c_ * yb);
+          if (RPL > 0) {
+#pragma unroll
+            for (int k = 0; k < (RPL > 0 ? RPL : 1); ++k) {
+              const int i = gl + k * tpp;
+              if (i < nrl) {
+                wa[i] = fma(c_, xa[k], -s_ * xb[k]);
+                wb[i] = fma(s_, xa[k], c_ * xb[k]);
+              }
+            }
+          } else {
+            for (int i = gl; i < nrl; i += tpp) {
+              const double x0 = wa[i], y0 = wb[i];
+              wa[i] = fma(c_, x0, -s_ * y0);
+              wb[i] = fma(s_, x0, c_ * y0);
+            }
           }
           if (Jl) {
             double* ja = Jl + (int64_t)a * ldj;
             double* jb = Jl + (int64_t)b * ldj;
             for (int i = gl; i < njl; i += tpp) {
-              const double xa = ja[i], yb = jb[i];
-              ja[i] = fma(c_, xa, -s_ * yb);
-              jb[i] = fma(s_, xa, c_ * yb);
+              const double x0 = ja[i], y0 = jb[i];
+              ja[i] = fma(c_, x0, -s_ * y0);
+              jb[i] = fma(s_, x0, c_ * y0);
             }
           }
           if (gl == 0) {
@@ -258,6 +291,18 @@ __device__ int cj_jacobi(cg::cluster_group& cl, const CJScratch& s, double* Wl, 
   }
   cj_norms(cl, s, Wl, ldl, nrl, nc);  // exact final norms
   return sweep;
+}
+
+__device__ int cj_jacobi(cg::cluster_group& cl, const CJScratch& s, double* Wl, int ldl, int nrl,
+                         int nc, double* Jl, int ldj, int njl, double tol, int max_sweeps) {
+  const int np = (nc + (nc & 1)) / 2;
+  int tpp = 1;
+  while (tpp * 2 * np <= (int)blockDim.x && tpp < 16) tpp *= 2;
+  const int rpl = (nrl + tpp - 1) / tpp;
+  if (rpl <= 4) return cj_jacobi_t<4>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
+  if (rpl <= 8) return cj_jacobi_t<8>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
+  if (rpl <= 16) return cj_jacobi_t<16>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
+  return cj_jacobi_t<0>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
 }
 
 // perm[k] = column with the k-th largest key (ties -> lower index)
@@ -476,6 +521,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CJ_THREADS)
 
 constexpr size_t CJ_SMEM_CAP = 224 * 1024;
 
+// Threads per CTA: up to 4 lanes per column pair (the device code uses the
+// largest power-of-two lanes-per-pair that fits), rounded to whole warps.
+static int cj_threads(int n) {
+  const int np = (n + 1) / 2;
+  int tpp = 1;
+  while (tpp * 2 * np <= CJ_THREADS && tpp < 4) tpp *= 2;
+  int t = ((tpp * np + 31) / 32) * 32;
+  return std::max(64, std::min(CJ_THREADS, t));
+}
+
 static int cj_set_smem(const void* fn, size_t bytes) {
   static const void* fns[8];
   static int nf = 0;
@@ -503,7 +558,7 @@ int cj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, 
   const size_t bytes = cj_scratch_bytes(n) + (size_t)nrl * n * sizeof(double);
   int st = cj_set_smem((const void*)cj_merge_core_kernel, bytes);
   if (st) return st;
-  cj_merge_core_kernel<<<CL, CJ_THREADS, bytes, stream>>>(sig1, (int)l1, M, ldm, R, ldr, sig2,
+  cj_merge_core_kernel<<<CL, cj_threads(n), bytes, stream>>>(sig1, (int)l1, M, ldm, R, ldr, sig2,
                                                            (int)l2, (int)r, (int)rcap, T, ldt,
                                                            (int)tcols, sig_new, info, nrl, 60);
   POD_CHECK_LAUNCH("cluster merge core");
@@ -517,7 +572,7 @@ int cj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t g
   const size_t bytes = cj_scratch_bytes((int)g) + (size_t)nrl * g * sizeof(double);
   int st = cj_set_smem((const void*)cj_gram_eigh_kernel, bytes);
   if (st) return st;
-  cj_gram_eigh_kernel<<<CL, CJ_THREADS, bytes, stream>>>(X, piv, rank, (int)g, (int)r, sigma, T,
+  cj_gram_eigh_kernel<<<CL, cj_threads((int)g), bytes, stream>>>(X, piv, rank, (int)g, (int)r, sigma, T,
                                                           ldt, info, nrl, 60);
   POD_CHECK_LAUNCH("cluster gram eigh");
   return POD_OK;
@@ -532,7 +587,7 @@ int cj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int6
   const size_t bytes = cj_scratch_bytes((int)nc) + ((size_t)nrl * nc + (size_t)njl * nc) * sizeof(double);
   int st = cj_set_smem((const void*)cj_svd_kernel, bytes);
   if (st) return st;
-  cj_svd_kernel<<<CL, CJ_THREADS, bytes, stream>>>(A, lda, (int)nr, (int)nc, U, ldu, sigma, V,
+  cj_svd_kernel<<<CL, cj_threads((int)nc), bytes, stream>>>(A, lda, (int)nr, (int)nc, U, ldu, sigma, V,
                                                     ldv, info, nrl, njl, 60);
   POD_CHECK_LAUNCH("cluster svd");
   return POD_OK;
