@@ -7,6 +7,7 @@ libpodsketch_b200.so.
 from __future__ import annotations
 
 import ctypes
+import warnings
 
 import numpy as np
 
@@ -274,5 +275,7 @@ def to_device_colmajor(a, device):
     arr = np.asarray(a)
     m, n = arr.shape
     arr = np.asarray(arr, dtype=np.float64, order="F")
-    host = torch.from_numpy(arr.T)  # (n, m) C-contiguous view of F-order data
+    with warnings.catch_warnings():  # read-only inputs are only read (copied to the device)
+        warnings.simplefilter("ignore", UserWarning)
+        host = torch.from_numpy(arr.T)  # (n, m) C-contiguous view of F-order data
     return ColMat(host.to(device), m, n)
