@@ -219,15 +219,21 @@ def main():
     from paper_1905_05107_b200.device import KernelProfile, get_ctx, to_device_colmajor
 
     ws, rank, local = _dist_env()
+    comm = None
     if ws > 1:
         torch.cuda.set_device(local)
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("POD_DIST_BACKEND", "nccl"))
+        from paper_1905_05107_b200.parallel import Comm, shard_rows
+
+        comm = Comm()
     w = WORKLOAD
     ctx = get_ctx()
     dev = ctx.device
-    at = workloads.config2_torch(w["data_seed"], w["side"], w["n"], device=dev)
+    m_total = w["side"] ** 2
+    rows = (0, m_total) if ws == 1 else shard_rows(m_total, ws, rank)  # row-sharded A
+    at = workloads.config2_torch(w["data_seed"], w["side"], w["n"], device=dev, rows=rows)
     m, n = at.shape[1], at.shape[0]
     A = to_device_colmajor(at.T, dev)
     cfg = pod.IsmaConfig(k=w["k"], r=w["r"], c=w["c"], tau=1 - w["tol"], strategy=w["strategy"],
@@ -235,7 +241,9 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def one_run():
-        return pod.isma_run(A, cfg)
+        if comm is None:
+            return pod.isma_run(A, cfg)
+        return pod.isma_run(A, cfg, comm=comm, m_total=m_total)
 
     for _ in range(args.warmup):
         factor, traces = one_run()
@@ -314,6 +322,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config-2 Fourier snapshot generator, on device)",
+        "parallelism": f"row-sharded dp{ws}" if ws > 1 else "single GPU",
         "config": _config_dict(n_rounds),
         "hbm_gbs_norm_pass": hbm_norm,
         "roofline": roof,
@@ -327,7 +336,7 @@ def main():
                          .LAST_STATS.items()},
     }
 
-    if rank == 0 and not args.no_e2e:
+    if rank == 0 and ws == 1 and not args.no_e2e:
         # public API with HOST buffers: H2D of A and D2H of the factor inside the timed region
         host = torch.empty((n, m), dtype=torch.float64).pin_memory()
         host.copy_(at)

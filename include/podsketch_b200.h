@@ -159,6 +159,14 @@ size_t pod_colwise_ws_bytes(int64_t m, int64_t l);
 int pod_fix_signs(double* U, int64_t m, int64_t l, int64_t ldu, double* V, int64_t n, int64_t ldv,
                   double* sign_out, void* ws, size_t ws_bytes, void* stream);
 
+/* Row-shard building blocks of fix_signs: per column the max |U| over this
+ * shard, its GLOBAL row (local + row_offset; first occurrence on ties) and
+ * the sign of that entry; and U[:, j] *= sign[j] (sign = +-1). */
+int pod_colargmax(const double* U, int64_t m, int64_t l, int64_t ldu, int64_t row_offset,
+                  double* val_out, int64_t* row_out, double* sign_out, void* ws, size_t ws_bytes,
+                  void* stream);
+int pod_scale_cols(double* U, int64_t m, int64_t l, int64_t ldu, const double* sign, void* stream);
+
 /* out[j] = sum_i P[i, j] Q[i, j] for j < kk, 0 for kk <= j < k; with
  * take_abs the |.| clipped to [0, 1] (convergence cosines, isma.py:195-201). */
 int pod_coldots(const double* P, int64_t ldp, const double* Q, int64_t ldq, int64_t m, int64_t k,

@@ -54,6 +54,8 @@ SIGNATURES = {
     "pod_maxabs": (_i32, [_vp, _i64, _i64, _i64, _f64, _vp, _vp, _vp]),
     "pod_colwise_ws_bytes": (_sz, [_i64, _i64]),
     "pod_fix_signs": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp, _sz, _vp]),
+    "pod_colargmax": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "pod_scale_cols": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp]),
     "pod_coldots": (_i32, [_vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _sz, _vp]),
 }
 

@@ -44,11 +44,14 @@ __global__ void __launch_bounds__(256) colargmax_partial_kernel(const double* __
   }
 }
 
-// sign[col] = -1 if U[argmax row, col] < 0 else +1 (chunks in ascending order)
+// sign[col] = -1 if U[argmax row, col] < 0 else +1 (chunks in ascending order);
+// optionally also the max |u| and its row (+ row_offset: global row index of a
+// row shard) for a cross-shard combination.
 __global__ void colargmax_final_kernel(const double* __restrict__ U, int64_t ldu, int l, int nchunk,
                                        const double* __restrict__ pval,
                                        const int64_t* __restrict__ prow,
-                                       double* __restrict__ sign) {
+                                       double* __restrict__ sign, double* __restrict__ val_out,
+                                       int64_t* __restrict__ row_out, int64_t row_offset) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= l) return;
   double best = -1.0;
@@ -58,6 +61,8 @@ __global__ void colargmax_final_kernel(const double* __restrict__ U, int64_t ldu
     if (v > best) { best = v; brow = prow[(int64_t)col * nchunk + c]; }
   }
   sign[col] = (U[brow + (int64_t)col * ldu] < 0.0) ? -1.0 : 1.0;
+  if (val_out) val_out[col] = best;
+  if (row_out) row_out[col] = brow + row_offset;
 }
 
 __global__ void scale_cols_kernel(double* __restrict__ U, int64_t m, int64_t ldu, int l,
@@ -121,8 +126,8 @@ extern "C" int pod_fix_signs(double* U, int64_t m, int64_t l, int64_t ldu, doubl
   double* sign = sign_out ? sign_out : (double*)(prow + (size_t)nchunk * l);
   colargmax_partial_kernel<<<dim3(nchunk, (unsigned)l), 256, 0, s>>>(U, m, ldu, (int)l, pval, prow);
   POD_CHECK_LAUNCH("colargmax partial");
-  colargmax_final_kernel<<<(unsigned)ceil_div(l, 128), 128, 0, s>>>(U, ldu, (int)l, nchunk, pval,
-                                                                     prow, sign);
+  colargmax_final_kernel<<<(unsigned)ceil_div(l, 128), 128, 0, s>>>(
+      U, ldu, (int)l, nchunk, pval, prow, sign, nullptr, nullptr, 0);
   POD_CHECK_LAUNCH("colargmax final");
   const int gx = (int)std::min<int64_t>(ceil_div(m, 256), 256);
   scale_cols_kernel<<<dim3(gx, (unsigned)l), 256, 0, s>>>(U, m, ldu, (int)l, sign);
@@ -152,5 +157,34 @@ extern "C" int pod_coldots(const double* P, int64_t ldp, const double* Q, int64_
   coldots_final_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, s>>>(pd, nchunk, (int)k, (int)kk,
                                                                   take_abs, out);
   POD_CHECK_LAUNCH("coldots final");
+  return POD_OK;
+}
+
+extern "C" int pod_colargmax(const double* U, int64_t m, int64_t l, int64_t ldu, int64_t row_offset,
+                             double* val_out, int64_t* row_out, double* sign_out, void* ws,
+                             size_t ws_bytes, void* stream) {
+  POD_REQUIRE(m >= 1 && l >= 0 && ldu >= m, "pod_colargmax: bad shape");
+  if (l == 0) return POD_OK;
+  POD_REQUIRE(ws_bytes >= pod_colwise_ws_bytes(m, l), "pod_colargmax: workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nchunk = (int)std::max<int64_t>(1, ceil_div(m, CHUNK_ROWS));
+  double* pval = (double*)ws;
+  int64_t* prow = (int64_t*)(pval + (size_t)nchunk * l);
+  colargmax_partial_kernel<<<dim3(nchunk, (unsigned)l), 256, 0, s>>>(U, m, ldu, (int)l, pval, prow);
+  POD_CHECK_LAUNCH("colargmax partial");
+  colargmax_final_kernel<<<(unsigned)ceil_div(l, 128), 128, 0, s>>>(
+      U, ldu, (int)l, nchunk, pval, prow, sign_out, val_out, row_out, row_offset);
+  POD_CHECK_LAUNCH("colargmax final");
+  return POD_OK;
+}
+
+extern "C" int pod_scale_cols(double* U, int64_t m, int64_t l, int64_t ldu, const double* sign,
+                              void* stream) {
+  POD_REQUIRE(m >= 0 && l >= 0 && ldu >= m, "pod_scale_cols: bad shape");
+  if (m == 0 || l == 0) return POD_OK;
+  const int gx = (int)std::min<int64_t>(ceil_div(m, 256), 256);
+  scale_cols_kernel<<<dim3(gx, (unsigned)l), 256, 0, (cudaStream_t)stream>>>(U, m, ldu, (int)l,
+                                                                            sign);
+  POD_CHECK_LAUNCH("scale cols");
   return POD_OK;
 }

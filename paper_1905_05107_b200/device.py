@@ -203,6 +203,16 @@ class Ctx:
         self._call("fix_signs", 4 if V is not None else 3, 0.0, 16.0 * U.m * l, "pod_fix_signs", U.ptr, U.m, l, U.ld, V.ptr if V is not None else None, n,
                   V.ld if V is not None else 1, None, _ptr(ws), ws.numel(), self.stream)
 
+    def colargmax(self, U, l, row_offset, val, row, sign):
+        ws = self.ws("colwise", _lib.load().pod_colwise_ws_bytes(U.m, max(l, 1)))
+        self._call("colargmax", 2, 0.0, 8.0 * U.m * l, "pod_colargmax", U.ptr, U.m, l, U.ld,
+                   int(row_offset), _ptr(val), _ptr(row), _ptr(sign), _ptr(ws), ws.numel(),
+                   self.stream)
+
+    def scale_cols(self, U, l, sign):
+        self._call("scale_cols", 1, 0.0, 16.0 * U.m * l, "pod_scale_cols", U.ptr, U.m, l, U.ld,
+                   _ptr(sign), self.stream)
+
     def coldots(self, P, Q, k, kk, take_abs, out):
         ws = self.ws("colwise", _lib.load().pod_colwise_ws_bytes(P.m, max(k, 1)))
         self._call("coldots", 2, 2.0 * P.m * kk, 16.0 * P.m * kk, "pod_coldots", P.ptr, P.ld, Q.ptr, Q.ld, P.m, k, kk, int(take_abs), _ptr(out),

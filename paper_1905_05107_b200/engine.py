@@ -63,8 +63,13 @@ class MergeWorkspace:
     factors (used by the ISMA engine, block_merge and the one-pass
     incremental driver)."""
 
-    def __init__(self, ctx, m, r, *, k=1, criterion="modes", upd_cap=None):
+    def __init__(self, ctx, m, r, *, k=1, criterion="modes", upd_cap=None, comm=None,
+                 row_offset=0):
+        from .parallel import Comm
+
         self.ctx = ctx
+        self.comm = comm if comm is not None else Comm()
+        self.row_offset = int(row_offset)
         self.m, self.r, self.k = int(m), int(r), int(k)
         self.criterion = criterion
         dev = ctx.device
@@ -119,7 +124,7 @@ class MergeWorkspace:
         return l
 
     # ------------------------------------------------------- launch pieces --
-    def cholqr_ops(self, Wsrc, Q, l, Rout, gate_base, first_gate=None):
+    def cholqr_ops(self, Wsrc, Q, l, Rout, gate_base, first_gate=None, sharded=True):
         """Q = orthonormal factor of Wsrc (m x l) with Wsrc = Q Rout (the
         Householder QR of merge.py:70/76, matcore.py:209 replaced by gated
         CholeskyQR passes).  Pass 0 runs when first_gate is null or set;
@@ -127,6 +132,8 @@ class MergeWorkspace:
         ctx, r = self.ctx, self.r
         g0 = first_gate
         ctx.tn(l, l, 1.0, Wsrc, Wsrc, dptr(self.Gq), r, gate=g0, tag="tn_cholqr_gram")
+        if sharded:
+            self.comm.allreduce_sum_(self.Gq)
         ctx.cholqr_factor(dptr(self.Gq), r, l, Wsrc.m, dptr(self.Rinv), r, dptr(self.Rk), r,
                           gate_in=g0, gate_out=self.gate(gate_base + 1), first_pass=1)
         ctx.nn(l, l, 1.0, Wsrc, dptr(self.Rinv), r, Q, gate=g0, tag="nn_cholqr_apply")
@@ -134,6 +141,8 @@ class MergeWorkspace:
         for p in range(1, CHOLQR_PASSES):
             gp = self.gate(gate_base + p)
             ctx.tn(l, l, 1.0, Q, Q, dptr(self.Gq), r, gate=gp, tag="tn_cholqr_gram")
+            if sharded:
+                self.comm.allreduce_sum_(self.Gq)
             ctx.cholqr_factor(dptr(self.Gq), r, l, Q.m, dptr(self.Rinv), r, dptr(self.Rk), r,
                               gate_in=gp, gate_out=self.gate(gate_base + p + 1), first_pass=0)
             ctx.nn(l, l, 1.0, Q, dptr(self.Rinv), r, Q, gate=gp, tag="nn_cholqr_apply")
@@ -150,10 +159,12 @@ class MergeWorkspace:
         U2 = self.Uupd.cols(0, r)
         Q = S.cols(r, 2 * r)
         ctx.tn(r, r, 1.0, U1, U2, dptr(self.M), r, tag="tn_merge_proj")       # merge.py:65
+        self.comm.allreduce_sum_(self.M)
         ctx.nn(r, r, -1.0, U1, dptr(self.M), r, self.W, beta=1.0, Z=U2,
                tag="nn_merge_resid")                                         # merge.py:69
         self.cholqr_ops(self.W, Q, r, self.Rt, G_QR)                         # merge.py:70
         ctx.tn(r, r, 1.0, U1, Q, dptr(self.C), r, tag="tn_merge_leak")       # merge.py:72
+        self.comm.allreduce_sum_(self.C)
         ctx.maxabs(dptr(self.C), r, r, r, dptr(self.leak), thr=REORTH_TOL,
                    gate_out=self.gate(G_LEAK))
         gl = self.gate(G_LEAK)                                               # merge.py:73-79
@@ -177,9 +188,11 @@ class MergeWorkspace:
         ctx, k = self.ctx, self.k
         P, Qn = self.S[old].cols(0, k), self.S[new].cols(0, k)
         if self.criterion == "modes":
-            ctx.coldots(P, Qn, k, k, True, self.xi)
+            ctx.coldots(P, Qn, k, k, False, self.xi)  # raw dots; |.| and clip on the host
+            self.comm.allreduce_sum_(self.xi)
         else:
             ctx.tn(k, k, 1.0, P, Qn, dptr(self.Ck), k, tag="tn_cosines")
+            self.comm.allreduce_sum_(self.Ck)
             ctx.svd_small(dptr(self.Ck), k, k, k, None, 1, self.xi, None, 1)
 
     def readback(self):
@@ -189,8 +202,35 @@ class MergeWorkspace:
     def read_record(self):
         torch.cuda.current_stream(self.ctx.device).synchronize()
         rec = [int(x) for x in self.h_rec.tolist()]
-        xi = np.clip(self.h_xi.numpy().astype(np.float64), 0.0, 1.0)
+        xi = np.clip(np.abs(self.h_xi.numpy().astype(np.float64)), 0.0, 1.0)
         return rec, xi
+
+    def fix_signs_ops(self, U, l, V=None, n=0):
+        """fix_signs (matcore.py:148-165) of a row-sharded basis: per-shard
+        arg-max, allgather, deterministic global choice, local flip."""
+        ctx = self.ctx
+        if not self.comm.active:
+            ctx.fix_signs(U, l, V, n)
+            return
+        dev = ctx.device
+        val = torch.empty(l, dtype=torch.float64, device=dev)
+        row = torch.empty(l, dtype=torch.int64, device=dev)
+        sign = torch.empty(l, dtype=torch.float64, device=dev)
+        ctx.colargmax(U, l, self.row_offset, val, row, sign)
+        from .parallel import combine_signs
+
+        g = combine_signs(self.comm.allgather(val), self.comm.allgather(row),
+                          self.comm.allgather(sign))
+        sign.copy_(g)
+        ctx.scale_cols(U, l, sign)
+        if V is not None:
+            ctx.scale_cols(V, l, sign)
+
+    def gather_rows(self, U, l, m_total):
+        """Full m_total x l host copy of a row-sharded basis."""
+        from .parallel import gather_row_shards
+
+        return gather_row_shards(U.t[U.col0:U.col0 + l, :U.m], m_total, self.comm)
 
     def merge_now(self, cur):
         """Standalone merge (block_merge): returns (next stack, keep)."""
@@ -201,12 +241,15 @@ class MergeWorkspace:
 
 
 class IsmaEngine(MergeWorkspace):
-    def __init__(self, ctx, A, *, k, r, c, criterion="modes", use_graphs=True):
+    def __init__(self, ctx, A, *, k, r, c, criterion="modes", use_graphs=True, comm=None,
+                 row_offset=0, m_total=None):
         self.A = A
         self.n = A.ncols
         self.c = int(c)
         gcap = min(self.c, A.ncols)
-        super().__init__(ctx, A.m, r, k=k, criterion=criterion, upd_cap=gcap)
+        super().__init__(ctx, A.m, r, k=k, criterion=criterion, upd_cap=gcap, comm=comm,
+                         row_offset=row_offset)
+        self.m_total = A.m if m_total is None else int(m_total)
         dev = ctx.device
         f64 = dict(dtype=torch.float64, device=dev)
         n, r, g = self.n, self.r, gcap
@@ -237,6 +280,8 @@ class IsmaEngine(MergeWorkspace):
     def norm_pass(self):
         """Fused validate + column norms (matcore.py:54, isma.py:260)."""
         self.ctx.colnorms2(self.A, self.norms2, self.nonfinite)
+        self.comm.allreduce_sum_(self.norms2)
+        self.comm.allreduce_max_(self.nonfinite)
         flag = int(self.nonfinite.item())
         if flag:
             raise ParameterError("matrix contains non-finite entries")
@@ -252,6 +297,7 @@ class IsmaEngine(MergeWorkspace):
                  self.c, self.idx, self.cnt, info=self.rec[REC_G:])
         ctx.tn(g, g, 1.0, A, A, dptr(self.G), g, xcols=self.idx, ycols=self.idx,
                tag="tn_gram_gather")                                         # baselines.py:43
+        self.comm.allreduce_sum_(self.G)
         ctx.gram_eigh(dptr(self.G), g, g, r, self.sig_upd, dptr(self.Tl), g,
                       info=self.rec[REC_RANK:])                                   # baselines:44-48
         ctx.nn(g, r, 1.0, A, dptr(self.Tl), g, dest, xcols=self.idx,
@@ -264,7 +310,7 @@ class IsmaEngine(MergeWorkspace):
         self.readback()
 
     def launch_round(self, mode, cur):
-        if not self.use_graphs or self.ctx.prof is not None:
+        if not self.use_graphs or self.ctx.prof is not None or self.comm.active:
             self.round_ops(mode, cur)
             return
         key = (mode, cur)
@@ -301,9 +347,10 @@ class IsmaEngine(MergeWorkspace):
         U = self.S[self.cur].cols(0, r)
         Cm = ColMat.zeros(n, r, dev)
         ctx.tn(n, r, 1.0, self.A, U, Cm.ptr, n, tag="tn_finalize_AtU")      # A^T U
+        self.comm.allreduce_sum_(Cm.t)
         Qc = ColMat.zeros(n, r, dev)
         Rc = torch.zeros(r * r, dtype=torch.float64, device=dev)
-        self.cholqr_ops(Cm, Qc, r, Rc, G_FQR)
+        self.cholqr_ops(Cm, Qc, r, Rc, G_FQR, sharded=False)  # A^T U is replicated
         Ur = torch.zeros(r * r, dtype=torch.float64, device=dev)
         Vr = torch.zeros(r * r, dtype=torch.float64, device=dev)
         sr = torch.zeros(r, dtype=torch.float64, device=dev)
@@ -313,7 +360,7 @@ class IsmaEngine(MergeWorkspace):
         ctx.nn(r, r, 1.0, U, dptr(Vr), r, Unew, tag="nn_finalize_rot")      # u @ vrt.T
         Vnew = ColMat.zeros(n, r, dev)
         ctx.nn(r, r, 1.0, Qc, dptr(Ur), r, Vnew, tag="nn_finalize_rot")     # q @ ur
-        ctx.fix_signs(Unew, r, Vnew, n)
+        self.fix_signs_ops(Unew, r, Vnew, n)
         self.sig[nxt].copy_(sr)
         self.cur = nxt
         return Vnew
@@ -367,12 +414,12 @@ class IsmaEngine(MergeWorkspace):
         if finalize and self.l:
             v = self.finalize()
         elif self.l:
-            self.ctx.fix_signs(self.S[self.cur].cols(0, self.l), self.l)
+            self.fix_signs_ops(self.S[self.cur].cols(0, self.l), self.l)
         return traces, v
 
     def result(self, keep, v=None):
         l = min(self.l, keep)
-        u = self.S[self.cur].to_numpy(l) if l else np.zeros((self.m, 0))
+        u = self.gather_rows(self.S[self.cur], l, self.m_total) if l else np.zeros((self.m_total, 0))
         s = self.sig[self.cur][:l].cpu().numpy().copy()
         vv = None if v is None else (v.to_numpy(l) if l else np.zeros((self.n, 0)))
         return u, s, vv
@@ -381,20 +428,22 @@ class IsmaEngine(MergeWorkspace):
 _ENGINE_CACHE = {}
 
 
-def get_engine(ctx, A, *, k, r, c, criterion, use_graphs):
+def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=0, m_total=None):
     """Reuse the engine (buffers + captured round graphs) of the previous run
     when the matrix buffer, shape and configuration match; one engine is
     cached per device.  Graph replay reads A and the staged uniforms at
     replay time, so a reused engine is valid for new contents of A."""
+    world = 1 if comm is None else comm.world
     key = (A.t.data_ptr() + 8 * A.ld * A.col0, A.m, A.ncols, A.ld, int(k), int(r), int(c),
-           criterion, bool(use_graphs), ctx.device.index)
+           criterion, bool(use_graphs), ctx.device.index, world, int(row_offset), m_total)
     eng = _ENGINE_CACHE.get(ctx.device.index)
     if eng is not None and eng.key == key:
         eng.A = A
         eng.reset()
         return eng
     _ENGINE_CACHE.pop(ctx.device.index, None)
-    eng = IsmaEngine(ctx, A, k=k, r=r, c=c, criterion=criterion, use_graphs=use_graphs)
+    eng = IsmaEngine(ctx, A, k=k, r=r, c=c, criterion=criterion, use_graphs=use_graphs,
+                     comm=comm, row_offset=row_offset, m_total=m_total)
     eng.key = key
     _ENGINE_CACHE[ctx.device.index] = eng
     return eng

@@ -129,19 +129,35 @@ def _validate_shape(a):
 
 
 def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False,
-             use_graphs=True):
+             use_graphs=True, comm=None, m_total=None):
     """Run the full iteration (isma.py:225-303) on the GPU.
 
     ``a`` may be a numpy array (copied host->device), a CUDA torch tensor
     or a ``device.ColMat`` (used in place).  Returns ``(TruncatedFactor,
     list[IterationTrace])`` exactly as the reference.
+
+    Row-sharded multi-GPU (parallel.py): pass ``comm=parallel.Comm()`` and
+    this rank's row block ``a`` = A[r0:r1] with r0, r1 = shard_rows(m_total,
+    world, rank); every rank must use an identically seeded generator.  The
+    returned factor is the full (gathered) one on every rank.
     """
     from .device import get_ctx, to_device_colmajor
     from .engine import get_engine
     from .matcore import TruncatedFactor
 
+    from .parallel import Comm, shard_rows
+
     _require_column_path(config)
     a, m, n = _validate_shape(a)
+    comm = comm if comm is not None else Comm()
+    row_offset = 0
+    if comm.active:
+        if m_total is None:
+            raise ParameterError("row-sharded isma_run needs m_total")
+        r0, r1 = shard_rows(int(m_total), comm.world, comm.rank)
+        if r1 - r0 != m:
+            raise ParameterError(f"rank {comm.rank} holds {m} rows, expected {r1 - r0}")
+        row_offset, m = r0, int(m_total)
     k = config.k
     if k > min(m, n):
         raise ParameterError(f"k={k} exceeds min(m, n)={min(m, n)}")
@@ -153,7 +169,8 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
     ctx = get_ctx(device)
     A = to_device_colmajor(a, ctx.device)
     eng = get_engine(ctx, A, k=k, r=config.r, c=config.column_budget(),
-                     criterion=config.criterion, use_graphs=use_graphs)
+                     criterion=config.criterion, use_graphs=use_graphs, comm=comm,
+                     row_offset=row_offset, m_total=m if comm.active else None)
     traces, v = eng.run(rng, strategy=config.strategy, tau=config.tau,
                         finalize=config.finalize, keep=keep, trace_cls=IterationTrace)
     u, s, vv = eng.result(keep, v)

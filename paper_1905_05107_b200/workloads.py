@@ -50,36 +50,49 @@ def _fourier_modes(seed, nmodes=40, kmax=12):
     return np.array(out, dtype=np.float64)
 
 
-def config2_torch(seed=0, side=512, n=2000, noise_var=1e-4, device="cpu",
-                  nmodes=40):
-    """BASELINE config 2 snapshot matrix as a column-major float64 torch
-    tensor of logical shape (m, n) (storage: n x m row-major, i.e. A^T
-    contiguous).  Deterministic for a (seed, device type) pair."""
+NOISE_CHUNK = 4096  # rows per independently seeded noise chunk (shard-invariant A)
+
+
+def config2_torch(seed=0, side=512, n=2000, noise_var=1e-4, device="cpu", nmodes=40,
+                  rows=None):
+    """BASELINE config 2 snapshot matrix rows [r0, r1) (default: all m rows)
+    as a column-major float64 torch tensor: storage (n, r1 - r0), i.e. the
+    row block's transpose is contiguous.  The noise of global rows
+    [c*4096, (c+1)*4096) comes from a generator seeded by (seed, c), so any
+    row partition (one GPU or a row-sharded multi-GPU run) produces the same
+    matrix.  Deterministic for a (seed, device type) pair."""
     import torch
 
     m = side * side
+    r0, r1 = (0, m) if rows is None else (int(rows[0]), int(rows[1]))
     modes = _fourier_modes(seed, nmodes)
+    dt = torch.float64
     gen = torch.Generator(device=device)
     gen.manual_seed(int(seed) * 7919 + 17)
-    dt = torch.float64
-    yy, xx = torch.meshgrid(torch.arange(side, dtype=dt, device=device),
-                            torch.arange(side, dtype=dt, device=device),
-                            indexing="ij")
-    x = xx.reshape(-1)
-    y = yy.reshape(-1)
-    kx = torch.tensor(modes[:, 0], dtype=dt, device=device)
-    ky = torch.tensor(modes[:, 1], dtype=dt, device=device)
-    theta = (2.0 * math.pi / side) * (x[:, None] * kx[None, :] + y[:, None] * ky[None, :])
-    basis = torch.cat([torch.cos(theta), torch.sin(theta)], dim=1)  # m x 2J
     amp = torch.arange(1, nmodes + 1, dtype=dt, device=device) ** -2.0
     phi = 2.0 * math.pi * torch.rand((nmodes, n), generator=gen, dtype=dt, device=device)
     coef = torch.cat([amp[:, None] * torch.cos(phi), -amp[:, None] * torch.sin(phi)], dim=0)
-    at = (basis @ coef).T.contiguous()  # n x m storage == A column-major
-    del basis, theta
-    at.add_(torch.randn(at.shape, generator=gen, dtype=dt, device=device),
-            alpha=math.sqrt(noise_var))
-    at.sub_(at.mean(dim=0, keepdim=True))  # subtract each row's mean of A
-    return at  # A = at.T
+    kx = torch.tensor(modes[:, 0], dtype=dt, device=device)
+    ky = torch.tensor(modes[:, 1], dtype=dt, device=device)
+    sd = math.sqrt(noise_var)
+    at = torch.empty((n, r1 - r0), dtype=dt, device=device)
+    # every quantity is computed per global 4096-row chunk (identical shapes
+    # whatever the row partition), then the requested rows are sliced out
+    for c in range(r0 // NOISE_CHUNK, (r1 + NOISE_CHUNK - 1) // NOISE_CHUNK):
+        c0, c1 = c * NOISE_CHUNK, min(m, (c + 1) * NOISE_CHUNK)
+        idx = torch.arange(c0, c1, dtype=torch.int64, device=device)
+        x = (idx % side).to(dt)
+        y = (idx // side).to(dt)
+        theta = (2.0 * math.pi / side) * (x[:, None] * kx[None, :] + y[:, None] * ky[None, :])
+        basis = torch.cat([torch.cos(theta), torch.sin(theta)], dim=1)  # chunk x 2J
+        blk = (basis @ coef).T.contiguous()  # (n, chunk)
+        g = torch.Generator(device=device)
+        g.manual_seed((int(seed) * 1000003 + c * 7 + 3) % (2 ** 62))
+        blk.add_(torch.randn((n, c1 - c0), generator=g, dtype=dt, device=device), alpha=sd)
+        blk.sub_(blk.mean(dim=0, keepdim=True))  # subtract each row's mean
+        lo, hi = max(c0, r0), min(c1, r1)
+        at[:, lo - r0:hi - r0].copy_(blk[:, lo - c0:hi - c0])
+    return at
 
 
 def config2(seed=0, side=512, n=2000, noise_var=1e-4):

@@ -1,0 +1,101 @@
+"""World-size-2 gloo tests (CPU) of the row-sharded collective protocol
+(parallel.py): partial reductions over row shards, the global sign
+convention, and the row gather."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import isma_oracle as orc
+from paper_1905_05107_b200.parallel import Comm, combine_signs, gather_row_shards, shard_rows
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, fn, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        q.put((rank, fn(Comm())))
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world(fn, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, fn, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return [out[r] for r in range(world)]
+
+
+def test_shard_rows_partition():
+    for m in (1, 7, 100, 262144):
+        for w in (1, 2, 3, 8):
+            bounds = [shard_rows(m, w, r) for r in range(w)]
+            assert bounds[0][0] == 0 and bounds[-1][1] == m
+            assert all(b[1] == c[0] for b, c in zip(bounds, bounds[1:]))
+
+
+def _gram_and_signs(comm):
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((101, 7))
+    a[40, 3] = -9.0  # global max of column 3 on rank 0's shard (negative)
+    a[77, 3] = 9.0   # tie on rank 1's shard: the lower row (40) must win
+    r0, r1 = shard_rows(101, comm.world, comm.rank)
+    loc = torch.as_tensor(a[r0:r1])
+    g = loc.T @ loc
+    comm.allreduce_sum_(g)
+    absl = loc.abs()
+    val, arg = absl.max(0)
+    # first occurrence on ties inside the shard
+    arg = torch.tensor([int(np.argmax(absl[:, j].numpy())) for j in range(7)])
+    sign = torch.where(loc[arg, torch.arange(7)] < 0, -1.0, 1.0).double()
+    s = combine_signs(comm.allgather(val.double()), comm.allgather(arg + r0), comm.allgather(sign))
+    full = gather_row_shards(loc.T.contiguous(), 101, comm)
+    return g.numpy(), s.numpy(), full
+
+
+def test_partial_grams_signs_and_gather_over_two_ranks():
+    res = run_world(_gram_and_signs, 2)
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((101, 7))
+    a[40, 3] = -9.0
+    a[77, 3] = 9.0
+    _, flip = orc.canon_signs(a, np.eye(7))
+    want = np.where(np.diag(flip) < 0, -1.0, 1.0)
+    for g, s, full in res:
+        np.testing.assert_allclose(g, a.T @ a, rtol=1e-13)
+        np.testing.assert_array_equal(s, want)
+        np.testing.assert_array_equal(full, a)
+    # every rank holds bitwise identical reductions (identical decisions)
+    assert np.array_equal(res[0][0], res[1][0])
+
+
+def test_config2_generator_is_shard_invariant():
+    from paper_1905_05107_b200 import workloads
+
+    full = workloads.config2_torch(3, side=96, n=25)
+    m = 96 * 96
+    for world in (2, 3):
+        parts = [workloads.config2_torch(3, side=96, n=25, rows=shard_rows(m, world, r))
+                 for r in range(world)]
+        assert torch.equal(full, torch.cat(parts, 1))

@@ -1,0 +1,72 @@
+"""Row-sharded isma_run on real kernels: two processes share the GPU and
+exchange through gloo (host-mediated collectives; no kernel waits on another
+rank), checked against the unsharded single-process run."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+from parity_util import ANGLE_TOL_RAD, SIGMA_RTOL, principal_angles_sin, sigma_relerr  # noqa: E402
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, crit, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import paper_1905_05107_b200 as pod
+    from paper_1905_05107_b200 import workloads
+    from paper_1905_05107_b200.parallel import Comm, shard_rows
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = workloads.config1(seed=0)
+        r0, r1 = shard_rows(a.shape[0], world, rank)
+        cfg = pod.IsmaConfig(k=10, r=30, c=50, tau=0.999, strategy="l2n", criterion=crit, seed=7)
+        f, tr = pod.isma_run(np.asfortranarray(a[r0:r1]), cfg, comm=Comm(), m_total=a.shape[0])
+        q.put((rank, (f.u, f.sigma, f.v, [t.remaining for t in tr])))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("crit", ["modes", "subspace"])
+def test_two_rank_row_sharded_run_matches_single_gpu(crit):
+    import paper_1905_05107_b200 as pod
+    from paper_1905_05107_b200 import workloads
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, crit, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a = workloads.config1(seed=0)
+    cfg = pod.IsmaConfig(k=10, r=30, c=50, tau=0.999, strategy="l2n", criterion=crit, seed=7)
+    f, tr = pod.isma_run(a, cfg)
+    for rank in (0, 1):
+        u, s, v, rem = res[rank]
+        assert rem == [t.remaining for t in tr]
+        assert sigma_relerr(s, f.sigma) <= SIGMA_RTOL
+        assert principal_angles_sin(u, f.u).max() <= ANGLE_TOL_RAD
+        assert principal_angles_sin(v, f.v).max() <= ANGLE_TOL_RAD
+    np.testing.assert_array_equal(res[0][1], res[1][1])  # identical on every rank
