@@ -221,7 +221,7 @@ def main():
     ws, rank, local = _dist_env()
     comm = None
     if ws > 1:
-        torch.cuda.set_device(local)
+        torch.cuda.set_device(local % torch.cuda.device_count())
         import torch.distributed as dist
 
         dist.init_process_group(os.environ.get("POD_DIST_BACKEND", "nccl"))

@@ -22,7 +22,7 @@ namespace cg = cooperative_groups;
 
 namespace pod {
 
-constexpr int CL = 8;              // cluster size (portable maximum)
+constexpr int CL_MAX = 8;          // cluster size (portable maximum)
 constexpr int CJ_THREADS = 256;
 constexpr int CJ_MAX_N = 512;      // columns
 
@@ -43,6 +43,7 @@ struct CJScratch {
   double* body;   // matrix storage after the scratch
 };
 
+template <int CL>
 __host__ __device__ inline size_t cj_scratch_bytes(int n) {
   const int np = (n + 1) / 2;
   size_t b = (size_t)(2 + 2 * CL * np + CL * n + n + 2 * np + n) * sizeof(double);
@@ -50,6 +51,7 @@ __host__ __device__ inline size_t cj_scratch_bytes(int n) {
   return (b + 15) & ~(size_t)15;
 }
 
+template <int CL>
 __device__ inline CJScratch cj_carve(double* base, int n) {
   const int np = (n + 1) / 2;
   CJScratch s;
@@ -67,7 +69,7 @@ __device__ inline CJScratch cj_carve(double* base, int n) {
   int* ip = reinterpret_cast<int*>(q);
   s.perm = ip; ip += n;
   s.flags = ip;
-  s.body = reinterpret_cast<double*>(reinterpret_cast<char*>(base) + cj_scratch_bytes(n));
+  s.body = reinterpret_cast<double*>(reinterpret_cast<char*>(base) + cj_scratch_bytes<CL>(n));
   return s;
 }
 
@@ -104,7 +106,7 @@ __device__ __forceinline__ void mbar_init(uint64_t* mb, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(count));
 }
 __device__ __forceinline__ void mbar_arrive_expect(uint64_t* mb, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n"
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n"
                ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
@@ -121,6 +123,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
 
 // Exchange per-column partial squared norms of the local rows and sum them
 // in rank order (identical result in every CTA).  Includes cluster barriers.
+template <int CL>
 __device__ void cj_norms(cg::cluster_group& cl, const CJScratch& s, const double* Wl, int ldl, int nrl,
                          int nc) {
   const int me = (int)cl.block_rank();
@@ -147,7 +150,23 @@ __device__ void cj_norms(cg::cluster_group& cl, const CJScratch& s, const double
 // One-sided cyclic Jacobi (round-robin pairs) on W distributed by rows.
 // Wl: this CTA's nrl rows (ld ldl) of all nc columns; Jl (nullable): this
 // CTA's njl rows (ld ldj) of the nc x nc accumulator.  Returns sweeps.
-template <int RPL>
+#ifdef POD_CJ_TIMING
+__device__ unsigned long long g_cj_phase[8];
+#define CJ_T(i)                                                              \
+  do {                                                                       \
+    if (threadIdx.x == 0 && cl.block_rank() == 0) {                          \
+      unsigned long long _t = clock64();                                     \
+      if (i) atomicAdd(&g_cj_phase[i], _t - _cj_last);                      \
+      _cj_last = _t;                                                         \
+    }                                                                        \
+  } while (0)
+#else
+#define CJ_T(i) \
+  do {          \
+  } while (0)
+#endif
+
+template <int CL, int RPL>
 __device__ int cj_jacobi_t(cg::cluster_group& cl, const CJScratch& s, double* Wl, int ldl, int nrl,
                            int nc, double* Jl, int ldj, int njl, double tol, int max_sweeps) {
   const int me = (int)cl.block_rank();
@@ -180,14 +199,18 @@ __device__ int cj_jacobi_t(cg::cluster_group& cl, const CJScratch& s, double* Wl
   }
   cl.sync();  // every CTA's barriers are initialised before any st.async
   if (nc < 2) {
-    cj_norms(cl, s, Wl, ldl, nrl, nc);
+    cj_norms<CL>(cl, s, Wl, ldl, nrl, nc);
     return 0;
   }
   while (sweep < max_sweeps) {
-    cj_norms(cl, s, Wl, ldl, nrl, nc);
+    cj_norms<CL>(cl, s, Wl, ldl, nrl, nc);
     if (threadIdx.x == 0) s.flags[0] = 0;
     __syncthreads();
+#ifdef POD_CJ_TIMING
+    unsigned long long _cj_last = clock64();
+#endif
     for (int step = 0; step < M1; ++step, ++gstep) {
+      CJ_T(0);
       parity = (int)(gstep & 1u);
       if (threadIdx.x == 0) mbar_arrive_expect(&s.mbar[parity], tx_bytes);
       // pair of this thread group (every lane takes part in the shuffles)
@@ -225,13 +248,16 @@ __device__ int cj_jacobi_t(cg::cluster_group& cl, const CJScratch& s, double* Wl
         for (int i = gl; i < nrl; i += tpp) g = fma(wa[i], wb[i], g);
       }
       for (int o = tpp / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o, tpp);
-      if (valid && gl == 0) {
+      if (valid) {  // the pair's lanes share the CL remote stores
         const uint32_t off = (uint32_t)(((parity * CL + me) * npairs + pr) * sizeof(double));
         const uint32_t moff = (uint32_t)(parity * sizeof(uint64_t));
 #pragma unroll
-        for (int c = 0; c < CL; ++c) st_async_f64(rpart[c] + off, g, rmbar[c] + moff);
+        for (int c = 0; c < CL; ++c)
+          if ((c % tpp) == gl) st_async_f64(rpart[c] + off, g, rmbar[c] + moff);
       }
+      CJ_T(1);
       mbar_wait(&s.mbar[parity], (gstep >> 1) & 1u);
+      CJ_T(2);
       // 2. full gamma (rank-ordered sum: identical in every CTA) and the
       //    rotation, computed redundantly by the pair's own lanes
       if (live) {
@@ -246,7 +272,9 @@ __device__ int cj_jacobi_t(cg::cluster_group& cl, const CJScratch& s, double* Wl
           const double d = be - al;
           const double rh = rsqrt_nr2(fma(d, d, 4.0 * gg * gg));
           const double x = 0.5 * fma(fabs(d), rh, 1.0);
-          const double ic = rsqrt_nr2(x);
+          double ic = (double)rsqrtf((float)x);  // x in [0.5, 1]: fp32 seed is in range
+          ic = ic * fma(-0.5 * x, ic * ic, 1.5);
+          ic = ic * fma(-0.5 * x, ic * ic, 1.5);
           const double c_ = x * ic;
           const double s_ = copysign(fabs(gg) * rh * ic, d * gg);
           if (RPL > 0) {
@@ -274,6 +302,7 @@ __device__ int cj_jacobi_t(cg::cluster_group& cl, const CJScratch& s, double* Wl
               jb[i] = fma(s_, x0, c_ * y0);
             }
           }
+          CJ_T(3);
           if (gl == 0) {
             const double c2 = c_ * c_, s2 = s_ * s_, csg = 2.0 * c_ * s_ * gg;
             s.nrm2[a] = fmax(fma(c2, al, fma(s2, be, -csg)), 0.0);
@@ -282,27 +311,30 @@ __device__ int cj_jacobi_t(cg::cluster_group& cl, const CJScratch& s, double* Wl
           }
         }
       }
+      CJ_T(4);
       __syncthreads();
+      CJ_T(5);
     }
     ++sweep;
     const int any = s.flags[0];  // identical in every CTA
     __syncthreads();
     if (!any) break;
   }
-  cj_norms(cl, s, Wl, ldl, nrl, nc);  // exact final norms
+  cj_norms<CL>(cl, s, Wl, ldl, nrl, nc);  // exact final norms
   return sweep;
 }
 
+template <int CL>
 __device__ int cj_jacobi(cg::cluster_group& cl, const CJScratch& s, double* Wl, int ldl, int nrl,
                          int nc, double* Jl, int ldj, int njl, double tol, int max_sweeps) {
   const int np = (nc + (nc & 1)) / 2;
   int tpp = 1;
   while (tpp * 2 * np <= (int)blockDim.x && tpp < 16) tpp *= 2;
   const int rpl = (nrl + tpp - 1) / tpp;
-  if (rpl <= 4) return cj_jacobi_t<4>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
-  if (rpl <= 8) return cj_jacobi_t<8>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
-  if (rpl <= 16) return cj_jacobi_t<16>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
-  return cj_jacobi_t<0>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
+  if (rpl <= 4) return cj_jacobi_t<CL, 4>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
+  if (rpl <= 8) return cj_jacobi_t<CL, 8>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
+  if (rpl <= 16) return cj_jacobi_t<CL, 16>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
+  return cj_jacobi_t<CL, 0>(cl, s, Wl, ldl, nrl, nc, Jl, ldj, njl, tol, max_sweeps);
 }
 
 // perm[k] = column with the k-th largest key (ties -> lower index)
@@ -324,7 +356,8 @@ __device__ __forceinline__ double cj_tol(int nr) { return 2.220446049250313e-16 
 // ------------------------------------------------------------ merge core --
 // E (n x n, n = l1 + l2) built row-locally; U_E = W / sigma row-local; T rows
 // in the stack layout [U1 (rcap) | Q (l2)].
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CJ_THREADS)
+template <int CL>
+__global__ void __launch_bounds__(CJ_THREADS)
     cj_merge_core_kernel(const double* __restrict__ sig1, int l1, const double* __restrict__ M,
                          int64_t ldm, const double* __restrict__ Rm, int64_t ldr,
                          const double* __restrict__ sig2, int l2, int r, int rcap,
@@ -334,7 +367,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CJ_THREADS)
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double smem_cj[];
   const int n = l1 + l2;
-  const CJScratch s = cj_carve(smem_cj, n);
+  const CJScratch s = cj_carve<CL>(smem_cj, n);
   double* Wl = s.body;  // nrl x n, ld nrl
   const int me = (int)cl.block_rank();
   const int r0 = me * nrl;
@@ -357,7 +390,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CJ_THREADS)
   }
   __syncthreads();
   const int nrl_eff = max(0, min(nrl, n - r0));
-  const int sweeps = cj_jacobi(cl, s, Wl, nrl, nrl_eff, n, nullptr, 0, 0, cj_tol(n), max_sweeps);
+  const int sweeps = cj_jacobi<CL>(cl, s, Wl, nrl, nrl_eff, n, nullptr, 0, 0, cj_tol(n), max_sweeps);
   for (int j = threadIdx.x; j < n; j += blockDim.x) s.nrm2[j] = sqrt(s.nrm2[j]);  // sigma
   __syncthreads();
   cj_rank_sort(s.nrm2, n, s.perm);
@@ -402,14 +435,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CJ_THREADS)
 // Input: X = R^T (g x g, ld g, columns >= rank zero) from the pivoted
 // Cholesky P G P^T = R^T R, and piv.  One-sided Jacobi on X's columns gives
 // X J = V' Sigma -> lambda = ||col||^2, eigenvector rows v'[i] row-local.
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CJ_THREADS)
+template <int CL>
+__global__ void __launch_bounds__(CJ_THREADS)
     cj_gram_eigh_kernel(const double* __restrict__ X, const int* __restrict__ piv,
                         const int64_t* __restrict__ rank_in, int g, int r,
                         double* __restrict__ sigma_out, double* __restrict__ T, int64_t ldt,
                         int64_t* __restrict__ info, int nrl, int max_sweeps) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double smem_cj[];
-  const CJScratch s = cj_carve(smem_cj, g);
+  const CJScratch s = cj_carve<CL>(smem_cj, g);
   double* Wl = s.body;  // nrl x g
   const int me = (int)cl.block_rank();
   const int r0 = me * nrl;
@@ -420,10 +454,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CJ_THREADS)
   }
   __syncthreads();
   const int nrl_eff = max(0, min(nrl, g - r0));
-  const int sweeps = rank >= 2 ? cj_jacobi(cl, s, Wl, nrl, nrl_eff, rank, nullptr, 0, 0,
+  const int sweeps = rank >= 2 ? cj_jacobi<CL>(cl, s, Wl, nrl, nrl_eff, rank, nullptr, 0, 0,
                                            cj_tol(g), max_sweeps)
                                : 0;
-  if (rank < 2) cj_norms(cl, s, Wl, nrl, nrl_eff, rank);
+  if (rank < 2) cj_norms<CL>(cl, s, Wl, nrl, nrl_eff, rank);
   // s.nrm2[j] = lambda_j (squared column norm) for j < rank
   for (int j = rank + threadIdx.x; j < g; j += blockDim.x) s.nrm2[j] = 0.0;
   __syncthreads();
@@ -468,14 +502,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CJ_THREADS)
 }
 
 // ------------------------------------------------------------- svd small --
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CJ_THREADS)
+template <int CL>
+__global__ void __launch_bounds__(CJ_THREADS)
     cj_svd_kernel(const double* __restrict__ A, int64_t lda, int nr, int nc,
                   double* __restrict__ U, int64_t ldu, double* __restrict__ sigma,
                   double* __restrict__ V, int64_t ldv, int64_t* __restrict__ info, int nrl,
                   int njl, int max_sweeps) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double smem_cj[];
-  const CJScratch s = cj_carve(smem_cj, nc);
+  const CJScratch s = cj_carve<CL>(smem_cj, nc);
   double* Wl = s.body;                                   // nrl x nc
   double* Jl = V ? s.body + (size_t)nrl * nc : nullptr;  // njl x nc (rows of J)
   const int me = (int)cl.block_rank();
@@ -492,7 +527,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CJ_THREADS)
   __syncthreads();
   const int nrl_eff = max(0, min(nrl, nr - r0));
   const int njl_eff = max(0, min(njl, nc - j0));
-  const int sweeps = cj_jacobi(cl, s, Wl, nrl, nrl_eff, nc, Jl, njl, njl_eff, cj_tol(nr),
+  const int sweeps = cj_jacobi<CL>(cl, s, Wl, nrl, nrl_eff, nc, Jl, njl, njl_eff, cj_tol(nr),
                                max_sweeps);
   for (int j = threadIdx.x; j < nc; j += blockDim.x) s.nrm2[j] = sqrt(s.nrm2[j]);
   __syncthreads();
@@ -548,49 +583,119 @@ static int cj_set_smem(const void* fn, size_t bytes) {
   return POD_OK;
 }
 
+template <typename K, typename... Args>
+static int cj_launch(K kernel, int cl, int threads, size_t smem, cudaStream_t stream,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  return e == cudaSuccess ? POD_OK : cuda_status(e, "cluster launch");
+}
+
+// Cluster size: 8 CTAs by default (POD_CJ_CLUSTER=2|4|8 overrides, for tuning).
+static int cj_cluster() {
+  static int cl = 0;
+  if (!cl) {
+    const char* e = getenv("POD_CJ_CLUSTER");
+    int v = e ? atoi(e) : 8;
+    cl = (v == 2 || v == 4 || v == 8) ? v : 8;
+  }
+  return cl;
+}
+
+template <int CL>
+static int cj_merge_core_t(const double* sig1, int64_t l1, const double* M, int64_t ldm,
+                           const double* R, int64_t ldr, const double* sig2, int64_t l2, int64_t r,
+                           int64_t rcap, double* T, int64_t ldt, int64_t tcols, double* sig_new,
+                           int64_t* info, cudaStream_t stream) {
+  const int n = (int)(l1 + l2);
+  const int nrl = (n + CL - 1) / CL;
+  const size_t bytes = cj_scratch_bytes<CL>(n) + (size_t)nrl * n * sizeof(double);
+  int st = cj_set_smem((const void*)cj_merge_core_kernel<CL>, bytes);
+  if (st) return st;
+  return cj_launch(cj_merge_core_kernel<CL>, CL, cj_threads(n), bytes, stream, sig1, (int)l1, M,
+                   ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new,
+                   info, nrl, 60);
+}
+
 int cj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
                   int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
                   int64_t ldt, int64_t tcols, double* sig_new, int64_t* info,
                   cudaStream_t stream) {
   const int n = (int)(l1 + l2);
   POD_REQUIRE(n <= CJ_MAX_N, "merge core: l1 + l2 = %d exceeds %d", n, CJ_MAX_N);
-  const int nrl = (n + CL - 1) / CL;
-  const size_t bytes = cj_scratch_bytes(n) + (size_t)nrl * n * sizeof(double);
-  int st = cj_set_smem((const void*)cj_merge_core_kernel, bytes);
+  switch (cj_cluster()) {
+    case 2: return cj_merge_core_t<2>(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info, stream);
+    case 4: return cj_merge_core_t<4>(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info, stream);
+    default: return cj_merge_core_t<8>(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info, stream);
+  }
+}
+
+template <int CL>
+static int cj_gram_eigh_t(const double* X, const int* piv, const int64_t* rank, int64_t g,
+                          int64_t r, double* sigma, double* T, int64_t ldt, int64_t* info,
+                          cudaStream_t stream) {
+  const int nrl = (int)((g + CL - 1) / CL);
+  const size_t bytes = cj_scratch_bytes<CL>((int)g) + (size_t)nrl * g * sizeof(double);
+  int st = cj_set_smem((const void*)cj_gram_eigh_kernel<CL>, bytes);
   if (st) return st;
-  cj_merge_core_kernel<<<CL, cj_threads(n), bytes, stream>>>(sig1, (int)l1, M, ldm, R, ldr, sig2,
-                                                           (int)l2, (int)r, (int)rcap, T, ldt,
-                                                           (int)tcols, sig_new, info, nrl, 60);
-  POD_CHECK_LAUNCH("cluster merge core");
-  return POD_OK;
+  return cj_launch(cj_gram_eigh_kernel<CL>, CL, cj_threads((int)g), bytes, stream, X, piv, rank,
+                   (int)g, (int)r, sigma, T, ldt, info, nrl, 60);
 }
 
 int cj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t g, int64_t r,
                  double* sigma, double* T, int64_t ldt, int64_t* info, cudaStream_t stream) {
   POD_REQUIRE(g <= CJ_MAX_N, "gram eigh: g = %lld exceeds %d", (long long)g, CJ_MAX_N);
-  const int nrl = (int)((g + CL - 1) / CL);
-  const size_t bytes = cj_scratch_bytes((int)g) + (size_t)nrl * g * sizeof(double);
-  int st = cj_set_smem((const void*)cj_gram_eigh_kernel, bytes);
+  switch (cj_cluster()) {
+    case 2: return cj_gram_eigh_t<2>(X, piv, rank, g, r, sigma, T, ldt, info, stream);
+    case 4: return cj_gram_eigh_t<4>(X, piv, rank, g, r, sigma, T, ldt, info, stream);
+    default: return cj_gram_eigh_t<8>(X, piv, rank, g, r, sigma, T, ldt, info, stream);
+  }
+}
+
+template <int CL>
+static int cj_svd_t(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int64_t ldu,
+                    double* sigma, double* V, int64_t ldv, int64_t* info, cudaStream_t stream) {
+  const int nrl = (int)((nr + CL - 1) / CL);
+  const int njl = V ? (int)((nc + CL - 1) / CL) : 0;
+  const size_t bytes =
+      cj_scratch_bytes<CL>((int)nc) + ((size_t)nrl * nc + (size_t)njl * nc) * sizeof(double);
+  int st = cj_set_smem((const void*)cj_svd_kernel<CL>, bytes);
   if (st) return st;
-  cj_gram_eigh_kernel<<<CL, cj_threads((int)g), bytes, stream>>>(X, piv, rank, (int)g, (int)r, sigma, T,
-                                                          ldt, info, nrl, 60);
-  POD_CHECK_LAUNCH("cluster gram eigh");
-  return POD_OK;
+  return cj_launch(cj_svd_kernel<CL>, CL, cj_threads((int)nc), bytes, stream, A, lda, (int)nr,
+                   (int)nc, U, ldu, sigma, V, ldv, info, nrl, njl, 60);
 }
 
 int cj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int64_t ldu,
            double* sigma, double* V, int64_t ldv, int64_t* info, cudaStream_t stream) {
   POD_REQUIRE(nc <= CJ_MAX_N && nr <= 4096, "svd small: %lld x %lld too large", (long long)nr,
               (long long)nc);
-  const int nrl = (int)((nr + CL - 1) / CL);
-  const int njl = V ? (int)((nc + CL - 1) / CL) : 0;
-  const size_t bytes = cj_scratch_bytes((int)nc) + ((size_t)nrl * nc + (size_t)njl * nc) * sizeof(double);
-  int st = cj_set_smem((const void*)cj_svd_kernel, bytes);
-  if (st) return st;
-  cj_svd_kernel<<<CL, cj_threads((int)nc), bytes, stream>>>(A, lda, (int)nr, (int)nc, U, ldu, sigma, V,
-                                                    ldv, info, nrl, njl, 60);
-  POD_CHECK_LAUNCH("cluster svd");
-  return POD_OK;
+  switch (cj_cluster()) {
+    case 2: return cj_svd_t<2>(A, lda, nr, nc, U, ldu, sigma, V, ldv, info, stream);
+    case 4: return cj_svd_t<4>(A, lda, nr, nc, U, ldu, sigma, V, ldv, info, stream);
+    default: return cj_svd_t<8>(A, lda, nr, nc, U, ldu, sigma, V, ldv, info, stream);
+  }
 }
 
 }  // namespace pod
+
+#ifdef POD_CJ_TIMING
+extern "C" int pod_debug_cj_phase(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, pod::g_cj_phase, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(pod::g_cj_phase, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
