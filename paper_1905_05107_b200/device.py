@@ -84,6 +84,7 @@ class Ctx:
         self.h_dinfo = torch.zeros(16, dtype=torch.float64).pin_memory()
         self.launches = 0      # kernels launched through this context
         self.prof = None       # KernelProfile when instrumenting
+        self.ws_suffix = ""    # workspace namespace of the stream being issued to
 
     def _call(self, name, nlaunch, flops, nbytes, fn, *args):
         """Invoke one ABI entry point; count its kernel launches and, when a
@@ -106,6 +107,7 @@ class Ctx:
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
     def ws(self, key, nbytes):
+        key = key + self.ws_suffix  # separate workspaces per concurrent stream
         nbytes = max(int(nbytes), 256)
         buf = self._ws.get(key)
         if buf is None or buf.numel() < nbytes:

@@ -48,7 +48,7 @@ MODE_L2N, MODE_UNIFORM, MODE_WEIGHTS = 0, 1, 2
 # round record slots (int64)
 REC_G, REC_REM, REC_STATUS, REC_RANK, REC_KEEP_UPD, REC_EIGH_SWEEPS, REC_KEEP, REC_MERGE_SWEEPS = \
     range(8)
-REC_LEN = 8
+REC_LEN = 8  # rec[0]: merge record; rec[1 + b]: update record of buffer b
 
 # gate slots (int32)
 G_QR = 0            # main CholeskyQR passes: slots 0..4
@@ -64,7 +64,7 @@ class MergeWorkspace:
     incremental driver)."""
 
     def __init__(self, ctx, m, r, *, k=1, criterion="modes", upd_cap=None, comm=None,
-                 row_offset=0):
+                 row_offset=0, nupd=1):
         from .parallel import Comm
 
         self.ctx = ctx
@@ -76,9 +76,11 @@ class MergeWorkspace:
         f64 = dict(dtype=torch.float64, device=dev)
         r = self.r
         self.S = [ColMat.zeros(self.m, 2 * r, dev), ColMat.zeros(self.m, 2 * r, dev)]
-        self.Uupd = ColMat.zeros(self.m, r, dev)
+        # update slots (two for the cross-round pipeline of the ISMA engine)
+        self.Uupd_b = [ColMat.zeros(self.m, r, dev) for _ in range(nupd)]
+        self.sig_upd_b = [torch.zeros(max(r, upd_cap or 0), **f64) for _ in range(nupd)]
+        self.Uupd, self.sig_upd = self.Uupd_b[0], self.sig_upd_b[0]
         self.W = ColMat.zeros(self.m, r, dev)
-        self.sig_upd = torch.zeros(max(r, upd_cap or 0), **f64)
         sq = r * r
         self.M = torch.zeros(sq, **f64)
         self.C = torch.zeros(sq, **f64)
@@ -94,8 +96,8 @@ class MergeWorkspace:
         self.xi = torch.zeros(kk, **f64)
         self.Ck = torch.zeros(kk * kk, **f64)
         self.gates = torch.ones(N_GATES, dtype=torch.int32, device=dev)
-        self.rec = torch.zeros(REC_LEN, dtype=torch.int64, device=dev)
-        self.h_rec = torch.zeros(REC_LEN, dtype=torch.int64).pin_memory()
+        self.rec = torch.zeros((1 + nupd, REC_LEN), dtype=torch.int64, device=dev)
+        self.h_rec = torch.zeros((1 + nupd, REC_LEN), dtype=torch.int64).pin_memory()
         self.h_xi = torch.zeros(kk, dtype=torch.float64).pin_memory()
         self.leak = torch.zeros(1, **f64)
         self.cur = 0
@@ -150,13 +152,14 @@ class MergeWorkspace:
                            dptr(self.Rtmp), r, gate=gp)
             ctx.small_copy(l, l, dptr(self.Rtmp), r, dptr(Rout), r, gate=gp)
 
-    def merge_ops(self, cur):
-        """block_merge (merge.py:37-91) of stack `cur` (U1, sig[cur]) with the
-        update slot (Uupd, sig_upd) into stack 1 - cur, all at capacity r."""
+    def merge_ops(self, cur, ub=0):
+        """block_merge (merge.py:37-91) of stack `cur` (U1, sig[cur]) with
+        update slot `ub` (Uupd, sig_upd) into stack 1 - cur, at capacity r."""
         ctx, r = self.ctx, self.r
         S, Snext = self.S[cur], self.S[1 - cur]
         U1 = S.cols(0, r)
-        U2 = self.Uupd.cols(0, r)
+        U2 = self.Uupd_b[ub].cols(0, r)
+        sig_upd = self.sig_upd_b[ub]
         Q = S.cols(r, 2 * r)
         ctx.tn(r, r, 1.0, U1, U2, dptr(self.M), r, tag="tn_merge_proj")       # merge.py:65
         self.comm.allreduce_sum_(self.M)
@@ -177,8 +180,8 @@ class MergeWorkspace:
                        dptr(self.Rtmp), r, gate=gl)
         ctx.small_copy(r, r, dptr(self.Rtmp), r, dptr(self.Rt), r, gate=gl)
         ctx.merge_core(dptr(self.sig[cur]), r, dptr(self.M), r, dptr(self.Rt), r,
-                       dptr(self.sig_upd), r, r, r, dptr(self.Tm), 2 * r, r,
-                       dptr(self.sig[1 - cur]), info=self.rec[REC_KEEP:])    # merge.py:80-85
+                       dptr(sig_upd), r, r, r, dptr(self.Tm), 2 * r, r,
+                       dptr(self.sig[1 - cur]), info=self.rec[0, REC_KEEP:])  # merge.py:80-85
         ctx.nn(2 * r, r, 1.0, S, dptr(self.Tm), 2 * r, Snext.cols(0, r),
                tag="nn_merge_rotate")                                        # merge.py:86-88
 
@@ -199,9 +202,14 @@ class MergeWorkspace:
         self.h_rec.copy_(self.rec, non_blocking=True)
         self.h_xi.copy_(self.xi, non_blocking=True)
 
-    def read_record(self):
+    def read_record(self, ub=0):
+        """(record, cosines): merge fields from rec[0], update fields of
+        buffer `ub` from rec[1 + ub]."""
         torch.cuda.current_stream(self.ctx.device).synchronize()
-        rec = [int(x) for x in self.h_rec.tolist()]
+        hr = self.h_rec.tolist()
+        rec = [int(x) for x in hr[0]]
+        for i in (REC_G, REC_REM, REC_STATUS, REC_RANK, REC_KEEP_UPD, REC_EIGH_SWEEPS):
+            rec[i] = int(hr[1 + ub][i])
         xi = np.clip(np.abs(self.h_xi.numpy().astype(np.float64)), 0.0, 1.0)
         return rec, xi
 
@@ -236,11 +244,22 @@ class MergeWorkspace:
         """Standalone merge (block_merge): returns (next stack, keep)."""
         self.merge_ops(cur)
         self.readback()
-        rec, _ = self.read_record()
+        rec, _ = self.read_record(0)
         return 1 - cur, rec[REC_KEEP]
 
 
 class IsmaEngine(MergeWorkspace):
+    """The ISMA loop on one GPU (or one row shard).
+
+    Cross-round pipeline: the update of round t+1 (draw, Gram, eigensolve,
+    lift) only depends on the candidate set, not on the merge of round t, so
+    each captured round graph runs merge(t) + cosines(t) on the main stream
+    and update(t+1) on a side stream into the other update buffer.  The
+    uniforms of round t+1 are staged speculatively before round t's loop test;
+    if the loop stops, the generator is rolled back to its state before that
+    batch, so it is consumed exactly as by the reference (numpy Generators;
+    other generator objects run without the pipeline)."""
+
     def __init__(self, ctx, A, *, k, r, c, criterion="modes", use_graphs=True, comm=None,
                  row_offset=0, m_total=None):
         self.A = A
@@ -248,7 +267,7 @@ class IsmaEngine(MergeWorkspace):
         self.c = int(c)
         gcap = min(self.c, A.ncols)
         super().__init__(ctx, A.m, r, k=k, criterion=criterion, upd_cap=gcap, comm=comm,
-                         row_offset=row_offset)
+                         row_offset=row_offset, nupd=2)
         self.m_total = A.m if m_total is None else int(m_total)
         dev = ctx.device
         f64 = dict(dtype=torch.float64, device=dev)
@@ -257,16 +276,17 @@ class IsmaEngine(MergeWorkspace):
         self.norms2 = torch.empty(n, **f64)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
         self.live = torch.ones(n, dtype=torch.uint8, device=dev)
-        self.uni = torch.empty(self.c, **f64)
-        self.h_uni = torch.empty(self.c, dtype=torch.float64).pin_memory()
-        self.idx = torch.empty(g, dtype=torch.int32, device=dev)
-        self.cnt = torch.empty(g, dtype=torch.int64, device=dev)
-        self.G = torch.empty(g * g, **f64)
-        self.Tl = torch.empty(g * r, **f64)
+        self.uni = [torch.empty(self.c, **f64) for _ in range(2)]
+        self.h_uni = [torch.empty(self.c, dtype=torch.float64).pin_memory() for _ in range(2)]
+        self.idx = [torch.empty(g, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.cnt = [torch.empty(g, dtype=torch.int64, device=dev) for _ in range(2)]
+        self.G = [torch.empty(g * g, **f64) for _ in range(2)]
+        self.Tl = [torch.empty(g * r, **f64) for _ in range(2)]
         self.npos = 0
         self.use_graphs = use_graphs
         self.graphs = {}
         self.graph_launches = {}
+        self.side = torch.cuda.Stream(dev)
 
     def reset(self):
         """Per-run state (the captured graphs and buffers are reused)."""
@@ -289,51 +309,73 @@ class IsmaEngine(MergeWorkspace):
         if self.npos == 0:
             raise DegenerateDistributionError("all candidate column weights are zero")
 
-    def update_ops(self, mode, dest):
-        """get_update (isma.py:144-178), column path, at capacity."""
+    def update_ops(self, mode, b, dest):
+        """get_update (isma.py:144-178), column path, at capacity, into
+        update buffer b (its own draw/Gram/eigensolver scratch)."""
         ctx, A, g, r = self.ctx, self.A, self.gcap, self.r
-        self.uni.copy_(self.h_uni, non_blocking=True)
-        ctx.draw(mode, self.norms2 if mode == MODE_L2N else None, self.live, self.n, self.uni,
-                 self.c, self.idx, self.cnt, info=self.rec[REC_G:])
-        ctx.tn(g, g, 1.0, A, A, dptr(self.G), g, xcols=self.idx, ycols=self.idx,
+        self.uni[b].copy_(self.h_uni[b], non_blocking=True)
+        ctx.draw(mode, self.norms2 if mode == MODE_L2N else None, self.live, self.n, self.uni[b],
+                 self.c, self.idx[b], self.cnt[b], info=self.rec[1 + b, REC_G:])
+        ctx.tn(g, g, 1.0, A, A, dptr(self.G[b]), g, xcols=self.idx[b], ycols=self.idx[b],
                tag="tn_gram_gather")                                         # baselines.py:43
-        self.comm.allreduce_sum_(self.G)
-        ctx.gram_eigh(dptr(self.G), g, g, r, self.sig_upd, dptr(self.Tl), g,
-                      info=self.rec[REC_RANK:])                                   # baselines:44-48
-        ctx.nn(g, r, 1.0, A, dptr(self.Tl), g, dest, xcols=self.idx,
+        self.comm.allreduce_sum_(self.G[b])
+        ctx.gram_eigh(dptr(self.G[b]), g, g, r, self.sig_upd_b[b], dptr(self.Tl[b]), g,
+                      info=self.rec[1 + b, REC_RANK:])                       # baselines.py:44-48
+        ctx.nn(g, r, 1.0, A, dptr(self.Tl[b]), g, dest, xcols=self.idx[b],
                tag="nn_lift_gather")                                         # baselines.py:62-63
 
-    def round_ops(self, mode, cur):
-        self.update_ops(mode, self.Uupd)
-        self.merge_ops(cur)
+    def update_side_ops(self, mode, b, join=True):
+        """update_ops on the side stream with its own workspaces (forked from
+        the current stream; joined back when `join`)."""
+        main = torch.cuda.current_stream(self.ctx.device)
+        self.side.wait_stream(main)
+        self.ctx.ws_suffix = "_upd"
+        try:
+            with torch.cuda.stream(self.side):
+                self.update_ops(mode, b, self.Uupd_b[b].cols(0, self.r))
+        finally:
+            self.ctx.ws_suffix = ""
+        if join:
+            main.wait_stream(self.side)
+
+    def round_ops(self, mode, cur, ub, pipelined):
+        """Round t: merge(t) with update buffer ub (+ cosines, readback);
+        pipelined: update(t+1) into buffer 1 - ub concurrently."""
+        if pipelined:
+            self.update_side_ops(mode, 1 - ub, join=False)  # update(t+1) || merge(t)
+        else:
+            self.update_ops(mode, ub, self.Uupd_b[ub].cols(0, self.r))
+        self.merge_ops(cur, ub)
         self.cosines_ops(cur, 1 - cur)
+        if pipelined:
+            torch.cuda.current_stream(self.ctx.device).wait_stream(self.side)
         self.readback()
 
-    def launch_round(self, mode, cur):
+    def launch_round(self, mode, cur, ub, pipelined):
         if not self.use_graphs or self.ctx.prof is not None or self.comm.active:
-            self.round_ops(mode, cur)
+            self.round_ops(mode, cur, ub, pipelined)
             return
-        key = (mode, cur)
+        key = (mode, cur, ub, pipelined)
         gr = self.graphs.get(key)
         if gr is None:
             dev = self.ctx.device
             # eager warm-up (grows every workspace) on a side stream, state restored
-            saved = [t.clone() for t in (self.live, self.rec, self.Uupd.t, self.S[1 - cur].t,
-                                         self.S[cur].t, self.sig[1 - cur], self.sig_upd)]
+            keep = (self.live, self.rec, self.Uupd_b[0].t, self.Uupd_b[1].t, self.S[0].t,
+                    self.S[1].t, self.sig[0], self.sig[1], self.sig_upd_b[0], self.sig_upd_b[1])
+            saved = [t.clone() for t in keep]
             st = torch.cuda.Stream(dev)
             st.wait_stream(torch.cuda.current_stream(dev))
             with torch.cuda.stream(st):
-                self.round_ops(mode, cur)
+                self.round_ops(mode, cur, ub, pipelined)
             torch.cuda.current_stream(dev).wait_stream(st)
             torch.cuda.synchronize(dev)
-            for dst, src in zip((self.live, self.rec, self.Uupd.t, self.S[1 - cur].t,
-                                 self.S[cur].t, self.sig[1 - cur], self.sig_upd), saved):
+            for dst, src in zip(keep, saved):
                 dst.copy_(src)
             torch.cuda.synchronize(dev)
             gr = torch.cuda.CUDAGraph()
             l0 = self.ctx.launches
             with torch.cuda.graph(gr, stream=st):
-                self.round_ops(mode, cur)
+                self.round_ops(mode, cur, ub, pipelined)
             self.graph_launches[key] = self.ctx.launches - l0
             self.graphs[key] = gr
             torch.cuda.synchronize(dev)
@@ -366,11 +408,11 @@ class IsmaEngine(MergeWorkspace):
         return Vnew
 
     # ------------------------------------------------------------ driver ---
-    def _stage_uniforms(self, rng):
+    def _stage_uniforms(self, rng, b):
         u = np.asarray(rng.random(int(self.c)), dtype=np.float64)  # one batch (sampling.py:213)
         if u.shape != (self.c,):
             raise ParameterError("generator returned a batch of the wrong shape")
-        self.h_uni.numpy()[:] = u
+        self.h_uni[b].numpy()[:] = u
 
     def run(self, rng, *, strategy, tau, finalize, keep, trace_cls):
         """isma_run main loop (isma.py:258-303) on the device."""
@@ -379,11 +421,15 @@ class IsmaEngine(MergeWorkspace):
         t0 = time.perf_counter()
         cur = self.cur
         r = self.r
-        self._stage_uniforms(rng)
-        self.update_ops(MODE_L2N, self.S[cur].cols(0, r))                    # bootstrap
-        self.sig[cur].copy_(self.sig_upd[:r])
+        # the pipeline stages uniforms one round ahead; only generators whose
+        # state can be rolled back support that
+        bitgen = getattr(rng, "bit_generator", None)
+        pipelined = bitgen is not None and not self.comm.active
+        self._stage_uniforms(rng, 0)
+        self.update_ops(MODE_L2N, 0, self.S[cur].cols(0, r))                 # bootstrap
+        self.sig[cur].copy_(self.sig_upd_b[0][:r])
         self.readback()
-        rec, _ = self.read_record()
+        rec, _ = self.read_record(0)
         g, rem, keep0 = rec[REC_G], rec[REC_REM], rec[REC_KEEP_UPD]
         self.npos -= g
         self.sig[cur][keep0:].zero_()  # the basis carries keep0 modes; zero sigma padding
@@ -392,14 +438,24 @@ class IsmaEngine(MergeWorkspace):
         xi = np.zeros(self.k)
         it = 0
         mode = MODE_L2N if strategy == "l2n" else MODE_UNIFORM
+        ub = 1
+        saved_state = None
+        if pipelined and rem and not (mode == MODE_L2N and self.npos <= 0):
+            saved_state = bitgen.state
+            self._stage_uniforms(rng, ub)                                    # round 1
+            self.update_side_ops(mode, ub)
         while rem and (it == 0 or bool(np.any(xi < tau))):
             it += 1
             t0 = time.perf_counter()
             if mode == MODE_L2N and self.npos <= 0:
                 break  # l2n over only zero-norm columns (isma.py:211-215, 280-281)
-            self._stage_uniforms(rng)
-            self.launch_round(mode, cur)
-            rec, xi = self.read_record()
+            if pipelined:
+                saved_state = bitgen.state
+                self._stage_uniforms(rng, 1 - ub)                            # round it + 1
+            else:
+                self._stage_uniforms(rng, ub)
+            self.launch_round(mode, cur, ub, pipelined)
+            rec, xi = self.read_record(ub)
             g, rem = rec[REC_G], rec[REC_REM]
             if mode == MODE_L2N:
                 self.npos -= g
@@ -409,6 +465,10 @@ class IsmaEngine(MergeWorkspace):
             self.stats.setdefault("eigh_sweeps", []).append(rec[REC_EIGH_SWEEPS])
             self.stats.setdefault("merge_sweeps", []).append(rec[REC_MERGE_SWEEPS])
             traces.append(trace_cls(it, g, 0, rem, xi.copy(), time.perf_counter() - t0))
+            if pipelined:
+                ub = 1 - ub
+        if pipelined and saved_state is not None:
+            bitgen.state = saved_state  # undo the speculative batch of the round never run
         self.cur = cur
         v = None
         if finalize and self.l:

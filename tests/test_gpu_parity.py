@@ -253,3 +253,28 @@ def test_large_rank_capacity_paths():
         assert [t.remaining for t in tr] == [t["remaining"] for t in o["trace"]]
         assert sigma_relerr(f.sigma, o["sigma"]) <= SIGMA_RTOL
         assert principal_angles_sin(f.u, o["u"]).max() <= ANGLE_TOL_RAD
+
+
+def test_pipelined_rounds_consume_generator_like_reference():
+    """The cross-round pipeline stages uniforms one round ahead; after the run
+    the caller's generator must be exactly where the reference leaves it."""
+    a = make_noisy_low_rank(200, 90, 5, np.random.default_rng(8), noise=0.05)
+    for strategy, tau in (("unf", 0.99), ("l2n", 0.999), ("l2n", 1.0)):
+        cfg = pod.IsmaConfig(k=5, c=12, tau=tau, strategy=strategy, seed=0)
+        g1 = np.random.default_rng(21)
+        f, tr = pod.isma_run(a, cfg, rng=g1)
+        g2 = np.random.default_rng(21)
+        o = orc.run(a, 5, c=12, tau=tau, strategy=strategy, rng=g2)
+        assert [t.remaining for t in tr] == [t["remaining"] for t in o["trace"]]
+        assert g1.random() == g2.random()
+        assert sigma_relerr(f.sigma, o["sigma"]) <= SIGMA_RTOL
+
+
+def test_pipelined_equals_unpipelined_bitwise():
+    """A generator without a rollback-able state runs the unpipelined round:
+    both orders of work produce identical results bit for bit."""
+    a = workloads.config1(seed=0)
+    cfg = pod.IsmaConfig(k=10, r=30, c=50, tau=1 - 1e-8, strategy="l2n", seed=7)
+    f1, t1 = pod.isma_run(a, cfg)  # numpy Generator -> pipelined
+    f2, t2 = pod.isma_run(a, cfg, rng=Recorder(7))  # plain object -> not pipelined
+    assert np.array_equal(f1.u, f2.u) and np.array_equal(f1.sigma, f2.sigma)
