@@ -270,9 +270,19 @@ def main():
         step_s = float(t.item())
     # instrumented pass: the same run launched eagerly with CUDA events around
     # every kernel (graph replay hides individual launches)
+    class _NoRollback:  # a generator without a rollback-able state: unpipelined rounds,
+        def __init__(self, seed):  # so every kernel is timed without a concurrent stream
+            self.g = np.random.default_rng(seed)
+
+        def random(self, k):
+            return self.g.random(k)
+
     prof = KernelProfile()
     ctx.prof = prof
-    one_run()
+    if comm is None:
+        pod.isma_run(A, cfg, rng=_NoRollback(w["seed"]))
+    else:
+        pod.isma_run(A, cfg, rng=_NoRollback(w["seed"]), comm=comm, m_total=m_total)
     ctx.prof = None
     kern = prof.summary()
     n_rounds = len(traces)

@@ -127,16 +127,26 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
   }
 }
 
-__global__ void reduce_kernel(int nsplit, int p, int q, double alpha, const double* __restrict__ ws,
-                              double* __restrict__ C, int64_t ldc, const int32_t* __restrict__ gate) {
+// C[i, j] = alpha * sum_k ws[k][i, j]: one warp per output element, lanes
+// take splits k = lane, lane + 32, ... and a fixed shuffle tree combines them
+// (deterministic; no atomics).
+__global__ void __launch_bounds__(256) reduce_kernel(int nsplit, int p, int q, double alpha,
+                                                     const double* __restrict__ ws,
+                                                     double* __restrict__ C, int64_t ldc,
+                                                     const int32_t* __restrict__ gate) {
   if (gate && *gate == 0) return;
   const int64_t total = (int64_t)p * q;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = wg; t < total; t += nw) {
     double s = 0.0;
-    for (int k = 0; k < nsplit; ++k) s += ws[(size_t)k * total + t];
-    const int64_t j = t / p, i = t - j * p;
-    C[i + j * ldc] = alpha * s;
+    for (int k = lane; k < nsplit; k += 32) s += ws[(size_t)k * total + t];
+    s = warp_sum(s);
+    if (lane == 0) {
+      const int64_t j = t / p, i = t - j * p;
+      C[i + j * ldc] = alpha * s;
+    }
   }
 }
 
@@ -280,6 +290,141 @@ __global__ void __launch_bounds__(THREADS) kernel(
 }
 }  // namespace nn
 
+// -------------------------------------------------- NN persistent ------
+// T (p x q, p <= PMAX) resident in shared memory for the whole kernel; each
+// CTA walks row blocks of BM rows with the next block's X prefetched by
+// cp.async while the current one is multiplied (two buffers).
+namespace nnp {
+constexpr int THREADS = 256;
+constexpr int BM = 64;
+constexpr int LDX = BM + 4;  // % 16 == 4: conflict-free A fragments
+
+template <int BN>
+struct Cfg {
+  static constexpr int WM = BM / 32;  // 2 warps along M
+  static constexpr int WN = 8 / WM;   // 4 warps along N
+  static constexpr int FN = BN / WN / 8;
+};
+
+__host__ __device__ inline int kpad(int p) { return (p + 7) & ~7; }
+__host__ __device__ inline int ldt(int p) { return kpad(p) + 4; }  // T stored [j][k], % 16 == 4 when kpad % 16 == 0
+inline size_t smem_bytes(int p, int bn) {
+  return ((size_t)2 * kpad(p) * LDX + (size_t)bn * ldt(p)) * sizeof(double);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, double alpha,
+                                                  const double* X, int64_t ldx,
+                                                  const int32_t* __restrict__ xcols,
+                                                  const double* __restrict__ T, int64_t ldT,
+                                                  double beta, const double* Z, int64_t ldz,
+                                                  double* Y, int64_t ldy,
+                                                  const int32_t* __restrict__ gate, int vec16) {
+  using C = Cfg<BN>;
+  if (gate && *gate == 0) return;
+  extern __shared__ __align__(16) double smem[];
+  const int KP = kpad(p), LT = ldt(p);
+  double* xs0 = smem;
+  double* xs1 = smem + (size_t)KP * LDX;
+  double* ts = smem + (size_t)2 * KP * LDX;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // T -> smem once (zero padded to KP x BN)
+  for (int e = threadIdx.x; e < BN * KP; e += THREADS) {
+    const int j = e / KP, k = e - j * KP;
+    ts[j * LT + k] = (j < q && k < p) ? T[k + (int64_t)j * ldT] : 0.0;
+  }
+  const int64_t nblk = (m + BM - 1) / BM;
+  auto load_block = [&](double* xs, int64_t rb) {
+    const int64_t r0 = rb * BM;
+    if (vec16) {
+      // 2 rows per lane-slot: BM/2 = 32 slots per column
+      for (int e = threadIdx.x; e < KP * (BM / 2); e += THREADS) {
+        const int c = e / (BM / 2), i2 = (e - c * (BM / 2)) * 2;
+        const int64_t row = r0 + i2;
+        bool v = c < p && row + 1 < m;
+        int64_t col = c;
+        if (c < p && xcols) {
+          col = xcols[c];
+          v = v && col >= 0;
+        }
+        if (v) {
+          cp_async16(xs + c * LDX + i2, X + col * ldx + row, true);
+        } else {
+          // tail / padding: element-wise with zero fill
+          const bool v0 = c < p && row < m && (!xcols || col >= 0);
+          cp_async8(xs + c * LDX + i2, v0 ? X + col * ldx + row : X, v0);
+          cp_async8(xs + c * LDX + i2 + 1, X, false);
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < KP * BM; e += THREADS) {
+        const int c = e / BM, i = e - c * BM;
+        const int64_t row = r0 + i;
+        bool v = c < p && row < m;
+        int64_t col = c;
+        if (v && xcols) {
+          col = xcols[c];
+          v = col >= 0;
+        }
+        cp_async8(xs + c * LDX + i, v ? X + col * ldx + row : X, v);
+      }
+    }
+  };
+  const int wm = warp % C::WM, wn = warp / C::WM;
+  int64_t rb = blockIdx.x;
+  if (rb < nblk) load_block(xs0, rb);
+  cp_async_commit();
+  int buf = 0;
+  for (; rb < nblk; rb += gridDim.x) {
+    const int64_t nb = rb + gridDim.x;
+    if (nb < nblk) load_block(buf ? xs0 : xs1, nb);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* xs = buf ? xs1 : xs0;
+    double acc[4][C::FN][2];
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+      for (int g = 0; g < C::FN; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+#pragma unroll 2
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      double a[4], b[C::FN];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+        a[f] = xs[(k0 + (lane & 3)) * LDX + wm * 32 + f * 8 + (lane >> 2)];
+#pragma unroll
+      for (int g = 0; g < C::FN; ++g)
+        b[g] = ts[(wn * (BN / C::WN) + g * 8 + (lane >> 2)) * LT + k0 + (lane & 3)];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int g = 0; g < C::FN; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
+    }
+    __syncthreads();  // xs fully consumed before the next prefetch overwrites it
+    const int64_t row0 = rb * BM + wm * 32;
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const int64_t i = row0 + f * 8 + (lane >> 2);
+      if (i >= m) continue;
+#pragma unroll
+      for (int g = 0; g < C::FN; ++g)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = wn * (BN / C::WN) + g * 8 + 2 * (lane & 3) + e;
+          if (j < q) {
+            double v = alpha * acc[f][g][e];
+            if (beta != 0.0) v += beta * Z[i + (int64_t)j * ldz];
+            Y[i + (int64_t)j * ldy] = v;
+          }
+        }
+    }
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+}
+}  // namespace nnp
+
 static bool g_attr_done = false;
 static int ensure_attrs() {
   if (g_attr_done) return POD_OK;
@@ -295,6 +440,12 @@ static int ensure_attrs() {
   e = cudaFuncSetAttribute(nn::kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)nn::Cfg<192>::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "nn attr");
+  for (int bn : {64, 128, 192}) {
+    const void* fn = bn == 64 ? (const void*)nnp::kernel<64>
+                   : bn == 128 ? (const void*)nnp::kernel<128> : (const void*)nnp::kernel<192>;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return cuda_status(e, "nnp attr");
+  }
   g_attr_done = true;
   return POD_OK;
 }
@@ -330,7 +481,7 @@ extern "C" int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
                                                          gate);
   POD_CHECK_LAUNCH("tn partial");
   int64_t tot = p * q;
-  int blocks = (int)std::min<int64_t>(ceil_div(tot, 256), 4 * 148);
+  int blocks = (int)std::min<int64_t>(ceil_div(tot, 8), 16 * 148);  // 8 warps = 8 outputs per block
   tn::reduce_kernel<<<blocks, 256, 0, s>>>(pl.splits, (int)p, (int)q, alpha, (const double*)ws, C,
                                            ldc, gate);
   POD_CHECK_LAUNCH("tn reduce");
@@ -349,6 +500,27 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
   int st = ensure_attrs();
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
+  {
+    const int bn = q <= 64 ? 64 : (q <= 128 ? 128 : 192);
+    const size_t bytes = nnp::smem_bytes((int)p, bn);
+    if (p >= 1 && bytes <= 110 * 1024) {  // T resident, 2 CTAs/SM: persistent kernel
+      const int vec16 = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && (ldx % 2 == 0);
+      const int per_sm = bytes <= 110 * 1024 ? 2 : 1;
+      const int64_t nblk = ceil_div(m, nnp::BM);
+      const unsigned grid = (unsigned)std::min<int64_t>(nblk, (int64_t)per_sm * 148);
+      if (bn == 64)
+        nnp::kernel<64><<<grid, nnp::THREADS, bytes, s>>>(m, (int)p, (int)q, alpha, X, ldx, xcols,
+                                                          T, ldt, beta, Z, ldz, Y, ldy, gate, vec16);
+      else if (bn == 128)
+        nnp::kernel<128><<<grid, nnp::THREADS, bytes, s>>>(m, (int)p, (int)q, alpha, X, ldx, xcols,
+                                                           T, ldt, beta, Z, ldz, Y, ldy, gate, vec16);
+      else
+        nnp::kernel<192><<<grid, nnp::THREADS, bytes, s>>>(m, (int)p, (int)q, alpha, X, ldx, xcols,
+                                                           T, ldt, beta, Z, ldz, Y, ldy, gate, vec16);
+      POD_CHECK_LAUNCH("nn persistent");
+      return POD_OK;
+    }
+  }
   if (q <= 64) {
     dim3 grid((unsigned)ceil_div(m, nn::Cfg<64>::BM));
     nn::kernel<64><<<grid, nn::THREADS, nn::Cfg<64>::SMEM, s>>>(m, (int)p, (int)q, alpha, X, ldx,
