@@ -54,7 +54,9 @@ int pod_colnorms2_f64(const double* A, int64_t m, int64_t n, int64_t lda, double
  * distribution it samples -- mode 0: l2n over live columns, weights =
  * raw norms2 normalised as sampling.py:55-65,34-53; mode 1: uniform over
  * live columns (sampling.py:150-155); mode 2: explicit normalised weights
- * over positions 0..n-1 (a Distribution's weights, no live mask) -- and the
+ * over positions 0..n-1 (a Distribution's weights, no live mask); mode 3:
+ * "ort" -- raw squared residuals over live columns, falling back to uniform
+ * when their sum <= thr (isma.py:216-220) -- and the
  * candidate-set update isma.py:164 (drawn columns cleared in `live`).
  * `uniforms` holds the c variates of ONE rng.random(c) batch.
  * Outputs: idx_out[0..g) ascending int32 (idx_out[g..cap) = -1: zero-column
@@ -64,7 +66,16 @@ int pod_colnorms2_f64(const double* A, int64_t m, int64_t n, int64_t lda, double
 size_t pod_draw_ws_bytes(int64_t n);
 int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n, const double* uniforms,
              int64_t c, int32_t* idx_out, int64_t* cnt_out, int64_t cap, void* ws,
-             size_t ws_bytes, int64_t* info, void* stream);
+             size_t ws_bytes, int64_t* info, double thr, void* stream);
+
+/* Squared residual norms after projection on an orthonormal basis:
+ * out[j] = ||A[:, cols[j]] - U C[:, j]||^2 with C = U^T A[:, cols] (r x n,
+ * from pod_gemm_tn_f64), U m x r.  The residual is never materialised.
+ * Replaces sampling.py:175-176 (residual_distribution, strategy "ort"). */
+size_t pod_resid_ws_bytes(int64_t m, int64_t n);
+int pod_resid_colnorms2(int64_t m, int64_t n, const double* A, int64_t lda, const int32_t* cols,
+                        const double* U, int64_t ldu, int64_t r, const double* C, int64_t ldc,
+                        double* out, void* ws, size_t ws_bytes, void* stream);
 
 /* Gates: every compute entry point below that takes `gate` (device int32,
  * nullable) does nothing when *gate == 0, so a round's launch sequence is

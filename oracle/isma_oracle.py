@@ -131,6 +131,23 @@ def cdf_draw(candidates, weights, uniforms):
     return uniq.astype(np.int64), counts.astype(np.int64)
 
 
+def residual_weights(a, u, candidates, degenerate_rtol=1e-14):
+    """sampling.py:158-187 -- squared residuals of the candidate columns after
+    projection on u, normalised (raw/total, then __post_init__ renormalises);
+    None when their total is <= degenerate_rtol ||A||_F^2 (the caller then
+    samples uniformly, isma.py:216-220)."""
+    cols = a[:, candidates]
+    if u.shape[1] == 0:
+        return normalized_weights(column_norms2(cols))
+    resid = cols - u @ (u.T @ cols)
+    res2 = np.einsum("ij,ij->j", resid, resid)
+    total = res2.sum()
+    if total <= degenerate_rtol * np.einsum("ij,ij->", a, a):
+        return None
+    w = res2 / total
+    return w / w.sum()
+
+
 def margin_to_cdf_boundary(weights, uniforms):
     """Smallest |u - cum| over draws and CDF breakpoints (tie-risk monitor,
     SURVEY.md section 8c)."""
@@ -238,8 +255,8 @@ def run(a, k, *, r=None, c, tau, strategy="l2n", criterion="modes", seed=0,
     per-round trace list of dicts (iteration, unique, counts, remaining,
     cosines, wall_time[, margin]) plus phase timings.  ``max_rounds`` stops
     after that many update rounds (a bounded CPU-timing sample only)."""
-    if strategy not in ("l2n", "unf"):
-        raise OracleParamError("oracle covers strategies l2n and unf")
+    if strategy not in ("l2n", "unf", "ort"):
+        raise OracleParamError("oracle covers strategies l2n, unf and ort")
     a = dense_f64(a)
     m, n = a.shape
     r = 3 * k if r is None else r
@@ -284,6 +301,10 @@ def run(a, k, *, r=None, c, tau, strategy="l2n", criterion="modes", seed=0,
                 w = normalized_weights(norms2[s])
             except OracleDegenerate:
                 break
+        elif strategy == "ort":
+            w = residual_weights(a, u, s)
+            if w is None:
+                w = uniform_weights(s.size)
         else:
             w = uniform_weights(s.size)
         u2, s2, s, info = one_round(s, w)

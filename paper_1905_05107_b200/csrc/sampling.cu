@@ -123,11 +123,13 @@ __device__ int64_t block_excl_scan_i64(int64_t v, int64_t* sh, int64_t* total) {
 // mode 0: l2n over live columns (weights = raw norms2, normalised twice)
 // mode 1: uniform over live columns
 // mode 2: explicit normalised weights over all n positions (no live mask)
+// mode 3: ort over live columns: raw squared residuals normalised twice, or
+//         uniform when their sum <= thr (isma.py:216-220, sampling.py:182-186)
 __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
     int mode, const double* __restrict__ raw, uint8_t* __restrict__ live, int64_t n,
     const double* __restrict__ uni, int64_t c, int32_t* __restrict__ idx_out,
     int64_t* __restrict__ cnt_out, int64_t cap, double* __restrict__ cum,
-    int32_t* __restrict__ counts, int64_t* __restrict__ info) {
+    int32_t* __restrict__ counts, int64_t* __restrict__ info, double thr) {
   __shared__ double shd[DRAW_THREADS + 1];
   __shared__ int64_t shi[DRAW_THREADS + 1];
   __shared__ double red[32];
@@ -148,6 +150,12 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
   // weights (sampling.py:55-65 then 34-53), kept in `cum` as scratch
   const double inv_s = 1.0 / (double)nlive;
   double loc = 0.0;
+  if (mode == 3) {  // residual weights, or the uniform fallback
+    for (int64_t j = j0; j < j1; ++j) loc += live[j] ? raw[j] : 0.0;
+    const double tot = block_sum(loc, red);
+    mode = (tot <= thr) ? 1 : 0;
+    loc = 0.0;
+  }
   for (int64_t j = j0; j < j1; ++j) {
     double w;
     if (mode == 2) w = raw[j];
@@ -251,8 +259,9 @@ extern "C" size_t pod_draw_ws_bytes(int64_t n) {
 
 extern "C" int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n,
                         const double* uniforms, int64_t c, int32_t* idx_out, int64_t* cnt_out,
-                        int64_t cap, void* ws, size_t ws_bytes, int64_t* info, void* stream) {
-  POD_REQUIRE(mode >= 0 && mode <= 2, "pod_draw: bad mode %d", mode);
+                        int64_t cap, void* ws, size_t ws_bytes, int64_t* info, double thr,
+                        void* stream) {
+  POD_REQUIRE(mode >= 0 && mode <= 3, "pod_draw: bad mode %d", mode);
   POD_REQUIRE(n > 0 && n < (int64_t)INT32_MAX, "pod_draw: bad n");
   POD_REQUIRE(c >= 1, "sample count must be >= 1");
   POD_REQUIRE(ws_bytes >= pod_draw_ws_bytes(n), "pod_draw: workspace too small");
@@ -264,7 +273,7 @@ extern "C" int pod_draw(int mode, const double* weights, uint8_t* live, int64_t 
   int32_t* counts = (int32_t*)(cum + n);
   draw_kernel<<<1, DRAW_THREADS, 0, (cudaStream_t)stream>>>(mode, weights, live, n, uniforms, c,
                                                               idx_out, cnt_out, cap, cum, counts,
-                                                              info);
+                                                              info, thr);
   POD_CHECK_LAUNCH("draw");
   return POD_OK;
 }

@@ -130,11 +130,18 @@ class Ctx:
         self._call("colnorms2", 1, 2.0 * A.m * A.ncols, 8.0 * A.m * A.ncols, "pod_colnorms2_f64", A.ptr, A.m, A.ncols, A.ld, _ptr(out), _ptr(flag),
                   self.stream)
 
-    def draw(self, mode, weights, live, n, uniforms, c, idx, cnt, info=None):
+    def draw(self, mode, weights, live, n, uniforms, c, idx, cnt, info=None, thr=0.0):
         ws = self.ws("draw", _lib.load().pod_draw_ws_bytes(n))
         self._call("draw", 1, 0.0, 24.0 * n + 8.0 * c, "pod_draw", mode, _ptr(weights),
                    _ptr(live), n, _ptr(uniforms), c, _ptr(idx), _ptr(cnt), idx.numel(), _ptr(ws),
-                   ws.numel(), _ptr(self.info if info is None else info), self.stream)
+                   ws.numel(), _ptr(self.info if info is None else info), float(thr),
+                   self.stream)
+
+    def resid_colnorms2(self, A, n, U, r, C, ldc, out, cols=None):
+        ws = self.ws("resid", _lib.load().pod_resid_ws_bytes(A.m, n))
+        self._call("resid_colnorms2", 2, 2.0 * A.m * n * r, 8.0 * A.m * (n + r),
+                   "pod_resid_colnorms2", A.m, n, A.ptr, A.ld, _ptr(cols), U.ptr, U.ld, r, C, ldc,
+                   _ptr(out), _ptr(ws), ws.numel(), self.stream)
 
     def tn(self, p, q, alpha, X, Y, C, ldc, xcols=None, ycols=None, m=None, gate=None,
            tag="gemm_tn"):

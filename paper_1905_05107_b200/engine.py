@@ -43,7 +43,8 @@ from .errors import DegenerateDistributionError, ParameterError
 REORTH_TOL = 1e-8  # merge.py:34
 CHOLQR_PASSES = 4  # pass 0 always; passes 1..3 gated on the previous pass
 
-MODE_L2N, MODE_UNIFORM, MODE_WEIGHTS = 0, 1, 2
+MODE_L2N, MODE_UNIFORM, MODE_WEIGHTS, MODE_ORT = 0, 1, 2, 3
+ORT_DEGENERATE_RTOL = 1e-14  # sampling.py:158 degenerate_rtol
 
 # round record slots (int64)
 REC_G, REC_REM, REC_STATUS, REC_RANK, REC_KEEP_UPD, REC_EIGH_SWEEPS, REC_KEEP, REC_MERGE_SWEEPS = \
@@ -287,6 +288,8 @@ class IsmaEngine(MergeWorkspace):
         self.graphs = {}
         self.graph_launches = {}
         self.side = torch.cuda.Stream(dev)
+        self.ort = None  # (C = U^T A, residual norms) buffers of the "ort" strategy
+        self.frob2 = 0.0
 
     def reset(self):
         """Per-run state (the captured graphs and buffers are reused)."""
@@ -306,16 +309,39 @@ class IsmaEngine(MergeWorkspace):
         if flag:
             raise ParameterError("matrix contains non-finite entries")
         self.npos = int((self.norms2 > 0).sum().item())
+        self.frob2 = float(self.norms2.double().sum().item())  # ||A||_F^2 (sampling.py:182)
         if self.npos == 0:
             raise DegenerateDistributionError("all candidate column weights are zero")
 
-    def update_ops(self, mode, b, dest):
+    def ort_weights_ops(self, cur):
+        """residual_distribution (sampling.py:158-187) against the current
+        basis: C = U^T A (TN) and ||a_j - U c_j||^2 (fused DMMA pass)."""
+        ctx, A, r, n = self.ctx, self.A, self.r, self.n
+        if self.ort is None:
+            dev = ctx.device
+            self.ort = (torch.zeros(r * n, dtype=torch.float64, device=dev),
+                        torch.zeros(n, dtype=torch.float64, device=dev))
+        C, res2 = self.ort
+        U = self.S[cur].cols(0, r)
+        ctx.tn(r, n, 1.0, U, A, dptr(C), r, tag="tn_ort_UtA")
+        self.comm.allreduce_sum_(C)
+        ctx.resid_colnorms2(A, n, U, r, dptr(C), r, res2)
+        self.comm.allreduce_sum_(res2)
+        return res2
+
+    def update_ops(self, mode, b, dest, cur=None):
         """get_update (isma.py:144-178), column path, at capacity, into
         update buffer b (its own draw/Gram/eigensolver scratch)."""
         ctx, A, g, r = self.ctx, self.A, self.gcap, self.r
         self.uni[b].copy_(self.h_uni[b], non_blocking=True)
-        ctx.draw(mode, self.norms2 if mode == MODE_L2N else None, self.live, self.n, self.uni[b],
-                 self.c, self.idx[b], self.cnt[b], info=self.rec[1 + b, REC_G:])
+        weights, thr = None, 0.0
+        if mode == MODE_L2N:
+            weights = self.norms2
+        elif mode == MODE_ORT:
+            weights = self.ort_weights_ops(cur)
+            thr = ORT_DEGENERATE_RTOL * self.frob2
+        ctx.draw(mode, weights, self.live, self.n, self.uni[b], self.c, self.idx[b], self.cnt[b],
+                 info=self.rec[1 + b, REC_G:], thr=thr)
         ctx.tn(g, g, 1.0, A, A, dptr(self.G[b]), g, xcols=self.idx[b], ycols=self.idx[b],
                tag="tn_gram_gather")                                         # baselines.py:43
         self.comm.allreduce_sum_(self.G[b])
@@ -344,7 +370,7 @@ class IsmaEngine(MergeWorkspace):
         if pipelined:
             self.update_side_ops(mode, 1 - ub, join=False)  # update(t+1) || merge(t)
         else:
-            self.update_ops(mode, ub, self.Uupd_b[ub].cols(0, self.r))
+            self.update_ops(mode, ub, self.Uupd_b[ub].cols(0, self.r), cur=cur)
         self.merge_ops(cur, ub)
         self.cosines_ops(cur, 1 - cur)
         if pipelined:
@@ -424,7 +450,9 @@ class IsmaEngine(MergeWorkspace):
         # the pipeline stages uniforms one round ahead; only generators whose
         # state can be rolled back support that
         bitgen = getattr(rng, "bit_generator", None)
-        pipelined = bitgen is not None and not self.comm.active
+        mode = {"l2n": MODE_L2N, "ort": MODE_ORT}.get(strategy, MODE_UNIFORM)
+        # ort's distribution depends on the merged basis: no pipelining
+        pipelined = bitgen is not None and not self.comm.active and mode != MODE_ORT
         self._stage_uniforms(rng, 0)
         self.update_ops(MODE_L2N, 0, self.S[cur].cols(0, r))                 # bootstrap
         self.sig[cur].copy_(self.sig_upd_b[0][:r])
@@ -437,7 +465,6 @@ class IsmaEngine(MergeWorkspace):
         traces.append(trace_cls(0, g, 0, rem, np.zeros(0), time.perf_counter() - t0))
         xi = np.zeros(self.k)
         it = 0
-        mode = MODE_L2N if strategy == "l2n" else MODE_UNIFORM
         ub = 1
         saved_state = None
         if pipelined and rem and not (mode == MODE_L2N and self.npos <= 0):

@@ -106,7 +106,7 @@ class IterationTrace:
 def _require_column_path(config):
     if config.rows:
         raise NotImplementedError("row sampling (rows=True) is not on the B200 path yet")
-    if config.strategy not in ("l2n", "unf"):
+    if config.strategy not in ("l2n", "unf", "ort"):
         raise NotImplementedError(f"strategy {config.strategy!r} is not on the B200 path yet")
 
 

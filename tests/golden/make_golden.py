@@ -89,6 +89,11 @@ def main():
     gen = np.random.default_rng(13)
     cases["exhaustive_40x18"] = (gen.standard_normal((40, 18)), podsketch.IsmaConfig(
         k=5, r=18, strategy="l2n", tau=1.0, c=60, seed=2), None)
+    cases["cfg1_ort_modes"] = (a1, podsketch.IsmaConfig(
+        k=10, r=30, c=50, tau=0.999, strategy="ort", seed=5), None)
+    cases["rank3_ort_fallback"] = (make_low_rank(60, 30, 3, np.random.default_rng(10)),
+                                   podsketch.IsmaConfig(k=3, strategy="ort", tau=0.99, c=100,
+                                                        seed=5), None)
     # config-2 generator proxy (64 x 64 grid, n=300)
     a2 = workloads.config2(seed=1, side=64, n=300)
     cases["cfg2proxy_l2n"] = (a2, podsketch.IsmaConfig(

@@ -31,6 +31,8 @@ class Recorder:
 
 
 def _matrix(name):
+    if name == "rank3_ort_fallback":
+        return make_low_rank(60, 30, 3, np.random.default_rng(10))
     if name.startswith("cfg1"):
         return workloads.config1(seed=0)
     if name.startswith("rank3"):
@@ -43,7 +45,8 @@ def _matrix(name):
 
 
 GOLDEN_CASES = ["cfg1_l2n_modes", "cfg1_unf_subspace", "cfg1_l2n_nofinal_keep11",
-                "rank3_unf", "rank3_l2n", "exhaustive_40x18", "cfg2proxy_l2n"]
+                "rank3_unf", "rank3_l2n", "exhaustive_40x18", "cfg2proxy_l2n", "cfg1_ort_modes",
+                "rank3_ort_fallback"]
 
 
 @pytest.mark.parametrize("name", GOLDEN_CASES)

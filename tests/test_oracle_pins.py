@@ -13,6 +13,9 @@ from paper_1905_05107_b200 import workloads
 def _case_matrix(name):
     if name.startswith("cfg1"):
         return workloads.config1(seed=0)
+    if name == "rank3_ort_fallback":
+        from conftest import make_low_rank
+        return make_low_rank(60, 30, 3, np.random.default_rng(10))
     if name.startswith("rank3"):
         from conftest import make_low_rank
         return make_low_rank(100, 60, 3, np.random.default_rng(7))
@@ -24,7 +27,8 @@ def _case_matrix(name):
 
 
 CASES = ["cfg1_l2n_modes", "cfg1_unf_subspace", "cfg1_l2n_nofinal_keep11",
-         "rank3_unf", "rank3_l2n", "exhaustive_40x18", "cfg2proxy_l2n"]
+         "rank3_unf", "rank3_l2n", "exhaustive_40x18", "cfg2proxy_l2n", "cfg1_ort_modes",
+         "rank3_ort_fallback"]
 
 
 @pytest.mark.parametrize("name", CASES)
