@@ -56,7 +56,9 @@ int pod_colnorms2_f64(const double* A, int64_t m, int64_t n, int64_t lda, double
  * live columns (sampling.py:150-155); mode 2: explicit normalised weights
  * over positions 0..n-1 (a Distribution's weights, no live mask); mode 3:
  * "ort" -- raw squared residuals over live columns, falling back to uniform
- * when their sum <= thr (isma.py:216-220) -- and the
+ * when their sum <= thr (isma.py:216-220); mode 4: row draw -- raw weights
+ * over all positions normalised as mode 0, no live mask, no retirement,
+ * p_out (nullable) = normalised weight of each drawn position -- and the
  * candidate-set update isma.py:164 (drawn columns cleared in `live`).
  * `uniforms` holds the c variates of ONE rng.random(c) batch.
  * Outputs: idx_out[0..g) ascending int32 (idx_out[g..cap) = -1: zero-column
@@ -66,7 +68,20 @@ int pod_colnorms2_f64(const double* A, int64_t m, int64_t n, int64_t lda, double
 size_t pod_draw_ws_bytes(int64_t n);
 int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n, const double* uniforms,
              int64_t c, int32_t* idx_out, int64_t* cnt_out, int64_t cap, void* ws,
-             size_t ws_bytes, int64_t* info, double thr, void* stream);
+             size_t ws_bytes, int64_t* info, double thr, double* p_out, void* stream);
+
+/* Row sampling (ICRS) building blocks, isma.py:168-176:
+ * out[i] = (sum_j X[i, cols[j]]^2) / div (div = *div_dev when non-null) --
+ * row_norm_distribution of the sampled block (sampling.py:143-147, div 1) or
+ * leverage scores of the top-k basis (sampling.py:190-201, div k); and the dedup-scaled row block
+ * Y[i, :] = A[rows[i], cols] sqrt(cnt[i] / (w p[i])) (scale_sampled_rows,
+ * sampling.py:248-258) for i < *hdev. */
+int pod_rownorms2(const double* X, int64_t m, int64_t ncols, int64_t ldx, const int32_t* cols,
+                  double div, const double* div_dev, double* out, void* stream);
+int pod_gather_scale_rows(const double* A, int64_t lda, const int32_t* cols, int64_t g,
+                          const int32_t* rows, const int64_t* cnt, const double* p, double w,
+                          int64_t hcap, const int64_t* hdev, double* Y, int64_t ldy,
+                          void* stream);
 
 /* Squared residual norms after projection on an orthonormal basis:
  * out[j] = ||A[:, cols[j]] - U C[:, j]||^2 with C = U^T A[:, cols] (r x n,

@@ -148,6 +148,31 @@ def residual_weights(a, u, candidates, degenerate_rtol=1e-14):
     return w / w.sum()
 
 
+def row_weights(d):
+    """sampling.py:143-147 -- rows of the sampled block by squared norm."""
+    return normalized_weights(np.einsum("ij,ij->i", d, d))
+
+
+def leverage_weights(u):
+    """sampling.py:190-201 -- leverage scores ||u_i||^2 / k, normalised."""
+    return normalized_weights(np.einsum("ij,ij->i", u, u) / u.shape[1])
+
+
+def scaled_rows(d, uniq, counts, weights, w):
+    """sampling.py:225-258 (_scale_factors + scale_sampled_rows, dedup) --
+    Y = d[uniq] * sqrt(t_i / (w q_i))."""
+    f = np.sqrt(counts / (w * weights[uniq]))
+    return np.asfortranarray(d[uniq, :] * f[:, None])
+
+
+def orthonormalize(u):
+    """isma.py:244-254 -- Q R = u, U_R = SVD(R), canonical signs of Q U_R."""
+    q0, rr = householder_qr(u)
+    ur, _, _ = lapack_svd(rr)
+    q, _ = canon_signs(q0 @ ur)
+    return q
+
+
 def margin_to_cdf_boundary(weights, uniforms):
     """Smallest |u - cum| over draws and CDF breakpoints (tie-risk monitor,
     SURVEY.md section 8c)."""
@@ -249,14 +274,18 @@ def finalize(a, u):
 # --------------------------------------------------------------------------
 
 def run(a, k, *, r=None, c, tau, strategy="l2n", criterion="modes", seed=0,
-        rng=None, do_finalize=True, keep=None, monitor=False, max_rounds=None):
-    """isma.py:225-303 restricted to the column-only path (rows=False) with
-    strategies l2n / unf.  Returns a dict with u, sigma, v (or None), and a
-    per-round trace list of dicts (iteration, unique, counts, remaining,
-    cosines, wall_time[, margin]) plus phase timings.  ``max_rounds`` stops
-    after that many update rounds (a bounded CPU-timing sample only)."""
-    if strategy not in ("l2n", "unf", "ort"):
-        raise OracleParamError("oracle covers strategies l2n, unf and ort")
+        rng=None, do_finalize=True, keep=None, monitor=False, max_rounds=None,
+        rows=False, w=None):
+    """isma.py:225-303: column sampling (strategies l2n / unf / ort) or,
+    with rows=True and a row budget w, ICRS row sampling (unf / ort / ls).
+    Returns a dict with u, sigma, v (or None), and a per-round trace list of
+    dicts (iteration, unique, counts, remaining, cosines, wall_time[, rows,
+    row_counts][, margin]) plus phase timings.  ``max_rounds`` stops after
+    that many update rounds (a bounded CPU-timing sample only)."""
+    if strategy not in (("unf", "ort", "ls") if rows else ("l2n", "unf", "ort")):
+        raise OracleParamError("strategy not valid for this sampling mode")
+    if rows and (w is None or int(w) < 1):
+        raise OracleParamError("row sampling needs a row budget w >= 1")
     a = dense_f64(a)
     m, n = a.shape
     r = 3 * k if r is None else r
@@ -272,21 +301,30 @@ def run(a, k, *, r=None, c, tau, strategy="l2n", criterion="modes", seed=0,
     t_norm = time.perf_counter() - t_start
     trace = []
 
-    def one_round(s, weights):
+    def one_round(s, weights, u_prev=None):
         t0 = time.perf_counter()
         uni = rng.random(int(c))
         idx, counts = cdf_draw(s, weights, uni)
         d = np.asfortranarray(a[:, idx])
         rest = np.setdiff1d(s, idx, assume_unique=True)
-        sig, v = gram_eig(d)
-        u2, s2 = lift(d, sig, v, r)
         info = {"unique": idx, "counts": counts, "remaining": rest.size, "t0": t0}
+        if not rows:
+            sig, v = gram_eig(d)
+        else:                                                   # isma.py:168-176
+            q = row_weights(d) if u_prev is None or u_prev.shape[1] == 0 \
+                else leverage_weights(u_prev)
+            ridx, rcnt = cdf_draw(np.arange(m), q, rng.random(int(w)))
+            sig, v = gram_eig(scaled_rows(d, ridx, rcnt, q, int(w)))
+            info.update(rows=ridx, row_counts=rcnt)
+        u2, s2 = lift(d, sig, v, r)
         if monitor:
             info["margin"] = margin_to_cdf_boundary(weights, uni)
         return u2, s2, rest, info
 
     s = np.arange(n)
     u, sig, s, info = one_round(s, normalized_weights(norms2))
+    if rows and sig.size:
+        u = orthonormalize(u)                                   # isma.py:267-269
     info.update(iteration=0, cosines=np.zeros(0),
                 wall_time=time.perf_counter() - info.pop("t0"))
     trace.append(info)
@@ -298,16 +336,20 @@ def run(a, k, *, r=None, c, tau, strategy="l2n", criterion="modes", seed=0,
         it += 1
         if strategy == "l2n":
             try:
-                w = normalized_weights(norms2[s])
+                wts = normalized_weights(norms2[s])
             except OracleDegenerate:
                 break
         elif strategy == "ort":
-            w = residual_weights(a, u, s)
-            if w is None:
-                w = uniform_weights(s.size)
+            wts = residual_weights(a, u, s)
+            if wts is None:
+                wts = uniform_weights(s.size)
         else:
-            w = uniform_weights(s.size)
-        u2, s2, s, info = one_round(s, w)
+            wts = uniform_weights(s.size)
+        u_rows = None
+        if rows and strategy == "ls" and sig.size:
+            # factor.truncate(k) (matcore.py:118-128): a C-order copy when it cuts
+            u_rows = u if k >= u.shape[1] else u[:, :k].copy()
+        u2, s2, s, info = one_round(s, wts, u_rows)
         um, sm = merge(u, sig, u2, s2, r)
         xi = cosines(u, um, k, criterion)
         u, sig = um, sm
@@ -350,7 +392,7 @@ def principal_angle_sines(u1, u2):
 
 
 def incremental(blocks, k, *, r=None, c, tau, strategy="l2n", criterion="modes",
-                seed=0):
+                seed=0, rows=False, w=None):
     """ooc.py:105-148 -- one-pass fold: per column block an ISMA run with
     finalize off and keep=r sharing ONE generator, then a rank-r merge into
     the accumulator; final truncation to k."""
@@ -361,7 +403,7 @@ def incremental(blocks, k, *, r=None, c, tau, strategy="l2n", criterion="modes",
     for blk in blocks:
         kk = min(k, min(blk.shape))
         out = run(blk, kk, r=r, c=c, tau=tau, strategy=strategy,
-                  criterion=criterion, rng=rng, do_finalize=False, keep=r)
+                  criterion=criterion, rng=rng, do_finalize=False, keep=r, rows=rows, w=w)
         trace.extend(out["trace"])
         if acc_u is None:
             acc_u, acc_s = out["u"], out["sigma"]

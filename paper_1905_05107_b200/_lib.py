@@ -36,7 +36,10 @@ SIGNATURES = {
     "pod_colnorms2_f64": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "pod_draw_ws_bytes": (_sz, [_i64]),
     "pod_draw": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp, _f64,
-                        _vp]),
+                        _vp, _vp]),
+    "pod_rownorms2": (_i32, [_vp, _i64, _i64, _i64, _vp, _f64, _vp, _vp, _vp]),
+    "pod_gather_scale_rows": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _f64, _i64, _vp, _vp,
+                                     _i64, _vp]),
     "pod_resid_ws_bytes": (_sz, [_i64, _i64]),
     "pod_resid_colnorms2": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp,
                                    _vp, _sz, _vp]),

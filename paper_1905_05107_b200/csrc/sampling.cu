@@ -125,11 +125,17 @@ __device__ int64_t block_excl_scan_i64(int64_t v, int64_t* sh, int64_t* total) {
 // mode 2: explicit normalised weights over all n positions (no live mask)
 // mode 3: ort over live columns: raw squared residuals normalised twice, or
 //         uniform when their sum <= thr (isma.py:216-220, sampling.py:182-186)
+// mode 4: rows -- raw weights over all n positions normalised twice (like
+//         mode 0) without a live mask and without retirement; p_out receives
+//         the normalised weight of every drawn position (sampling.py:225-258)
 __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
     int mode, const double* __restrict__ raw, uint8_t* __restrict__ live, int64_t n,
     const double* __restrict__ uni, int64_t c, int32_t* __restrict__ idx_out,
     int64_t* __restrict__ cnt_out, int64_t cap, double* __restrict__ cum,
-    int32_t* __restrict__ counts, int64_t* __restrict__ info, double thr) {
+    int32_t* __restrict__ counts, int64_t* __restrict__ info, double thr,
+    double* __restrict__ p_out) {
+  const bool rows = (mode == 4);
+  if (rows) mode = 0;
   __shared__ double shd[DRAW_THREADS + 1];
   __shared__ int64_t shi[DRAW_THREADS + 1];
   __shared__ double red[32];
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
 
   // |S| = number of live candidates
   int64_t nlive_local = 0;
-  for (int64_t j = j0; j < j1; ++j) nlive_local += (mode == 2) ? 1 : (live[j] != 0);
+  for (int64_t j = j0; j < j1; ++j) nlive_local += (mode == 2 || rows) ? 1 : (live[j] != 0);
   int64_t nlive = 0;
   (void)block_excl_scan_i64(nlive_local, shi, &nlive);
   if (nlive == 0) {
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
   const double inv_s = 1.0 / (double)nlive;
   double loc = 0.0;
   if (mode == 3) {  // residual weights, or the uniform fallback
-    for (int64_t j = j0; j < j1; ++j) loc += live[j] ? raw[j] : 0.0;
+    for (int64_t j = j0; j < j1; ++j) loc += (rows || live[j]) ? raw[j] : 0.0;
     const double tot = block_sum(loc, red);
     mode = (tot <= thr) ? 1 : 0;
     loc = 0.0;
@@ -159,12 +165,13 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
   for (int64_t j = j0; j < j1; ++j) {
     double w;
     if (mode == 2) w = raw[j];
-    else if (live[j] == 0) w = 0.0;
+    else if (!rows && live[j] == 0) w = 0.0;
     else w = (mode == 0) ? raw[j] : inv_s;
     cum[j] = w;
     loc += w;
   }
   double total = block_sum(loc, red);
+  double total1 = 1.0;
   if (mode == 2) total = 1.0;  // a Distribution's weights are used as given (sampling.py:214)
   if (mode == 0) {
     if (!(total > 0.0)) {
@@ -174,6 +181,7 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
     }
     loc = 0.0;
     for (int64_t j = j0; j < j1; ++j) { double w = cum[j] / total; cum[j] = w; loc += w; }
+    total1 = total;
     total = block_sum(loc, red);
   }
   // renormalise and scan
@@ -219,8 +227,9 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
     if (counts[j] > 0) {
       idx_out[pos] = (int32_t)j;
       cnt_out[pos] = counts[j];
+      if (p_out) p_out[pos] = (raw[j] / total1) / total;  // the Distribution's weight
       ++pos;
-      if (mode != 2) live[j] = 0;
+      if (mode != 2 && !rows) live[j] = 0;
     }
   }
   for (int64_t j = g + t; j < cap; j += DRAW_THREADS) idx_out[j] = -1;  // zero-column padding
@@ -260,20 +269,88 @@ extern "C" size_t pod_draw_ws_bytes(int64_t n) {
 extern "C" int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n,
                         const double* uniforms, int64_t c, int32_t* idx_out, int64_t* cnt_out,
                         int64_t cap, void* ws, size_t ws_bytes, int64_t* info, double thr,
-                        void* stream) {
-  POD_REQUIRE(mode >= 0 && mode <= 3, "pod_draw: bad mode %d", mode);
+                        double* p_out, void* stream) {
+  POD_REQUIRE(mode >= 0 && mode <= 4, "pod_draw: bad mode %d", mode);
   POD_REQUIRE(n > 0 && n < (int64_t)INT32_MAX, "pod_draw: bad n");
   POD_REQUIRE(c >= 1, "sample count must be >= 1");
   POD_REQUIRE(ws_bytes >= pod_draw_ws_bytes(n), "pod_draw: workspace too small");
   POD_REQUIRE(cap >= std::min<int64_t>(c, n), "pod_draw: output capacity %lld < min(c, n)",
               (long long)cap);
   POD_REQUIRE(mode == 1 || weights != nullptr, "pod_draw: weights required");
-  POD_REQUIRE(mode == 2 || live != nullptr, "pod_draw: live mask required");
+  POD_REQUIRE(mode == 2 || mode == 4 || live != nullptr, "pod_draw: live mask required");
+  POD_REQUIRE(p_out == nullptr || mode == 4 || mode == 0, "pod_draw: p_out needs mode 0 or 4");
   double* cum = (double*)ws;
   int32_t* counts = (int32_t*)(cum + n);
   draw_kernel<<<1, DRAW_THREADS, 0, (cudaStream_t)stream>>>(mode, weights, live, n, uniforms, c,
                                                               idx_out, cnt_out, cap, cum, counts,
-                                                              info, thr);
+                                                              info, thr, p_out);
   POD_CHECK_LAUNCH("draw");
+  return POD_OK;
+}
+
+namespace pod {
+// out[i] = (sum_j X[i, cols[j]]^2) / div (cols -1: zero column), one thread per
+// row; div = *div_dev when given (a graph-invariant launch with a per-round k)
+__global__ void rownorms2_kernel(const double* __restrict__ X, int64_t m, int ncols, int64_t ldx,
+                                 const int32_t* __restrict__ cols, double div,
+                                 const double* __restrict__ div_dev, double* __restrict__ out) {
+  if (div_dev) div = *div_dev;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < ncols; ++j) {
+      const int64_t c = cols ? (int64_t)cols[j] : (int64_t)j;
+      if (c < 0) continue;
+      const double v = X[i + c * ldx];
+      s = fma(v, v, s);
+    }
+    out[i] = s / div;
+  }
+}
+
+// Y[i, j] = A[rows[i], cols[j]] * sqrt(cnt[i] / (w p[i])) for i < h (rows -1: zero)
+__global__ void gather_scale_rows_kernel(const double* __restrict__ A, int64_t lda,
+                                         const int32_t* __restrict__ cols, int g,
+                                         const int32_t* __restrict__ rows,
+                                         const int64_t* __restrict__ cnt,
+                                         const double* __restrict__ p, double w, int hcap,
+                                         const int64_t* __restrict__ hdev,
+                                         double* __restrict__ Y, int64_t ldy) {
+  const int64_t h = *hdev;
+  const int64_t tot = (int64_t)hcap * g;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(t / hcap), i = (int)(t - (int64_t)j * hcap);
+    double v = 0.0;
+    if (i < h) {
+      const int64_t c = cols ? (int64_t)cols[j] : (int64_t)j;
+      const int64_t r = rows[i];
+      if (c >= 0 && r >= 0) v = A[r + c * lda] * sqrt((double)cnt[i] / (w * p[i]));
+    }
+    Y[i + (int64_t)j * ldy] = v;
+  }
+}
+}  // namespace pod
+
+extern "C" int pod_rownorms2(const double* X, int64_t m, int64_t ncols, int64_t ldx,
+                             const int32_t* cols, double div, const double* div_dev, double* out,
+                             void* stream) {
+  POD_REQUIRE(m >= 1 && ncols >= 0 && ldx >= m, "pod_rownorms2: bad shape");
+  const int grid = (int)std::min<int64_t>(ceil_div(m, 256), 148 * 16);
+  rownorms2_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(X, m, (int)ncols, ldx, cols, div,
+                                                                      div_dev, out);
+  POD_CHECK_LAUNCH("rownorms2");
+  return POD_OK;
+}
+
+extern "C" int pod_gather_scale_rows(const double* A, int64_t lda, const int32_t* cols, int64_t g,
+                                     const int32_t* rows, const int64_t* cnt, const double* p,
+                                     double w, int64_t hcap, const int64_t* hdev, double* Y,
+                                     int64_t ldy, void* stream) {
+  POD_REQUIRE(g >= 1 && hcap >= 1 && ldy >= hcap, "pod_gather_scale_rows: bad shape");
+  const int grid = (int)std::min<int64_t>(ceil_div(hcap * g, 256), 148 * 8);
+  gather_scale_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, cols, (int)g, rows, cnt,
+                                                                     p, w, (int)hcap, hdev, Y, ldy);
+  POD_CHECK_LAUNCH("gather_scale_rows");
   return POD_OK;
 }

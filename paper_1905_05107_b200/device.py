@@ -78,6 +78,7 @@ class Ctx:
             device = torch.device("cuda", torch.cuda.current_device())
         self.device = torch.device(device)
         self._ws = {}
+        self.ws_epoch = 0
         self.info = torch.zeros(16, dtype=torch.int64, device=self.device)
         self.dinfo = torch.zeros(16, dtype=torch.float64, device=self.device)
         self.h_info = torch.zeros(16, dtype=torch.int64).pin_memory()
@@ -113,6 +114,7 @@ class Ctx:
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
             self._ws[key] = buf
+            self.ws_epoch += 1  # captured graphs holding the old buffer are stale
         return buf
 
     def read_info(self, n=4):
@@ -130,12 +132,22 @@ class Ctx:
         self._call("colnorms2", 1, 2.0 * A.m * A.ncols, 8.0 * A.m * A.ncols, "pod_colnorms2_f64", A.ptr, A.m, A.ncols, A.ld, _ptr(out), _ptr(flag),
                   self.stream)
 
-    def draw(self, mode, weights, live, n, uniforms, c, idx, cnt, info=None, thr=0.0):
+    def draw(self, mode, weights, live, n, uniforms, c, idx, cnt, info=None, thr=0.0, p_out=None):
         ws = self.ws("draw", _lib.load().pod_draw_ws_bytes(n))
         self._call("draw", 1, 0.0, 24.0 * n + 8.0 * c, "pod_draw", mode, _ptr(weights),
                    _ptr(live), n, _ptr(uniforms), c, _ptr(idx), _ptr(cnt), idx.numel(), _ptr(ws),
                    ws.numel(), _ptr(self.info if info is None else info), float(thr),
+                   _ptr(p_out), self.stream)
+
+    def rownorms2(self, X, ncols, out, cols=None, div=1.0, div_dev=None):
+        self._call("rownorms2", 1, 2.0 * X.m * ncols, 8.0 * X.m * ncols, "pod_rownorms2", X.ptr,
+                   X.m, ncols, X.ld, _ptr(cols), float(div), _ptr(div_dev), _ptr(out),
                    self.stream)
+
+    def gather_scale_rows(self, A, cols, g, rows, cnt, p, w, hcap, hdev, Y):
+        self._call("gather_scale_rows", 1, 0.0, 8.0 * hcap * g, "pod_gather_scale_rows", A.ptr,
+                   A.ld, _ptr(cols), g, _ptr(rows), _ptr(cnt), _ptr(p), float(w), hcap,
+                   _ptr(hdev), Y.ptr, Y.ld, self.stream)
 
     def resid_colnorms2(self, A, n, U, r, C, ldc, out, cols=None):
         ws = self.ws("resid", _lib.load().pod_resid_ws_bytes(A.m, n))

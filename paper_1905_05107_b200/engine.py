@@ -43,13 +43,16 @@ from .errors import DegenerateDistributionError, ParameterError
 REORTH_TOL = 1e-8  # merge.py:34
 CHOLQR_PASSES = 4  # pass 0 always; passes 1..3 gated on the previous pass
 
-MODE_L2N, MODE_UNIFORM, MODE_WEIGHTS, MODE_ORT = 0, 1, 2, 3
+MODE_L2N, MODE_UNIFORM, MODE_WEIGHTS, MODE_ORT, MODE_ROWS = 0, 1, 2, 3, 4
 ORT_DEGENERATE_RTOL = 1e-14  # sampling.py:158 degenerate_rtol
 
 # round record slots (int64)
 REC_G, REC_REM, REC_STATUS, REC_RANK, REC_KEEP_UPD, REC_EIGH_SWEEPS, REC_KEEP, REC_MERGE_SWEEPS = \
     range(8)
-REC_LEN = 8  # rec[0]: merge record; rec[1 + b]: update record of buffer b
+REC_H, REC_HREM, REC_HSTATUS = 8, 9, 10  # row draw (ICRS): distinct rows, -, status
+REC_LEN = 11  # rec[0]: merge record; rec[1 + b]: update record of buffer b
+UPDATE_FIELDS = (REC_G, REC_REM, REC_STATUS, REC_RANK, REC_KEEP_UPD, REC_EIGH_SWEEPS, REC_H,
+                 REC_HREM, REC_HSTATUS)
 
 # gate slots (int32)
 G_QR = 0            # main CholeskyQR passes: slots 0..4
@@ -209,7 +212,7 @@ class MergeWorkspace:
         torch.cuda.current_stream(self.ctx.device).synchronize()
         hr = self.h_rec.tolist()
         rec = [int(x) for x in hr[0]]
-        for i in (REC_G, REC_REM, REC_STATUS, REC_RANK, REC_KEEP_UPD, REC_EIGH_SWEEPS):
+        for i in UPDATE_FIELDS:
             rec[i] = int(hr[1 + ub][i])
         xi = np.clip(np.abs(self.h_xi.numpy().astype(np.float64)), 0.0, 1.0)
         return rec, xi
@@ -262,7 +265,7 @@ class IsmaEngine(MergeWorkspace):
     other generator objects run without the pipeline)."""
 
     def __init__(self, ctx, A, *, k, r, c, criterion="modes", use_graphs=True, comm=None,
-                 row_offset=0, m_total=None):
+                 row_offset=0, m_total=None, w=0):
         self.A = A
         self.n = A.ncols
         self.c = int(c)
@@ -287,9 +290,27 @@ class IsmaEngine(MergeWorkspace):
         self.use_graphs = use_graphs
         self.graphs = {}
         self.graph_launches = {}
+        self.graph_epoch = -1
         self.side = torch.cuda.Stream(dev)
         self.ort = None  # (C = U^T A, residual norms) buffers of the "ort" strategy
         self.frob2 = 0.0
+        # row sampling (ICRS, isma.py:168-176): w row draws per round over the m rows
+        self.w = int(w)
+        if self.w:
+            if self.comm.active:
+                raise NotImplementedError("row sampling is not row-sharded")
+            m = self.m
+            self.hcap = min(self.w, m)
+            self.rowq = torch.empty(m, **f64)
+            self.uniw = [torch.empty(self.w, **f64) for _ in range(2)]
+            self.h_uniw = [torch.empty(self.w, dtype=torch.float64).pin_memory()
+                           for _ in range(2)]
+            self.ridx = [torch.empty(self.hcap, dtype=torch.int32, device=dev) for _ in range(2)]
+            self.rcnt = [torch.empty(self.hcap, dtype=torch.int64, device=dev) for _ in range(2)]
+            self.rp = [torch.empty(self.hcap, **f64) for _ in range(2)]
+            self.Y = [ColMat.zeros(self.hcap, g, dev) for _ in range(2)]
+            self.levdiv = torch.ones(1, **f64)
+            self.h_levdiv = torch.ones(1, dtype=torch.float64).pin_memory()
 
     def reset(self):
         """Per-run state (the captured graphs and buffers are reused)."""
@@ -329,9 +350,12 @@ class IsmaEngine(MergeWorkspace):
         self.comm.allreduce_sum_(res2)
         return res2
 
-    def update_ops(self, mode, b, dest, cur=None):
-        """get_update (isma.py:144-178), column path, at capacity, into
-        update buffer b (its own draw/Gram/eigensolver scratch)."""
+    def update_ops(self, mode, b, dest, cur=None, rowsrc=None):
+        """get_update (isma.py:144-178) at capacity into update buffer b (its
+        own draw/Gram/eigensolver scratch).  rowsrc None: column path (Gram
+        of the gathered columns D).  rowsrc "norms"/"lev": ICRS -- w rows
+        drawn from D's squared row norms or from the leverage of the current
+        top-k basis (stack `cur`), the dedup-scaled row block Y and Y^T Y."""
         ctx, A, g, r = self.ctx, self.A, self.gcap, self.r
         self.uni[b].copy_(self.h_uni[b], non_blocking=True)
         weights, thr = None, 0.0
@@ -342,9 +366,23 @@ class IsmaEngine(MergeWorkspace):
             thr = ORT_DEGENERATE_RTOL * self.frob2
         ctx.draw(mode, weights, self.live, self.n, self.uni[b], self.c, self.idx[b], self.cnt[b],
                  info=self.rec[1 + b, REC_G:], thr=thr)
-        ctx.tn(g, g, 1.0, A, A, dptr(self.G[b]), g, xcols=self.idx[b], ycols=self.idx[b],
-               tag="tn_gram_gather")                                         # baselines.py:43
-        self.comm.allreduce_sum_(self.G[b])
+        if rowsrc is None:
+            ctx.tn(g, g, 1.0, A, A, dptr(self.G[b]), g, xcols=self.idx[b], ycols=self.idx[b],
+                   tag="tn_gram_gather")                                     # baselines.py:43
+            self.comm.allreduce_sum_(self.G[b])
+        else:
+            self.uniw[b].copy_(self.h_uniw[b], non_blocking=True)
+            if rowsrc == "lev":                                              # sampling.py:190-201
+                self.levdiv.copy_(self.h_levdiv, non_blocking=True)
+                ctx.rownorms2(self.S[cur], self.k, self.rowq, div_dev=self.levdiv)
+            else:                                                            # sampling.py:143-147
+                ctx.rownorms2(A, g, self.rowq, cols=self.idx[b])
+            hinfo = self.rec[1 + b, REC_H:]
+            ctx.draw(MODE_ROWS, self.rowq, None, self.m, self.uniw[b], self.w, self.ridx[b],
+                     self.rcnt[b], info=hinfo, p_out=self.rp[b])
+            ctx.gather_scale_rows(A, self.idx[b], g, self.ridx[b], self.rcnt[b], self.rp[b],
+                                  self.w, self.hcap, hinfo, self.Y[b])      # sampling.py:248-258
+            ctx.tn(g, g, 1.0, self.Y[b], self.Y[b], dptr(self.G[b]), g, tag="tn_gram_rows")
         ctx.gram_eigh(dptr(self.G[b]), g, g, r, self.sig_upd_b[b], dptr(self.Tl[b]), g,
                       info=self.rec[1 + b, REC_RANK:])                       # baselines.py:44-48
         ctx.nn(g, r, 1.0, A, dptr(self.Tl[b]), g, dest, xcols=self.idx[b],
@@ -364,24 +402,26 @@ class IsmaEngine(MergeWorkspace):
         if join:
             main.wait_stream(self.side)
 
-    def round_ops(self, mode, cur, ub, pipelined):
+    def round_ops(self, mode, cur, ub, pipelined, rowsrc=None):
         """Round t: merge(t) with update buffer ub (+ cosines, readback);
         pipelined: update(t+1) into buffer 1 - ub concurrently."""
         if pipelined:
             self.update_side_ops(mode, 1 - ub, join=False)  # update(t+1) || merge(t)
         else:
-            self.update_ops(mode, ub, self.Uupd_b[ub].cols(0, self.r), cur=cur)
+            self.update_ops(mode, ub, self.Uupd_b[ub].cols(0, self.r), cur=cur, rowsrc=rowsrc)
         self.merge_ops(cur, ub)
         self.cosines_ops(cur, 1 - cur)
         if pipelined:
             torch.cuda.current_stream(self.ctx.device).wait_stream(self.side)
         self.readback()
 
-    def launch_round(self, mode, cur, ub, pipelined):
+    def launch_round(self, mode, cur, ub, pipelined, rowsrc=None):
         if not self.use_graphs or self.ctx.prof is not None or self.comm.active:
-            self.round_ops(mode, cur, ub, pipelined)
+            self.round_ops(mode, cur, ub, pipelined, rowsrc)
             return
-        key = (mode, cur, ub, pipelined)
+        key = (mode, cur, ub, pipelined, rowsrc)
+        if self.graphs and self.graph_epoch != self.ctx.ws_epoch:
+            self.graphs.clear()  # a workspace was reallocated since these were captured
         gr = self.graphs.get(key)
         if gr is None:
             dev = self.ctx.device
@@ -392,18 +432,21 @@ class IsmaEngine(MergeWorkspace):
             st = torch.cuda.Stream(dev)
             st.wait_stream(torch.cuda.current_stream(dev))
             with torch.cuda.stream(st):
-                self.round_ops(mode, cur, ub, pipelined)
+                self.round_ops(mode, cur, ub, pipelined, rowsrc)
             torch.cuda.current_stream(dev).wait_stream(st)
             torch.cuda.synchronize(dev)
             for dst, src in zip(keep, saved):
                 dst.copy_(src)
             torch.cuda.synchronize(dev)
+            if self.graph_epoch != self.ctx.ws_epoch:
+                self.graphs.clear()  # the warm-up grew a workspace other graphs captured
             gr = torch.cuda.CUDAGraph()
             l0 = self.ctx.launches
             with torch.cuda.graph(gr, stream=st):
-                self.round_ops(mode, cur, ub, pipelined)
+                self.round_ops(mode, cur, ub, pipelined, rowsrc)
             self.graph_launches[key] = self.ctx.launches - l0
             self.graphs[key] = gr
+            self.graph_epoch = self.ctx.ws_epoch
             torch.cuda.synchronize(dev)
         gr.replay()
         self.ctx.launches += self.graph_launches[key]
@@ -434,11 +477,38 @@ class IsmaEngine(MergeWorkspace):
         return Vnew
 
     # ------------------------------------------------------------ driver ---
-    def _stage_uniforms(self, rng, b):
-        u = np.asarray(rng.random(int(self.c)), dtype=np.float64)  # one batch (sampling.py:213)
+    def _stage_uniforms(self, rng, b, rows=False):
+        """One rng.random(c) batch for the column draw (sampling.py:213); with
+        rows, then one rng.random(w) batch for the row draw (isma.py:173)."""
+        u = np.asarray(rng.random(int(self.c)), dtype=np.float64)
         if u.shape != (self.c,):
             raise ParameterError("generator returned a batch of the wrong shape")
         self.h_uni[b].numpy()[:] = u
+        if rows:
+            u = np.asarray(rng.random(int(self.w)), dtype=np.float64)
+            if u.shape != (self.w,):
+                raise ParameterError("generator returned a batch of the wrong shape")
+            self.h_uniw[b].numpy()[:] = u
+
+    def _check_rows(self, rec, rng, state):
+        """A zero row distribution raises (sampling.py:62-64) before the row
+        batch is drawn in the reference: restore the generator, then raise."""
+        if rec[REC_HSTATUS] == 2:
+            if state is not None:
+                rng.bit_generator.state = state
+            raise DegenerateDistributionError("all row weights are zero")
+
+    def _orthonormalize_ops(self, cur, l):
+        """isma.py:267-269 / orthonormalize (isma.py:244-254): Q0 R = U
+        (CholeskyQR into the stack's Q half), U_R = SVD(R), U <- fix_signs(Q0
+        U_R); sigma is kept."""
+        ctx, r = self.ctx, self.r
+        S = self.S[cur]
+        U, Q0 = S.cols(0, l), S.cols(r, r + l)
+        self.cholqr_ops(U, Q0, l, self.Rt, G_QR)
+        ctx.svd_small(dptr(self.Rt), r, l, l, dptr(self.Rt2), r, self.sig_upd_b[1][:l], None, 1)
+        ctx.nn(l, l, 1.0, Q0, dptr(self.Rt2), r, U, tag="nn_orthonormalize")
+        self.fix_signs_ops(U, l)
 
     def run(self, rng, *, strategy, tau, finalize, keep, trace_cls):
         """isma_run main loop (isma.py:258-303) on the device."""
@@ -451,18 +521,28 @@ class IsmaEngine(MergeWorkspace):
         # state can be rolled back support that
         bitgen = getattr(rng, "bit_generator", None)
         mode = {"l2n": MODE_L2N, "ort": MODE_ORT}.get(strategy, MODE_UNIFORM)
-        # ort's distribution depends on the merged basis: no pipelining
-        pipelined = bitgen is not None and not self.comm.active and mode != MODE_ORT
-        self._stage_uniforms(rng, 0)
-        self.update_ops(MODE_L2N, 0, self.S[cur].cols(0, r))                 # bootstrap
+        rows = self.w > 0
+        # ort's distribution depends on the merged basis, and so does the
+        # leverage-driven row draw: no pipelining for either (nor for ICRS)
+        pipelined = (bitgen is not None and not self.comm.active and mode != MODE_ORT
+                     and not rows)
+        state = bitgen.state if (rows and bitgen is not None) else None
+        self._stage_uniforms(rng, 0, rows)
+        self.update_ops(MODE_L2N, 0, self.S[cur].cols(0, r),                 # bootstrap
+                        rowsrc="norms" if rows else None)
         self.sig[cur].copy_(self.sig_upd_b[0][:r])
         self.readback()
         rec, _ = self.read_record(0)
-        g, rem, keep0 = rec[REC_G], rec[REC_REM], rec[REC_KEEP_UPD]
+        if rows:
+            self._check_rows(rec, rng, state)
+        g, rem, keep0, h = rec[REC_G], rec[REC_REM], rec[REC_KEEP_UPD], rec[REC_H]
         self.npos -= g
         self.sig[cur][keep0:].zero_()  # the basis carries keep0 modes; zero sigma padding
         self.l = keep0
-        traces.append(trace_cls(0, g, 0, rem, np.zeros(0), time.perf_counter() - t0))
+        if rows and keep0:
+            self._orthonormalize_ops(cur, keep0)                             # isma.py:267-269
+        traces.append(trace_cls(0, g, h if rows else 0, rem, np.zeros(0),
+                                time.perf_counter() - t0))
         xi = np.zeros(self.k)
         it = 0
         ub = 1
@@ -476,13 +556,20 @@ class IsmaEngine(MergeWorkspace):
             t0 = time.perf_counter()
             if mode == MODE_L2N and self.npos <= 0:
                 break  # l2n over only zero-norm columns (isma.py:211-215, 280-281)
+            rowsrc = None
             if pipelined:
                 saved_state = bitgen.state
                 self._stage_uniforms(rng, 1 - ub)                            # round it + 1
             else:
-                self._stage_uniforms(rng, ub)
-            self.launch_round(mode, cur, ub, pipelined)
+                if rows:
+                    state = bitgen.state if bitgen is not None else None
+                    rowsrc = "lev" if (strategy == "ls" and self.l) else "norms"  # isma.py:283-284
+                    self.h_levdiv[0] = float(min(self.k, self.l))
+                self._stage_uniforms(rng, ub, rows)
+            self.launch_round(mode, cur, ub, pipelined, rowsrc)
             rec, xi = self.read_record(ub)
+            if rows:
+                self._check_rows(rec, rng, state)
             g, rem = rec[REC_G], rec[REC_REM]
             if mode == MODE_L2N:
                 self.npos -= g
@@ -491,7 +578,8 @@ class IsmaEngine(MergeWorkspace):
             self.stats["rounds"] += 1
             self.stats.setdefault("eigh_sweeps", []).append(rec[REC_EIGH_SWEEPS])
             self.stats.setdefault("merge_sweeps", []).append(rec[REC_MERGE_SWEEPS])
-            traces.append(trace_cls(it, g, 0, rem, xi.copy(), time.perf_counter() - t0))
+            traces.append(trace_cls(it, g, rec[REC_H] if rows else 0, rem, xi.copy(),
+                                    time.perf_counter() - t0))
             if pipelined:
                 ub = 1 - ub
         if pipelined and saved_state is not None:
@@ -515,14 +603,15 @@ class IsmaEngine(MergeWorkspace):
 _ENGINE_CACHE = {}
 
 
-def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=0, m_total=None):
+def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=0, m_total=None,
+               w=0):
     """Reuse the engine (buffers + captured round graphs) of the previous run
     when the matrix buffer, shape and configuration match; one engine is
     cached per device.  Graph replay reads A and the staged uniforms at
     replay time, so a reused engine is valid for new contents of A."""
     world = 1 if comm is None else comm.world
     key = (A.t.data_ptr() + 8 * A.ld * A.col0, A.m, A.ncols, A.ld, int(k), int(r), int(c),
-           criterion, bool(use_graphs), ctx.device.index, world, int(row_offset), m_total)
+           criterion, bool(use_graphs), ctx.device.index, world, int(row_offset), m_total, int(w))
     eng = _ENGINE_CACHE.get(ctx.device.index)
     if eng is not None and eng.key == key:
         eng.A = A
@@ -530,7 +619,7 @@ def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=
         return eng
     _ENGINE_CACHE.pop(ctx.device.index, None)
     eng = IsmaEngine(ctx, A, k=k, r=r, c=c, criterion=criterion, use_graphs=use_graphs,
-                     comm=comm, row_offset=row_offset, m_total=m_total)
+                     comm=comm, row_offset=row_offset, m_total=m_total, w=w)
     eng.key = key
     _ENGINE_CACHE[ctx.device.index] = eng
     return eng

@@ -1,5 +1,5 @@
 """Iterative sampling and merging on the GPU -- drop-in for the reference's
-``podsketch.isma`` (isma.py:1-303), column-sampling path.
+``podsketch.isma`` (isma.py:1-303).
 
 Same names, arguments, defaults, validation and error classes as the
 reference: ``IsmaConfig`` (isma.py:59-119), ``IterationTrace``
@@ -9,9 +9,11 @@ numerics run in libpodsketch_b200.so (see engine.py); the caller's numpy
 Generator supplies the uniforms, one ``rng.random(c)`` batch per round,
 so sampled index sets follow the reference's stream.
 
-Not on this path (raise NotImplementedError rather than fall back):
-row sampling (``rows=True``, ICRS) and the ``ort`` strategy -- SURVEY.md
-section 8(f) ranks them next.
+Every strategy of the reference runs here: column sampling with "l2n",
+"unf" and "ort", and row sampling (``rows=True``, ICRS) with "unf", "ort"
+and "ls" -- one further ``rng.random(w)`` batch per round for the row draw.
+Row-sharded multi-GPU runs cover the column path only (row draws are global
+over all m rows).
 """
 
 from __future__ import annotations
@@ -20,7 +22,7 @@ import dataclasses
 
 import numpy as np
 
-from .errors import ParameterError
+from .errors import DegenerateDistributionError, ParameterError
 from .sampling import ctsvd_sample_count, ltsvd_sample_count
 
 STRATEGIES = ("l2n", "unf", "ort", "ls")
@@ -103,13 +105,6 @@ class IterationTrace:
         object.__setattr__(self, "cosines", cos)
 
 
-def _require_column_path(config):
-    if config.rows:
-        raise NotImplementedError("row sampling (rows=True) is not on the B200 path yet")
-    if config.strategy not in ("l2n", "unf", "ort"):
-        raise NotImplementedError(f"strategy {config.strategy!r} is not on the B200 path yet")
-
-
 def _validate_shape(a):
     from .device import ColMat
 
@@ -147,7 +142,6 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
 
     from .parallel import Comm, shard_rows
 
-    _require_column_path(config)
     a, m, n = _validate_shape(a)
     comm = comm if comm is not None else Comm()
     row_offset = 0
@@ -170,7 +164,8 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
     A = to_device_colmajor(a, ctx.device)
     eng = get_engine(ctx, A, k=k, r=config.r, c=config.column_budget(),
                      criterion=config.criterion, use_graphs=use_graphs, comm=comm,
-                     row_offset=row_offset, m_total=m if comm.active else None)
+                     row_offset=row_offset, m_total=m if comm.active else None,
+                     w=config.row_budget() if config.rows else 0)
     traces, v = eng.run(rng, strategy=config.strategy, tau=config.tau,
                         finalize=config.finalize, keep=keep, trace_cls=IterationTrace)
     u, s, vv = eng.result(keep, v)
@@ -184,25 +179,29 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
 
 
 def get_update(a, s, u_prev, dist, c, w, rows, rng, r):
-    """One sampling round (isma.py:144-178), column path, on the GPU.
+    """One sampling round (isma.py:144-178) on the GPU.
 
-    Draws ``c`` indices from ``dist`` (one ``rng.random(c)`` batch), factors
-    the distinct sampled columns through their Gram matrix and returns
-    ``(factor, remaining, g, h)``; an empty candidate set returns
-    ``(None, s, 0, 0)``.
+    Draws ``c`` indices from ``dist`` (one ``rng.random(c)`` batch) and
+    factors the distinct sampled columns D.  rows=False: through the Gram
+    matrix D^T D.  rows=True (ICRS): ``w`` rows are drawn (one
+    ``rng.random(w)`` batch) from D's squared row norms, or from the leverage
+    scores of ``u_prev`` when it is a non-empty factor, and the eigensolve
+    runs on Y^T Y of the dedup-scaled row block Y; the left vectors are lifted
+    through D either way.  Returns ``(factor, remaining, g, h)``; an empty
+    candidate set returns ``(None, s, 0, 0)``.
     """
     import torch
 
-    from .device import get_ctx, to_device_colmajor, dptr
-    from .engine import MODE_WEIGHTS
+    from .device import ColMat, dptr, get_ctx, to_device_colmajor
+    from .engine import MODE_ROWS, MODE_WEIGHTS
     from .matcore import TruncatedFactor
 
     s = np.asarray(s, dtype=np.int64)
     if s.size == 0:
         return None, s, 0, 0
-    if rows:
-        raise NotImplementedError("row sampling (rows=True) is not on the B200 path yet")
     a, m, n = _validate_shape(a)
+    if rows and int(w) < 1:
+        raise ParameterError("sample count must be >= 1")
     ctx = get_ctx()
     A = to_device_colmajor(a, ctx.device)
     dev = ctx.device
@@ -219,19 +218,43 @@ def get_update(a, s, u_prev, dist, c, w, rows, rng, r):
     idx = torch.as_tensor(picked.astype(np.int32), device=dev)
     remaining = np.setdiff1d(s, picked, assume_unique=True)
     G = torch.empty(g * g, dtype=torch.float64, device=dev)
-    ctx.tn(g, g, 1.0, A, A, dptr(G), g, xcols=idx, ycols=idx)
+    h = 0
+    if not rows:
+        ctx.tn(g, g, 1.0, A, A, dptr(G), g, xcols=idx, ycols=idx)
+    else:
+        q = torch.empty(m, dtype=torch.float64, device=dev)
+        if u_prev is None or u_prev.is_empty:
+            ctx.rownorms2(A, g, q, cols=idx)                    # row_norm_distribution(d)
+        else:
+            up = np.asarray(u_prev.u, dtype=np.float64)
+            if up.ndim != 2 or up.shape[0] != m:
+                raise ParameterError("u_prev must have the same row count as a")
+            U = to_device_colmajor(np.asfortranarray(up), dev)
+            ctx.rownorms2(U, up.shape[1], q, div=float(up.shape[1]))  # leverage_distribution
+        if not bool((q.sum() > 0).item()):
+            raise DegenerateDistributionError("all row weights are zero")
+        wu = torch.as_tensor(np.asarray(rng.random(int(w)), dtype=np.float64), device=dev)
+        h_cap = min(int(w), m)
+        ridx = torch.empty(h_cap, dtype=torch.int32, device=dev)
+        rcnt = torch.empty(h_cap, dtype=torch.int64, device=dev)
+        rp = torch.empty(h_cap, dtype=torch.float64, device=dev)
+        ctx.draw(MODE_ROWS, q, None, m, wu, int(w), ridx, rcnt, p_out=rp)
+        h, _, rstatus = ctx.read_info(3)
+        if rstatus == 2:
+            raise DegenerateDistributionError("all row weights are zero")
+        Y = ColMat.zeros(h, g, dev)
+        ctx.gather_scale_rows(A, idx, g, ridx, rcnt, rp, int(w), h, ctx.info[0:1], Y)
+        ctx.tn(g, g, 1.0, Y, Y, dptr(G), g)                     # gram_spectrum(y)
     sig = torch.empty(g, dtype=torch.float64, device=dev)
     T = torch.empty(g * int(r), dtype=torch.float64, device=dev)
     ctx.gram_eigh(dptr(G), g, g, int(r), sig, dptr(T), g)
     _, keep, _ = ctx.read_info(3)
     if keep == 0:
-        return TruncatedFactor.empty(m), remaining, g, 0
-    from .device import ColMat
-
+        return TruncatedFactor.empty(m), remaining, g, h
     U = ColMat.zeros(m, keep, dev)
     ctx.nn(g, keep, 1.0, A, dptr(T), g, U, xcols=idx)
     ctx.fix_signs(U, keep)
-    return TruncatedFactor(U.to_numpy(), sig[:keep].cpu().numpy()), remaining, g, 0
+    return TruncatedFactor(U.to_numpy(), sig[:keep].cpu().numpy()), remaining, g, h
 
 
 def convergence_cosines(prev, next_, k, criterion):

@@ -51,6 +51,7 @@ def run_case(a, cfg, keep=None, rng=None):
         "n_rounds": np.int64(len(traces)),
         "remaining": np.array([t.remaining for t in traces], dtype=np.int64),
         "columns_sampled": np.array([t.columns_sampled for t in traces], dtype=np.int64),
+        "rows_sampled": np.array([t.rows_sampled for t in traces], dtype=np.int64),
         "cosines": np.array([np.pad(t.cosines, (0, cfg.k - t.cosines.size))
                              for t in traces]),
     }
@@ -99,10 +100,23 @@ def main():
     cases["cfg2proxy_l2n"] = (a2, podsketch.IsmaConfig(
         k=20, r=60, c=100, tau=1 - 1e-8, strategy="l2n", seed=7), None)
 
+    # ICRS row sampling (rows=True): reference-test-shaped rank-3 cases for
+    # every row strategy, and config-1 runs with explicit row budgets
+    for strat in ("unf", "ort", "ls"):
+        cases[f"rank3_{strat}_rows"] = (
+            make_low_rank(100, 60, 3, np.random.default_rng(7)),
+            podsketch.IsmaConfig(k=3, strategy=strat, rows=True, tau=0.99, seed=11), None)
+    cases["cfg1_ls_rows"] = (a1, podsketch.IsmaConfig(
+        k=10, r=30, c=50, w=400, tau=0.999, strategy="ls", rows=True, seed=5), None)
+    cases["cfg1_unf_rows_subspace"] = (a1, podsketch.IsmaConfig(
+        k=10, r=30, c=50, w=300, tau=0.99, strategy="unf", rows=True, criterion="subspace",
+        seed=4), None)
+
     for name, (a, cfg, keep) in cases.items():
         out = run_case(a, cfg, keep=keep)
         meta = np.array([cfg.k, cfg.r, cfg.column_budget(), int(cfg.finalize),
-                         -1 if keep is None else keep], dtype=np.int64)
+                         -1 if keep is None else keep,
+                         cfg.row_budget() if cfg.rows else 0], dtype=np.int64)
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), meta=meta,
                             tau=np.float64(cfg.tau), strategy=cfg.strategy,
                             criterion=cfg.criterion, seed=np.int64(cfg.seed), **out)

@@ -46,22 +46,24 @@ def _matrix(name):
 
 GOLDEN_CASES = ["cfg1_l2n_modes", "cfg1_unf_subspace", "cfg1_l2n_nofinal_keep11",
                 "rank3_unf", "rank3_l2n", "exhaustive_40x18", "cfg2proxy_l2n", "cfg1_ort_modes",
-                "rank3_ort_fallback"]
+                "rank3_ort_fallback", "rank3_unf_rows", "rank3_ort_rows", "rank3_ls_rows",
+                "cfg1_ls_rows", "cfg1_unf_rows_subspace"]
 
 
 @pytest.mark.parametrize("name", GOLDEN_CASES)
 def test_isma_run_matches_reference_golden(name):
     g = load_golden(name)
-    k, r, c, fin, keep = (int(x) for x in g["meta"])
+    k, r, c, fin, keep, w = (int(x) for x in g["meta"])
     cfg = pod.IsmaConfig(k=k, r=r, c=c, tau=float(g["tau"]), strategy=str(g["strategy"]),
                          criterion=str(g["criterion"]), seed=int(g["seed"]),
-                         finalize=bool(fin))
+                         finalize=bool(fin), rows=w > 0, w=w or None)
     a = _matrix(name)
     factor, traces = pod.isma_run(a, cfg, keep=None if keep < 0 else keep)
     # rounds, index-set bookkeeping: exact
     assert len(traces) == int(g["n_rounds"])
     np.testing.assert_array_equal([t.remaining for t in traces], g["remaining"])
     np.testing.assert_array_equal([t.columns_sampled for t in traces], g["columns_sampled"])
+    np.testing.assert_array_equal([t.rows_sampled for t in traces], g["rows_sampled"])
     # singular values and modes within the fp64 tolerance
     assert factor.nmodes == g["sigma"].size
     assert sigma_relerr(factor.sigma, g["sigma"]) <= SIGMA_RTOL

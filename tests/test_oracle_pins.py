@@ -28,24 +28,32 @@ def _case_matrix(name):
 
 CASES = ["cfg1_l2n_modes", "cfg1_unf_subspace", "cfg1_l2n_nofinal_keep11",
          "rank3_unf", "rank3_l2n", "exhaustive_40x18", "cfg2proxy_l2n", "cfg1_ort_modes",
-         "rank3_ort_fallback"]
+         "rank3_ort_fallback", "rank3_unf_rows", "rank3_ort_rows", "rank3_ls_rows",
+         "cfg1_ls_rows", "cfg1_unf_rows_subspace"]
 
 
 @pytest.mark.parametrize("name", CASES)
 def test_oracle_matches_reference_golden(name):
     g = load_golden(name)
-    k, r, c, fin, keep = (int(x) for x in g["meta"])
+    k, r, c, fin, keep, w = (int(x) for x in g["meta"])
     a = _case_matrix(name)
     out = orc.run(a, k, r=r, c=c, tau=float(g["tau"]), strategy=str(g["strategy"]),
                   criterion=str(g["criterion"]), seed=int(g["seed"]),
-                  do_finalize=bool(fin), keep=None if keep < 0 else keep)
+                  do_finalize=bool(fin), keep=None if keep < 0 else keep,
+                  rows=w > 0, w=w or None)
     tr = out["trace"]
     assert len(tr) == int(g["n_rounds"])
-    # per-round index sets and counts bit-exact
+    # per-round index sets and counts bit-exact (ICRS: column draw, row draw)
     off = g["draw_off"]
+    per = 2 if w else 1
     for i, t in enumerate(tr):
-        np.testing.assert_array_equal(t["unique"], g["draw_idx"][off[i]:off[i + 1]])
-        np.testing.assert_array_equal(t["counts"], g["draw_cnt"][off[i]:off[i + 1]])
+        j = per * i
+        np.testing.assert_array_equal(t["unique"], g["draw_idx"][off[j]:off[j + 1]])
+        np.testing.assert_array_equal(t["counts"], g["draw_cnt"][off[j]:off[j + 1]])
+        if w:
+            np.testing.assert_array_equal(t["rows"], g["draw_idx"][off[j + 1]:off[j + 2]])
+            np.testing.assert_array_equal(t["row_counts"], g["draw_cnt"][off[j + 1]:off[j + 2]])
+            assert t["rows"].size == g["rows_sampled"][i]
         assert t["remaining"] == g["remaining"][i]
     # same arithmetic in the same order: bit-identical on this machine
     np.testing.assert_array_equal(out["sigma"], g["sigma"])
