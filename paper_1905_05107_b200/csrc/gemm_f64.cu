@@ -21,6 +21,83 @@
 
 namespace pod {
 
+// NN epilogue helpers: a warp's 4 x FN fragments of 8 x 8 outputs at rows
+// row0 + f*8 + lane/4, columns col0 + g*8 + 2*(lane%4) + e.  The beta * Z
+// operand is loaded into registers first (all loads in flight together, or
+// prefetched under the last k-chunk's DMMAs), then combined and stored.
+template <int FN>
+__device__ __forceinline__ void nn_load_z(double (&zv)[4][FN][2], int64_t row0, int col0,
+                                          int lane, int64_t m, int q, const double* Z,
+                                          int64_t ldz) {
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t i = row0 + f * 8 + (lane >> 2);
+#pragma unroll
+    for (int g = 0; g < FN; ++g)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = col0 + g * 8 + 2 * (lane & 3) + e;
+        zv[f][g][e] = (i < m && j < q) ? Z[i + (int64_t)j * ldz] : 0.0;
+      }
+  }
+}
+
+template <int FN>
+__device__ __forceinline__ void nn_store(const double (&acc)[4][FN][2],
+                                         const double (&zv)[4][FN][2], int64_t row0, int col0,
+                                         int lane, int64_t m, int q, double alpha, double beta,
+                                         double* Y, int64_t ldy) {
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t i = row0 + f * 8 + (lane >> 2);
+#pragma unroll
+    for (int g = 0; g < FN; ++g)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = col0 + g * 8 + 2 * (lane & 3) + e;
+        if (i < m && j < q) {
+          double v = alpha * acc[f][g][e];
+          if (beta != 0.0) v += beta * zv[f][g][e];
+          Y[i + (int64_t)j * ldy] = v;
+        }
+      }
+  }
+}
+
+// Same, without a full register copy of Z: each of the 4 row fragments loads
+// its FN x 2 Z values together, then stores (4 load latencies per epilogue).
+template <int FN>
+__device__ __forceinline__ void nn_epilogue(const double (&acc)[4][FN][2], int64_t row0, int col0,
+                                            int lane, int64_t m, int q, double alpha, double beta,
+                                            const double* Z, int64_t ldz, double* Y,
+                                            int64_t ldy) {
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t i = row0 + f * 8 + (lane >> 2);
+    double zr[FN][2];
+    if (beta != 0.0) {
+#pragma unroll
+      for (int g = 0; g < FN; ++g)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int j = col0 + g * 8 + 2 * (lane & 3) + e;
+          zr[g][e] = (i < m && j < q) ? Z[i + (int64_t)j * ldz] : 0.0;
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < FN; ++g)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = col0 + g * 8 + 2 * (lane & 3) + e;
+        if (i < m && j < q) {
+          double v = alpha * acc[f][g][e];
+          if (beta != 0.0) v += beta * zr[g][e];
+          Y[i + (int64_t)j * ldy] = v;
+        }
+      }
+  }
+}
+
 // ---------------------------------------------------------------- TN ------
 namespace tn {
 constexpr int BP = 64, BQ = 64, BK = 32, LDS = BK + 4;  // LDS % 16 == 4: conflict-free frags
@@ -38,11 +115,20 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
     int64_t m, int p, int q, const double* __restrict__ X, int64_t ldx,
     const int32_t* __restrict__ xcols, const double* __restrict__ Y, int64_t ldy,
     const int32_t* __restrict__ ycols, int64_t rows_per_split, double* __restrict__ ws,
-    const int32_t* __restrict__ gate) {
+    const int32_t* __restrict__ gate, int sym) {
   if (gate && *gate == 0) return;
   extern __shared__ __align__(16) double smem[];
   const int tiles_p = (p + BP - 1) / BP;
-  const int tp = blockIdx.x % tiles_p, tq = blockIdx.x / tiles_p;
+  int tp, tq;
+  if (sym) {  // symmetric product (X == Y): upper-triangular tiles tp <= tq only
+    int t = blockIdx.x;
+    tq = 0;
+    while (t > tq) { t -= tq + 1; ++tq; }
+    tp = t;
+  } else {
+    tp = blockIdx.x % tiles_p;
+    tq = blockIdx.x / tiles_p;
+  }
   const int split = blockIdx.y;
   const int64_t r0 = (int64_t)split * rows_per_split;
   const int64_t r1 = min(m, r0 + rows_per_split);
@@ -133,20 +219,20 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
 __global__ void __launch_bounds__(256) reduce_kernel(int nsplit, int p, int q, double alpha,
                                                      const double* __restrict__ ws,
                                                      double* __restrict__ C, int64_t ldc,
-                                                     const int32_t* __restrict__ gate) {
+                                                     const int32_t* __restrict__ gate, int sym) {
   if (gate && *gate == 0) return;
   const int64_t total = (int64_t)p * q;
   const int lane = threadIdx.x & 31;
   const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t t = wg; t < total; t += nw) {
+    const int64_t j = t / p, i = t - j * p;
+    // symmetric: the lower triangle mirrors the upper one (exactly symmetric C)
+    const int64_t src = (sym && i > j) ? (j + i * p) : t;
     double s = 0.0;
-    for (int k = lane; k < nsplit; k += 32) s += ws[(size_t)k * total + t];
+    for (int k = lane; k < nsplit; k += 32) s += ws[(size_t)k * total + src];
     s = warp_sum(s);
-    if (lane == 0) {
-      const int64_t j = t / p, i = t - j * p;
-      C[i + j * ldc] = alpha * s;
-    }
+    if (lane == 0) C[i + j * ldc] = alpha * s;
   }
 }
 
@@ -155,11 +241,12 @@ struct Plan {
   int64_t rows_per_split;
 };
 
-inline Plan plan(int64_t m, int64_t p, int64_t q) {
+inline Plan plan(int64_t m, int64_t p, int64_t q, bool sym) {
   Plan pl;
-  pl.tiles = (int)(ceil_div(p, BP) * ceil_div(q, BQ));
-  const int target = 2 * 148;
-  int64_t want = ceil_div(target, pl.tiles);
+  const int64_t tp = ceil_div(p, BP);
+  pl.tiles = (int)(sym ? tp * (tp + 1) / 2 : tp * ceil_div(q, BQ));
+  const int target = 2 * 148;  // 2 CTAs/SM (110 KB smem each): ONE wave, never a partial second
+  int64_t want = std::max<int64_t>(1, target / pl.tiles);
   int64_t max_by_rows = std::max<int64_t>(1, ceil_div(m, 4 * BK));  // >= 4 k-blocks per CTA
   int64_t splits = std::min<int64_t>(want, max_by_rows);
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, 65535));
@@ -271,22 +358,8 @@ __global__ void __launch_bounds__(THREADS) kernel(
   }
   cp_async_wait<0>();
 
-#pragma unroll
-  for (int f = 0; f < 4; ++f) {
-    const int64_t i = row0 + wm * 32 + f * 8 + (lane >> 2);
-    if (i >= m) continue;
-#pragma unroll
-    for (int g = 0; g < C::FN; ++g)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int j = wn * (BN / C::WN) + g * 8 + 2 * (lane & 3) + e;
-        if (j < q) {
-          double v = alpha * acc[f][g][e];
-          if (beta != 0.0) v += beta * Z[i + (int64_t)j * ldz];
-          Y[i + (int64_t)j * ldy] = v;
-        }
-      }
-  }
+  nn_epilogue<C::FN>(acc, row0 + wm * 32, wn * (BN / C::WN), lane, m, q, alpha, beta, Z, ldz, Y,
+                     ldy);
 }
 }  // namespace nn
 
@@ -403,29 +476,188 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
     }
     __syncthreads();  // xs fully consumed before the next prefetch overwrites it
     const int64_t row0 = rb * BM + wm * 32;
-#pragma unroll
-    for (int f = 0; f < 4; ++f) {
-      const int64_t i = row0 + f * 8 + (lane >> 2);
-      if (i >= m) continue;
-#pragma unroll
-      for (int g = 0; g < C::FN; ++g)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int j = wn * (BN / C::WN) + g * 8 + 2 * (lane & 3) + e;
-          if (j < q) {
-            double v = alpha * acc[f][g][e];
-            if (beta != 0.0) v += beta * Z[i + (int64_t)j * ldz];
-            Y[i + (int64_t)j * ldy] = v;
-          }
-        }
-    }
+    nn_epilogue<C::FN>(acc, row0, wn * (BN / C::WN), lane, m, q, alpha, beta, Z, ldz, Y, ldy);
     buf ^= 1;
   }
   cp_async_wait<0>();
 }
 }  // namespace nnp
 
+// -------------------------------------------------- NN streamed, persistent ----
+// For p too large to keep T resident: every CTA walks its row blocks and the
+// k-chunks of each block as ONE flattened (block, chunk) sequence behind a
+// STAGES-deep cp.async pipeline, so the next block's X and T chunks load while
+// the current block finishes and writes its epilogue (no per-block pipeline
+// fill/drain).  T chunks are re-read per block from L2; X rows come from HBM
+// once.  A CTA reads all chunks of a block before writing that block's rows,
+// so Y may alias X or Z.
+namespace nns {
+constexpr int THREADS = 256;
+constexpr int BK = 16;
+constexpr int LDT = BK + 4;  // T chunk stored [j][k]
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = (BN == 128) ? 3 : 4;
+  static constexpr int BM = (BN == 64) ? 128 : 64;  // rows per block (T reuse)
+  static constexpr int LDX = BM + 4;                // X chunk stored [k][row]
+  static constexpr int WM = BM / 32;  // warps along M
+  static constexpr int WN = 8 / WM;   // 4 warps along N
+  static constexpr int FN = BN / WN / 8;
+  static constexpr int XT = BK * LDX, TT = BN * LDT;
+  static constexpr size_t SMEM = size_t(STAGES) * (XT + TT) * sizeof(double);
+  static constexpr int PER_SM = (BN == 192) ? 1 : 2;
+};
+// blockIdx.y selects a group of BN output columns (q0 = blockIdx.y * BN); more
+// than one group only when Y aliases neither X nor Z (a group writes its
+// columns of a row block while another group may still be reading X there).
+
+template <int BN>
+__global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, double alpha,
+                                                  const double* X, int64_t ldx,
+                                                  const int32_t* __restrict__ xcols,
+                                                  const double* __restrict__ T, int64_t ldT,
+                                                  double beta, const double* Z, int64_t ldz,
+                                                  double* Y, int64_t ldy,
+                                                  const int32_t* __restrict__ gate, int vx, int vt) {
+  using C = Cfg<BN>;
+  constexpr int ST = C::STAGES;
+  if (gate && *gate == 0) return;
+  extern __shared__ __align__(16) double smem[];
+  {
+    const int q0 = blockIdx.y * BN;
+    T += (int64_t)q0 * ldT;
+    Y += (int64_t)q0 * ldy;
+    if (Z) Z += (int64_t)q0 * ldz;
+    q = min(BN, q - q0);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nkb = (p + BK - 1) / BK;
+  const int64_t nblk = (m + C::BM - 1) / C::BM;
+  const int64_t G = gridDim.x;
+  if ((int64_t)blockIdx.x >= nblk) return;
+  const int64_t nmine = (nblk - blockIdx.x + G - 1) / G;
+  const int64_t total = nmine * nkb;
+
+  // (block, chunk) of the next load, advanced incrementally: no 64-bit
+  // division in the loop (its DMUL-based emulation shares the FP64 pipe)
+  int64_t l_r0 = (int64_t)blockIdx.x * C::BM;
+  int l_kb = 0;
+  auto load_stage = [&](int st) {
+    double* xs = smem + (size_t)st * (C::XT + C::TT);
+    double* ts = xs + C::XT;
+    const int k0 = l_kb * BK;
+    const int64_t r0 = l_r0;
+    if (++l_kb == nkb) {
+      l_kb = 0;
+      l_r0 += G * C::BM;
+    }
+    // X: C::BM rows x BK cols as row pairs (2 x 8 B)
+    for (int e = threadIdx.x; e < BK * (C::BM / 2); e += THREADS) {
+      const int cl = e / (C::BM / 2), i2 = (e - cl * (C::BM / 2)) * 2;
+      const int c = k0 + cl;
+      const int64_t row = r0 + i2;
+      int64_t col = c;
+      bool cv = c < p;
+      if (cv && xcols) {
+        col = xcols[c];
+        cv = col >= 0;  // index -1: zero column
+      }
+      double* dst = xs + cl * C::LDX + i2;
+      const double* src = X + col * ldx + row;
+      if (cv && vx && row + 1 < m) {
+        cp_async16(dst, src, true);
+      } else {
+        cp_async8(dst, cv && row < m ? src : X, cv && row < m);
+        cp_async8(dst + 1, cv && row + 1 < m ? src + 1 : X, cv && row + 1 < m);
+      }
+    }
+    // T: rows k0..k0+BK, all BN cols, k pairs
+    for (int e = threadIdx.x; e < BN * (BK / 2); e += THREADS) {
+      const int j = e / (BK / 2), k2 = (e - j * (BK / 2)) * 2;
+      const int k = k0 + k2;
+      const bool jv = j < q;
+      double* dst = ts + j * LDT + k2;
+      const double* src = T + k + (int64_t)j * ldT;
+      if (jv && vt && k + 1 < p) {
+        cp_async16(dst, src, true);
+      } else {
+        cp_async8(dst, jv && k < p ? src : T, jv && k < p);
+        cp_async8(dst + 1, jv && k + 1 < p ? src + 1 : T, jv && k + 1 < p);
+      }
+    }
+  };
+
+  const int wm = warp % C::WM, wn = warp / C::WM;
+  double acc[4][C::FN][2];
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) {
+    if (s < total) load_stage(s);
+    cp_async_commit();
+  }
+  int kb = 0, st_c = 0, st_l = ST - 1;
+  int64_t c_r0 = (int64_t)blockIdx.x * C::BM;
+  for (int64_t it = 0; it < total; ++it) {
+    if (it + ST - 1 < total) load_stage(st_l);
+    if (++st_l == ST) st_l = 0;
+    cp_async_commit();
+    cp_async_wait<ST - 1>();
+    __syncthreads();
+    if (kb == 0) {
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int g = 0; g < C::FN; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+    }
+    const double* xs = smem + (size_t)st_c * (C::XT + C::TT);
+    const double* ts = xs + C::XT;
+    if (++st_c == ST) st_c = 0;
+
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double a[4], b[C::FN];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+        a[f] = xs[(kk * 4 + (lane & 3)) * C::LDX + wm * 32 + f * 8 + (lane >> 2)];
+#pragma unroll
+      for (int g = 0; g < C::FN; ++g)
+        b[g] = ts[(wn * (BN / C::WN) + g * 8 + (lane >> 2)) * LDT + kk * 4 + (lane & 3)];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int g = 0; g < C::FN; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
+    }
+    __syncthreads();  // this stage is refilled by the next iteration's prefetch
+    if (++kb == nkb) {
+      kb = 0;
+      const int64_t row0 = c_r0 + wm * 32;
+      c_r0 += G * C::BM;
+      nn_epilogue<C::FN>(acc, row0, wn * (BN / C::WN), lane, m, q, alpha, beta, Z, ldz, Y, ldy);
+    }
+  }
+  cp_async_wait<0>();
+}
+}  // namespace nns
+
 static bool g_attr_done = false;
+// POD_NN_GROUPS=0 disables column groups in the streamed NN kernel (A/B)
+static bool nn_groups_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_NN_GROUPS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+// POD_NN_LEGACY=1 selects the per-block streaming kernel (A/B measurements)
+static bool nn_streamed_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_NN_LEGACY");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
 static int ensure_attrs() {
   if (g_attr_done) return POD_OK;
   cudaError_t e = cudaFuncSetAttribute(tn::partial_kernel,
@@ -446,6 +678,15 @@ static int ensure_attrs() {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return cuda_status(e, "nnp attr");
   }
+  e = cudaFuncSetAttribute(nns::kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)nns::Cfg<64>::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "nns attr");
+  e = cudaFuncSetAttribute(nns::kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)nns::Cfg<128>::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "nns attr");
+  e = cudaFuncSetAttribute(nns::kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)nns::Cfg<192>::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "nns attr");
   g_attr_done = true;
   return POD_OK;
 }
@@ -456,8 +697,8 @@ using namespace pod;
 
 extern "C" size_t pod_gemm_tn_ws_bytes(int64_t m, int64_t p, int64_t q) {
   if (m <= 0 || p <= 0 || q <= 0) return 0;
-  tn::Plan pl = tn::plan(m, p, q);
-  return (size_t)pl.splits * p * q * sizeof(double);
+  const tn::Plan a = tn::plan(m, p, q, false), b = tn::plan(m, p, q, p == q);
+  return (size_t)std::max(a.splits, b.splits) * p * q * sizeof(double);
 }
 
 extern "C" int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
@@ -471,19 +712,20 @@ extern "C" int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
   POD_REQUIRE(m > 0, "pod_gemm_tn_f64: m must be >= 1");
   int st = ensure_attrs();
   if (st) return st;
-  tn::Plan pl = tn::plan(m, p, q);
+  const int sym = (X == Y && ldx == ldy && xcols == ycols && p == q) ? 1 : 0;
+  tn::Plan pl = tn::plan(m, p, q, sym != 0);
   POD_REQUIRE(ws_bytes >= (size_t)pl.splits * p * q * sizeof(double),
               "pod_gemm_tn_f64: workspace too small (%zu < %zu)", ws_bytes,
               (size_t)pl.splits * p * q * sizeof(double));
   dim3 grid(pl.tiles, pl.splits);
   tn::partial_kernel<<<grid, tn::THREADS, tn::SMEM, s>>>(m, (int)p, (int)q, X, ldx, xcols, Y, ldy,
                                                          ycols, pl.rows_per_split, (double*)ws,
-                                                         gate);
+                                                         gate, sym);
   POD_CHECK_LAUNCH("tn partial");
   int64_t tot = p * q;
   int blocks = (int)std::min<int64_t>(ceil_div(tot, 8), 16 * 148);  // 8 warps = 8 outputs per block
   tn::reduce_kernel<<<blocks, 256, 0, s>>>(pl.splits, (int)p, (int)q, alpha, (const double*)ws, C,
-                                           ldc, gate);
+                                           ldc, gate, sym);
   POD_CHECK_LAUNCH("tn reduce");
   return POD_OK;
 }
@@ -520,6 +762,41 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
       POD_CHECK_LAUNCH("nn persistent");
       return POD_OK;
     }
+  }
+  if (nn_streamed_enabled()) {
+    const int vx = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && (ldx % 2 == 0);
+    const int vt = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ldt % 2 == 0);
+    
+    // Y aliasing X or Z (in-place Q <- Q R^-1): one column group only
+    auto overlaps = [&](const double* a, int64_t lda, int64_t ncols) {
+      if (!a) return false;
+      const char* a0 = (const char*)a;
+      const char* a1 = (const char*)(a + (ncols - 1) * lda + m);
+      const char* y0 = (const char*)Y;
+      const char* y1 = (const char*)(Y + (q - 1) * ldy + m);
+      return a0 < y1 && y0 < a1;
+    };
+    const bool alias = overlaps(X, ldx, p) || (beta != 0.0 && overlaps(Z, ldz, q));
+    if (q <= 64 || (!alias && nn_groups_enabled())) {
+      const int64_t nblk = ceil_div(m, nns::Cfg<64>::BM);
+      const unsigned gy = (unsigned)ceil_div(q, 64);
+      const int64_t per = std::max<int64_t>(1, nns::Cfg<64>::PER_SM * 148 / gy);
+      const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
+      nns::kernel<64><<<grid, nns::THREADS, nns::Cfg<64>::SMEM, s>>>(
+          m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+    } else if (q <= 128) {
+      const int64_t nblk = ceil_div(m, nns::Cfg<128>::BM);
+      const unsigned grid = (unsigned)std::min<int64_t>(nblk, nns::Cfg<128>::PER_SM * 148);
+      nns::kernel<128><<<grid, nns::THREADS, nns::Cfg<128>::SMEM, s>>>(
+          m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+    } else {
+      const int64_t nblk = ceil_div(m, nns::Cfg<192>::BM);
+      const unsigned grid = (unsigned)std::min<int64_t>(nblk, nns::Cfg<192>::PER_SM * 148);
+      nns::kernel<192><<<grid, nns::THREADS, nns::Cfg<192>::SMEM, s>>>(
+          m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+    }
+    POD_CHECK_LAUNCH("nn streamed");
+    return POD_OK;
   }
   if (q <= 64) {
     dim3 grid((unsigned)ceil_div(m, nn::Cfg<64>::BM));

@@ -14,6 +14,14 @@ Noise "N(0, x)" is read as variance x.
   cos/sin basis, so it is a GEMM on the device; ``side`` shrinks the grid
   for proxies.
 
+* ``config3`` -- power-law low-rank-plus-noise: A = U diag(i^-1.5) V^T +
+  N(0, 1e-6), rank 200, m=1,000,000, n=20,000 (160 GB fp64), generated on
+  the device.  U is Haar: G R^-1 with G ~ N(0,1) per 4096-row chunk and R the
+  Cholesky factor of G^T G summed over all chunks in chunk order (= the R of
+  a positive-diagonal QR), so every row partition yields the same matrix;
+  V = Q of a (replicated) QR of an n x 200 Gaussian.  ``m``/``n`` shrink it
+  for parity proxies.
+
 Data generation is outside every timed region.
 """
 
@@ -25,6 +33,7 @@ import numpy as np
 
 CFG1 = dict(m=2000, n=500, k=10, r=30, c=50, tol=1e-8)
 CFG2 = dict(side=512, n=2000, k=20, r=60, c=100, tol=1e-8)
+CFG3 = dict(m=1_000_000, n=20_000, rank=200, k=50, r=150, c=200, tol=1e-8)
 
 
 def config1(seed=0, m=2000, n=500, noise_var=1e-6):
@@ -98,4 +107,59 @@ def config2_torch(seed=0, side=512, n=2000, noise_var=1e-4, device="cpu", nmodes
 def config2(seed=0, side=512, n=2000, noise_var=1e-4):
     """Host (numpy, F-order) copy of ``config2_torch`` generated on the CPU."""
     at = config2_torch(seed, side, n, noise_var, device="cpu")
+    return np.asfortranarray(at.numpy().T)
+
+
+def _chunk_gen(device, seed, c, salt):
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed((int(seed) * 1000003 + c * 7919 + salt) % (2 ** 62))
+    return g
+
+
+def config3_torch(seed=0, m=1_000_000, n=20_000, rank=200, noise_var=1e-6, device="cpu",
+                  rows=None, chunk=NOISE_CHUNK):
+    """BASELINE config 3 rows [r0, r1) as a column-major float64 torch tensor
+    (storage (n, r1 - r0), like ``config2_torch``); identical for any row
+    partition of the same (seed, m, n, device type)."""
+    import torch
+
+    dt = torch.float64
+    r0, r1 = (0, m) if rows is None else (int(rows[0]), int(rows[1]))
+    nchunk = (m + chunk - 1) // chunk
+    # V: Haar n x rank (replicated on every rank)
+    gv = _chunk_gen(device, seed, 0, 11)
+    v = torch.linalg.qr(torch.randn((n, rank), generator=gv, dtype=dt, device=device))[0]
+    sig = torch.arange(1, rank + 1, dtype=dt, device=device) ** -1.5
+    vs = (v * sig).T.contiguous()  # rank x n: diag(sigma) V^T
+
+    def gauss(c):
+        c0, c1 = c * chunk, min(m, (c + 1) * chunk)
+        return torch.randn((c1 - c0, rank), generator=_chunk_gen(device, seed, c, 5), dtype=dt,
+                           device=device)
+
+    # R of the positive-diagonal QR of G = [G_0; G_1; ...]: Cholesky of sum G_c^T G_c
+    gram = torch.zeros((rank, rank), dtype=dt, device=device)
+    for c in range(nchunk):
+        gc = gauss(c)
+        gram += gc.T @ gc
+    rf = torch.linalg.cholesky(gram, upper=True)
+    sd = math.sqrt(noise_var)
+    at = torch.empty((n, r1 - r0), dtype=dt, device=device)
+    for c in range(r0 // chunk, (r1 + chunk - 1) // chunk):
+        c0, c1 = c * chunk, min(m, (c + 1) * chunk)
+        uc = torch.linalg.solve_triangular(rf, gauss(c), upper=True, left=False)  # G_c R^-1
+        blk = (uc @ vs).T.contiguous()  # n x chunk
+        blk.add_(torch.randn((n, c1 - c0), generator=_chunk_gen(device, seed, c, 3), dtype=dt,
+                             device=device), alpha=sd)
+        lo, hi = max(c0, r0), min(c1, r1)
+        at[:, lo - r0:hi - r0].copy_(blk[:, lo - c0:hi - c0])
+        del blk, uc
+    return at
+
+
+def config3(seed=0, m=20_000, n=2_000, rank=200, noise_var=1e-6):
+    """Host (numpy, F-order) copy of a ``config3_torch`` proxy made on the CPU."""
+    at = config3_torch(seed, m, n, rank, noise_var, device="cpu")
     return np.asfortranarray(at.numpy().T)
