@@ -1,0 +1,951 @@
+// Column-distributed BLOCK one-sided Jacobi on a thread-block cluster (sm_100a).
+//
+// Same problems as cluster_jacobi.cu (the E-SVD of merge.py:80-85, the
+// sampled-Gram eigensolve of baselines.py:43-48, the small SVDs of finalize
+// isma.py:297 / orthonormalize isma.py:251-252), different parallel layout:
+// the n columns are cut into NB = 2 CL blocks of bs columns and every CTA of
+// the cluster OWNS two whole blocks (all rows), so a column pair's dot
+// products, rotation and norm update are local to one CTA -- no per-pair
+// partial-sum exchange.  One sweep:
+//   - intra phase: every CTA rotates the pairs inside each of its two blocks
+//   - NB - 1 steps of the round-robin ("circle") block tournament: a CTA
+//     rotates all bs^2 pairs between its two blocks (bs sub-rounds of bs
+//     disjoint pairs), then the blocks move to their next owners with
+//     cp.async.bulk DSMEM copies completing on the receiver's mbarrier;
+//     one cluster barrier per step.
+// Each unordered column pair is visited exactly once per sweep (as in the
+// cyclic scalar method), in a fixed order, so results are deterministic.
+// The rotation formulas, threshold (gamma^2 > tol^2 a b) and stopping rule (a
+// sweep without rotations) are those of cluster_jacobi.cu.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pod {
+
+namespace bj {
+
+constexpr int MAX_CL = 8;
+
+#ifdef POD_BJ_TIMING
+__device__ unsigned long long g_bj_phase[16];
+#define BJ_TI(i)                                                             \
+  do {                                                                       \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                               \
+      unsigned long long _t = clock64();                                     \
+      if (i) atomicAdd(&g_bj_phase[i], _t - _bi_last);                      \
+      _bi_last = _t;                                                         \
+    }                                                                        \
+  } while (0)
+#define BJ_T(i)                                                              \
+  do {                                                                       \
+    if (threadIdx.x == 0 && cl.block_rank() == 0) {                          \
+      unsigned long long _t = clock64();                                     \
+      if (i) atomicAdd(&g_bj_phase[i], _t - _bj_last);                      \
+      _bj_last = _t;                                                         \
+    }                                                                        \
+  } while (0)
+#else
+#define BJ_T(i) \
+  do {          \
+  } while (0)
+#define BJ_TI(i) \
+  do {           \
+  } while (0)
+#endif
+constexpr size_t SMEM_CAP = 224 * 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t cluster_map(uint32_t saddr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mb, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mb)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;\n"
+               ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
+  const uint32_t a = smem_u32(mb);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  }
+}
+// bulk DSMEM copy of `bytes` (multiple of 16) from this CTA's shared memory
+// to CTA-mapped address dst, completing on the destination's mbarrier
+__device__ __forceinline__ void bulk_to_cluster(uint32_t dst, const void* src, uint32_t bytes,
+                                                uint32_t dst_mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+      "[%3];\n" ::"r"(dst), "r"(smem_u32(src)), "r"(bytes), "r"(dst_mbar)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// fp64 1/sqrt(x) for positive normal x (as cluster_jacobi.cu)
+__device__ __forceinline__ double rsqrt_nr2(double x) {
+  int e;
+  double m = frexp(x, &e);
+  if (e & 1) {
+    m *= 2.0;
+    e -= 1;
+  }
+  double y = (double)rsqrtf((float)m);
+  y = y * fma(-0.5 * m, y * y, 1.5);
+  y = y * fma(-0.5 * m, y * y, 1.5);
+  return ldexp(y, -e / 2);
+}
+
+// 1/sqrt(x): fp32 seed + two Newton steps directly when x is well inside the
+// fp32 range (the common case), else with exact power-of-two scaling
+__device__ __forceinline__ double rsqrt_d(double x) {
+  if (x > 1e-30 && x < 1e30) {
+    double y = (double)rsqrtf((float)x);
+    y = y * fma(-0.5 * x, y * y, 1.5);
+    y = y * fma(-0.5 * x, y * y, 1.5);
+    return y;
+  }
+  return rsqrt_nr2(x);
+}
+
+// Jacobi rotation (c, s) annihilating gamma between columns with squared
+// norms al, be (|theta| <= pi/4; formulas of cluster_jacobi.cu)
+__device__ __forceinline__ void rot_params(double g, double al, double be, double& c_,
+                                           double& s_) {
+  const double d = be - al;
+  const double h2 = fma(d, d, 4.0 * g * g);
+  double rh, ic;
+  if (h2 > 1e-30 && h2 < 1e30) {
+    // both fp32 seeds first (short MUFU chain), then the fp64 Newton steps;
+    // ic's seed comes from the fp32 x, which Newton corrects to the fp64 x
+    const float rhf = rsqrtf((float)h2);
+    const float xf = 0.5f * fmaf(fabsf((float)d), rhf, 1.0f);
+    const float icf = rsqrtf(xf);
+    rh = (double)rhf;
+    rh = rh * fma(-0.5 * h2, rh * rh, 1.5);
+    rh = rh * fma(-0.5 * h2, rh * rh, 1.5);
+    ic = (double)icf;
+  } else {
+    rh = rsqrt_nr2(h2);
+    ic = -1.0;
+  }
+  const double x = 0.5 * fma(fabs(d), rh, 1.0);  // in [0.5, 1]
+  if (ic < 0.0) ic = (double)rsqrtf((float)x);
+  ic = ic * fma(-0.5 * x, ic * ic, 1.5);
+  ic = ic * fma(-0.5 * x, ic * ic, 1.5);
+  c_ = x * ic;
+  s_ = copysign(fabs(g) * rh * ic, d * g);
+}
+
+// A slot holds one column block: W (bs x ld), J (bs x ldj, optional), the
+// block's current squared norms and its global column ids (as doubles), all
+// contiguous so one bulk copy moves it.
+struct Geo {
+  int n, nrows, njrows, bs, ld, ldj, bse;
+  int slot;  // doubles per slot (even)
+  __host__ __device__ Geo(int n_, int nrows_, int njrows_, int cl) {
+    n = n_;
+    nrows = nrows_;
+    njrows = njrows_;
+    bs = (n + 2 * cl - 1) / (2 * cl);
+    ld = (nrows + 1) & ~1;
+    ldj = (njrows + 1) & ~1;
+    bse = (bs + 1) & ~1;
+    slot = bs * ld + bs * ldj + 2 * bse;
+  }
+  __host__ __device__ size_t smem_bytes(int cl) const {
+    // 2 mbarriers + flags [2][CL] (as doubles) + gathered norms [2 cl bs] + 4 slots
+    return (size_t)(2 + 2 * cl + 2 * cl * bs + 4 * (size_t)slot) * sizeof(double);
+  }
+};
+
+struct Slot {
+  double* w;
+  double* j;
+  double* nrm;
+  double* id;
+};
+__device__ __forceinline__ Slot slot_at(double* slots, const Geo& g, int set, int t) {
+  Slot s;
+  double* b = slots + (size_t)(set * 2 + t) * g.slot;
+  s.w = b;
+  s.j = b + (size_t)g.bs * g.ld;
+  s.nrm = s.j + (size_t)g.bs * g.ldj;
+  s.id = s.nrm + g.bse;
+  return s;
+}
+
+// Rotate column pairs (pa[k], pb[k]) k < P of the given slots (columns are
+// pointers into smem) -- one thread group of tpp lanes per pair.
+struct PairRef {
+  double* x;
+  double* y;
+  double* jx;
+  double* jy;
+  double* nx;
+  double* ny;
+};
+
+template <int RPL>
+__device__ __forceinline__ bool rotate_pair(const PairRef& pr, bool live, int gl, int tpp,
+                                            int nrows, int njrows, double tol2) {
+  double g = 0.0;
+  double xa[RPL > 0 ? RPL : 1], xb[RPL > 0 ? RPL : 1];
+  if (RPL > 0) {
+#pragma unroll
+    for (int k = 0; k < (RPL > 0 ? RPL : 1); ++k) {
+      const int i = gl + k * tpp;
+      const bool ok = live && i < nrows;
+      xa[k] = ok ? pr.x[i] : 0.0;
+      xb[k] = ok ? pr.y[i] : 0.0;
+      g = fma(xa[k], xb[k], g);
+    }
+  } else if (live) {
+    for (int i = gl; i < nrows; i += tpp) g = fma(pr.x[i], pr.y[i], g);
+  }
+  // norms are read before the (synchronising) shuffles; lane 0 rewrites them
+  // only after its group has passed the shuffles
+  const double al = live ? *pr.nx : 0.0, be = live ? *pr.ny : 0.0;
+  for (int o = tpp / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o, tpp);
+  if (!live) return false;
+  if (!(g * g > tol2 * al * be && al > 0.0 && be > 0.0)) return false;
+  double c_, s_;
+  rot_params(g, al, be, c_, s_);
+  if (RPL > 0) {
+#pragma unroll
+    for (int k = 0; k < (RPL > 0 ? RPL : 1); ++k) {
+      const int i = gl + k * tpp;
+      if (i < nrows) {
+        pr.x[i] = fma(c_, xa[k], -s_ * xb[k]);
+        pr.y[i] = fma(s_, xa[k], c_ * xb[k]);
+      }
+    }
+  } else {
+    for (int i = gl; i < nrows; i += tpp) {
+      const double x0 = pr.x[i], y0 = pr.y[i];
+      pr.x[i] = fma(c_, x0, -s_ * y0);
+      pr.y[i] = fma(s_, x0, c_ * y0);
+    }
+  }
+  if (pr.jx) {
+    for (int i = gl; i < njrows; i += tpp) {
+      const double x0 = pr.jx[i], y0 = pr.jy[i];
+      pr.jx[i] = fma(c_, x0, -s_ * y0);
+      pr.jy[i] = fma(s_, x0, c_ * y0);
+    }
+  }
+  if (gl == 0) {
+    const double c2 = c_ * c_, s2 = s_ * s_, csg = 2.0 * c_ * s_ * g;
+    *pr.nx = fmax(fma(c2, al, fma(s2, be, -csg)), 0.0);
+    *pr.ny = fma(s2, al, fma(c2, be, csg));
+  }
+  return true;
+}
+
+__device__ __forceinline__ int pow2_floor(int v) {
+  int p = 1;
+  while (p * 2 <= v) p *= 2;
+  return p;
+}
+
+// One sub-round: P disjoint pairs in parallel; pairs produced by `pick(k,
+// &x_slot, &x_col, &y_slot, &y_col)`; returns whether this thread's pair rotated.
+template <int RPL, typename Pick>
+__device__ bool sub_round(const Slot& c0, const Slot& c1, const Geo& g, int P, double tol2,
+                          Pick pick) {
+  const int tpp = min(32, pow2_floor(max(1, (int)blockDim.x / max(P, 1))));
+  const int grp = threadIdx.x / tpp, gl = threadIdx.x % tpp;
+  const int ngrp = blockDim.x / tpp;
+  bool rot = false;
+  // groups beyond P still take part in the shuffles (full-warp masks)
+  for (int k0 = 0; k0 < P; k0 += ngrp) {
+    const int k = k0 + grp;
+    int xs = 0, xc = 0, ys = 0, yc = 0;
+    bool live = false;
+    if (k < P) live = pick(k, xs, xc, ys, yc);
+    const Slot& sx = xs ? c1 : c0;
+    const Slot& sy = ys ? c1 : c0;
+    PairRef pr;
+    pr.x = sx.w + (size_t)xc * g.ld;
+    pr.y = sy.w + (size_t)yc * g.ld;
+    pr.jx = g.ldj ? sx.j + (size_t)xc * g.ldj : nullptr;
+    pr.jy = g.ldj ? sy.j + (size_t)yc * g.ldj : nullptr;
+    pr.nx = sx.nrm + xc;
+    pr.ny = sy.nrm + yc;
+    rot |= rotate_pair<RPL>(pr, live, gl, tpp, g.nrows, g.njrows, tol2);
+  }
+  __syncthreads();
+  return rot;
+}
+
+// One tournament step's inter-block pairs: group k keeps top column k (rows
+// in registers when RPL > 0, norm in a register) and meets bottom columns
+// k, k+1, ... (mod bs) in bs sub-rounds.
+template <int RPL>
+__device__ bool inter_step(const Slot& c0, const Slot& c1, const Geo& g, double tol2) {
+  const int bs = g.bs;
+  const int tpp = min(32, pow2_floor(max(1, (int)blockDim.x / bs)));
+  const int grp = threadIdx.x / tpp, gl = threadIdx.x % tpp;
+  const bool has = grp < bs;
+  uint32_t m1 = 0;
+  for (int c = 0; c < bs; ++c) m1 |= ((int)c1.id[c] < g.n ? 1u : 0u) << c;
+  const int xc = has ? grp : 0;
+  const bool xlive = has && (int)c0.id[xc] < g.n;
+  double* xw = c0.w + (size_t)xc * g.ld;
+  double* xj = g.ldj ? c0.j + (size_t)xc * g.ldj : nullptr;
+  double xa[RPL > 0 ? RPL : 1];
+  if (RPL > 0) {
+#pragma unroll
+    for (int k = 0; k < (RPL > 0 ? RPL : 1); ++k) {
+      const int i = gl + k * tpp;
+      xa[k] = (xlive && i < g.nrows) ? xw[i] : 0.0;
+    }
+  }
+  double al = xlive ? c0.nrm[xc] : 0.0;
+  bool rot = false;
+#ifdef POD_BJ_TIMING
+  unsigned long long _bi_last = clock64();
+#endif
+  for (int t = 0; t < bs; ++t) {
+    BJ_TI(0);
+    int yc = xc + t;
+    if (yc >= bs) yc -= bs;
+    const bool live = xlive && ((m1 >> yc) & 1u);
+    double* yw = c1.w + (size_t)yc * g.ld;
+    double gam = 0.0;
+    double yb[RPL > 0 ? RPL : 1];
+    if (RPL > 0) {
+      double g2 = 0.0;  // two independent FMA chains
+#pragma unroll
+      for (int k = 0; k < (RPL > 0 ? RPL : 1); ++k) {
+        const int i = gl + k * tpp;
+        yb[k] = (live && i < g.nrows) ? yw[i] : 0.0;
+        if (k & 1) g2 = fma(xa[k], yb[k], g2);
+        else gam = fma(xa[k], yb[k], gam);
+      }
+      gam += g2;
+    } else if (live) {
+      for (int i = gl; i < g.nrows; i += tpp) gam = fma(xw[i], yw[i], gam);
+    }
+    const double be = live ? c1.nrm[yc] : 0.0;  // read before the shuffles
+    BJ_TI(8);
+    for (int o = tpp / 2; o > 0; o >>= 1) gam += __shfl_xor_sync(0xffffffffu, gam, o, tpp);
+    BJ_TI(9);
+    if (live && gam * gam > tol2 * al * be && al > 0.0 && be > 0.0) {
+      double c_, s_;
+      rot_params(gam, al, be, c_, s_);
+      if (RPL > 0) {
+#pragma unroll
+        for (int k = 0; k < (RPL > 0 ? RPL : 1); ++k) {
+          const int i = gl + k * tpp;
+          const double x0 = xa[k], y0 = yb[k];
+          xa[k] = fma(c_, x0, -s_ * y0);
+          if (i < g.nrows) yw[i] = fma(s_, x0, c_ * y0);
+        }
+      } else {
+        for (int i = gl; i < g.nrows; i += tpp) {
+          const double x0 = xw[i], y0 = yw[i];
+          xw[i] = fma(c_, x0, -s_ * y0);
+          yw[i] = fma(s_, x0, c_ * y0);
+        }
+      }
+      if (xj) {
+        double* yj = c1.j + (size_t)yc * g.ldj;
+        for (int i = gl; i < g.njrows; i += tpp) {
+          const double x0 = xj[i], y0 = yj[i];
+          xj[i] = fma(c_, x0, -s_ * y0);
+          yj[i] = fma(s_, x0, c_ * y0);
+        }
+      }
+      const double c2 = c_ * c_, s2 = s_ * s_, csg = 2.0 * c_ * s_ * gam;
+      const double nal = fmax(fma(c2, al, fma(s2, be, -csg)), 0.0);
+      if (gl == 0) c1.nrm[yc] = fma(s2, al, fma(c2, be, csg));
+      al = nal;
+      rot = true;
+    }
+    BJ_TI(10);
+    __syncthreads();
+    BJ_TI(11);
+  }
+  if (xlive) {
+    if (RPL > 0) {
+#pragma unroll
+      for (int k = 0; k < (RPL > 0 ? RPL : 1); ++k) {
+        const int i = gl + k * tpp;
+        if (i < g.nrows) xw[i] = xa[k];
+      }
+    }
+    if (gl == 0) c0.nrm[xc] = al;
+  }
+  __syncthreads();
+  return rot;
+}
+
+// column ids: id < n real, otherwise padding (zero column, never rotated)
+__device__ __forceinline__ bool col_live(const Slot& s, int c, int n) {
+  return (int)s.id[c] < n;
+}
+
+// Runs the sweeps.  On return the CURRENT set holds the converged blocks
+// (exact squared norms in nrm) and every CTA's gnorm[id] holds all n squared
+// norms.  Returns the sweep count.
+template <int CL, int RPL>
+__device__ int run_sweeps(cg::cluster_group& cl, const Geo& g, double* slots, uint64_t* mbar,
+                          double* flags, double* gnorm, int& cur_set, double tol,
+                          int max_sweeps) {
+  const int me = (int)cl.block_rank();
+  const int bs = g.bs;
+  const double tol2 = tol * tol;
+  const int NB = 2 * CL;
+  int set = cur_set;
+  uint32_t use[2] = {0u, 0u};
+  // destinations of this CTA's slot 0 (top) and slot 1 (bottom) after a step
+  int d0c, d0s, d1c, d1s;
+  if (me == 0) { d0c = 0; d0s = 0; d1c = (CL > 1) ? 1 : 0; d1s = 0; }
+  else {
+    d1c = me - 1; d1s = 1;
+    if (me == CL - 1) { d0c = me; d0s = 1; }
+    else { d0c = me + 1; d0s = 0; }
+  }
+  const uint32_t slot_bytes = (uint32_t)(g.slot * sizeof(double));
+  const uint32_t slots_u32 = smem_u32(slots);
+  const uint32_t mbar_u32 = smem_u32(mbar);
+  int sweep = 0;
+  bool converged = false;
+#ifdef POD_BJ_TIMING
+  unsigned long long _bj_last = clock64();
+#endif
+  while (sweep < max_sweeps && !converged) {
+    BJ_T(0);
+    Slot c0 = slot_at(slots, g, set, 0), c1 = slot_at(slots, g, set, 1);
+    // exact squared norms of the owned columns
+    for (int t = threadIdx.x; t < 2 * bs; t += blockDim.x) {
+      const Slot& s = (t < bs) ? c0 : c1;
+      const int c = t % bs;
+      const double* w = s.w + (size_t)c * g.ld;
+      double a = 0.0;
+      for (int i = 0; i < g.nrows; ++i) a = fma(w[i], w[i], a);
+      s.nrm[c] = a;
+    }
+    __syncthreads();
+    BJ_T(1);
+    bool rot = false;
+    // intra phase: round-robin inside each owned block (both blocks at once)
+    {
+      const int B = bs + (bs & 1);
+      for (int step = 0; step < B - 1; ++step) {
+        const int half = B / 2;
+        rot |= sub_round<RPL>(c0, c1, g, 2 * half, tol2, [&](int k, int& xs, int& xc, int& ys, int& yc) {
+          const int blk = k / half, pr = k % half;
+          int a, b;
+          if (pr == 0) { a = 0; b = 1 + step; }
+          else {
+            a = step + pr; a = (a >= B - 1 ? a - (B - 1) : a) + 1;
+            b = step - pr + B - 1; b = (b >= B - 1 ? b - (B - 1) : b) + 1;
+          }
+          if (a > b) { const int t = a; a = b; b = t; }
+          xs = ys = blk;
+          xc = a;
+          yc = b;
+          const Slot& sb = blk ? c1 : c0;
+          return b < bs && col_live(sb, a, g.n) && col_live(sb, b, g.n);
+        });
+      }
+    }
+    BJ_T(2);
+    for (int st = 0; st < NB - 1; ++st) {
+      // inter phase: all bs^2 pairs (top col i, bottom col (i + t) % bs)
+      rot |= inter_step<RPL>(c0, c1, g, tol2);
+      BJ_T(3);
+      const bool last = (st == NB - 2);
+      if (last) {
+        // cluster-wide OR of "rotated this sweep": write my flag everywhere
+        const int any = __syncthreads_or(rot ? 1 : 0);
+        if (threadIdx.x < CL) {
+          double* dst = cl.map_shared_rank(&flags[(sweep & 1) * CL + me], (int)threadIdx.x);
+          *dst = any ? 1.0 : 0.0;
+        }
+      }
+      // generic-proxy writes of this step -> visible to the async-proxy bulk copies
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncthreads();
+      BJ_T(4);
+      cluster_barrier();  // every CTA done with this step (and its incoming copies consumed)
+      BJ_T(5);
+      if (last) {
+        double tot = 0.0;
+        for (int c = 0; c < CL; ++c) tot += flags[(sweep & 1) * CL + c];
+        converged = (tot == 0.0);
+        rot = false;
+      }
+      if (last && (converged || sweep + 1 >= max_sweeps)) break;
+      // move both blocks to their next owners (set -> 1 - set)
+      const int nxt = 1 - set;
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect(&mbar[nxt], 2u * slot_bytes);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        const uint32_t off0 = (uint32_t)((size_t)(nxt * 2 + d0s) * g.slot * sizeof(double));
+        const uint32_t off1 = (uint32_t)((size_t)(nxt * 2 + d1s) * g.slot * sizeof(double));
+        const uint32_t mb = (uint32_t)(nxt * sizeof(uint64_t));
+        bulk_to_cluster(cluster_map(slots_u32 + off0, d0c), c0.w, slot_bytes,
+                        cluster_map(mbar_u32 + mb, d0c));
+        bulk_to_cluster(cluster_map(slots_u32 + off1, d1c), c1.w, slot_bytes,
+                        cluster_map(mbar_u32 + mb, d1c));
+      }
+      BJ_T(6);
+      mbar_wait(&mbar[nxt], use[nxt] & 1u);
+      ++use[nxt];
+      BJ_T(7);
+      set = nxt;
+      c0 = slot_at(slots, g, set, 0);
+      c1 = slot_at(slots, g, set, 1);
+    }
+    ++sweep;
+  }
+  // exact final norms, then all-gather by column id
+  const Slot f0 = slot_at(slots, g, set, 0), f1 = slot_at(slots, g, set, 1);
+  for (int t = threadIdx.x; t < 2 * bs; t += blockDim.x) {
+    const Slot& s = (t < bs) ? f0 : f1;
+    const int c = t % bs;
+    const double* w = s.w + (size_t)c * g.ld;
+    double a = 0.0;
+    for (int i = 0; i < g.nrows; ++i) a = fma(w[i], w[i], a);
+    s.nrm[c] = a;
+    const int id = (int)s.id[c];
+    if (id < g.n)
+      for (int r = 0; r < CL; ++r) *cl.map_shared_rank(&gnorm[id], r) = a;
+  }
+  cluster_barrier();
+  cur_set = set;
+  return sweep;
+}
+
+// initial ownership: CTA c holds block c (top) and block 2CL-1-c (bottom)
+__device__ __forceinline__ int init_block(int me, int t, int CL) { return t == 0 ? me : 2 * CL - 1 - me; }
+
+template <int CL>
+struct Smem {
+  uint64_t* mbar;
+  double* flags;
+  double* gnorm;
+  double* slots;
+};
+template <int CL>
+__device__ __forceinline__ Smem<CL> carve(double* base, const Geo& g) {
+  Smem<CL> s;
+  s.mbar = reinterpret_cast<uint64_t*>(base);
+  s.flags = base + 2;
+  s.gnorm = s.flags + 2 * CL;
+  s.slots = s.gnorm + 2 * CL * g.bs;
+  return s;
+}
+
+template <int CL>
+__device__ void setup(cg::cluster_group& cl, const Smem<CL>& sm) {
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.mbar[0], 1);
+    mbar_init(&sm.mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int t = threadIdx.x; t < 2 * CL; t += blockDim.x) sm.flags[t] = 0.0;
+  __syncthreads();
+  cluster_barrier();
+}
+
+// rank of column id j among the n gathered norms (descending, ties -> lower id)
+__device__ __forceinline__ int rank_of(const double* key, int n, int j) {
+  const double kj = key[j];
+  int rank = 0;
+  for (int i = 0; i < n; ++i) {
+    const double ki = key[i];
+    rank += (ki > kj) || (ki == kj && i < j);
+  }
+  return rank;
+}
+
+// ------------------------------------------------------------ merge core --
+template <int CL, int RPL>
+__global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
+    merge_core_kernel(const double* __restrict__ sig1, int l1, const double* __restrict__ M,
+                      int64_t ldm, const double* __restrict__ Rm, int64_t ldr,
+                      const double* __restrict__ sig2, int l2, int r, int rcap,
+                      double* __restrict__ T, int64_t ldt, int tcols, double* __restrict__ sig_new,
+                      int64_t* __restrict__ info, int max_sweeps) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double smem_bj[];
+  const int n = l1 + l2;
+  const Geo g(n, n, 0, CL);
+  const Smem<CL> sm = carve<CL>(smem_bj, g);
+  const int me = (int)cl.block_rank();
+  // E = [[S1, M S2], [0, R S2]] columns of the two owned blocks
+  for (int t2 = 0; t2 < 2; ++t2) {
+    const Slot s = slot_at(sm.slots, g, 0, t2);
+    const int blk = init_block(me, t2, CL);
+    for (int t = threadIdx.x; t < g.bs * g.ld; t += blockDim.x) {
+      const int c = t / g.ld, i = t - c * g.ld;
+      const int j = blk * g.bs + c;
+      double e = 0.0;
+      if (j < n && i < n) {
+        if (j < l1) e = (i == j) ? sig1[j] : 0.0;
+        else {
+          const int jj = j - l1;
+          if (i < l1) e = M[i + (int64_t)jj * ldm] * sig2[jj];
+          else {
+            const int ii = i - l1;
+            e = (ii <= jj) ? Rm[ii + (int64_t)jj * ldr] * sig2[jj] : 0.0;
+          }
+        }
+      }
+      s.w[t] = e;
+    }
+    for (int c = threadIdx.x; c < g.bse; c += blockDim.x) {
+      s.id[c] = (double)(c < g.bs ? blk * g.bs + c : 1 << 30);
+      s.nrm[c] = 0.0;
+    }
+  }
+  setup<CL>(cl, sm);
+  int set = 0;
+  const int sweeps = run_sweeps<CL, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
+                                         2.220446049250313e-16 * (double)max(n, 16), max_sweeps);
+  // sigma, keep (identical in every CTA)
+  double s0 = 0.0;
+  for (int i = 0; i < n; ++i) s0 = fmax(s0, sm.gnorm[i]);
+  s0 = sqrt(s0);
+  const double thr = 1e-14 * fmax(s0, 1e-300);
+  int cnt = 0;
+  for (int i = 0; i < n; ++i) cnt += sqrt(sm.gnorm[i]) > thr;
+  const int keep = min(r, cnt);
+  if (me == 0 && threadIdx.x == 0) {
+    info[0] = keep;
+    info[1] = sweeps;
+  }
+  if (me == 0)
+    for (int k = keep + threadIdx.x; k < rcap; k += blockDim.x) sig_new[k] = 0.0;
+  for (int t2 = 0; t2 < 2; ++t2) {
+    const Slot s = slot_at(sm.slots, g, set, t2);
+    for (int c = 0; c < g.bs; ++c) {
+      const int id = (int)s.id[c];
+      if (id >= n) continue;
+      const int k = rank_of(sm.gnorm, n, id);
+      if (k >= tcols) continue;
+      const double sg = sqrt(sm.gnorm[id]);
+      if (threadIdx.x == 0 && k < keep && k < rcap) sig_new[k] = sg;
+      const double* w = s.w + (size_t)c * g.ld;
+      for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const int row = (e < l1) ? e : rcap + (e - l1);
+        T[row + (int64_t)k * ldt] = (k < keep) ? w[e] / sg : 0.0;
+      }
+    }
+  }
+  if (me == 0)
+    for (int t = threadIdx.x; t < (rcap - l1) * tcols; t += blockDim.x) {
+      const int k = t / (rcap - l1), row = l1 + t % (rcap - l1);
+      T[row + (int64_t)k * ldt] = 0.0;
+    }
+  if (me == 0)  // columns beyond n (only when tcols > n)
+    for (int t = threadIdx.x; t < (tcols > n ? (tcols - n) : 0) * (rcap + l2); t += blockDim.x) {
+      const int k = n + t / (rcap + l2), row = t % (rcap + l2);
+      T[row + (int64_t)k * ldt] = 0.0;
+    }
+  cluster_barrier();
+}
+
+// ------------------------------------------------------------- gram eigh --
+template <int CL, int RPL>
+__global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
+    gram_eigh_kernel(const double* __restrict__ X, const int* __restrict__ piv,
+                     const int64_t* __restrict__ rank_in, int gdim, int r,
+                     double* __restrict__ sigma_out, double* __restrict__ T, int64_t ldt,
+                     int64_t* __restrict__ info, int max_sweeps) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double smem_bj[];
+  const Geo g(gdim, gdim, 0, CL);
+  const Smem<CL> sm = carve<CL>(smem_bj, g);
+  const int me = (int)cl.block_rank();
+  const int rank = (int)*rank_in;
+  for (int t2 = 0; t2 < 2; ++t2) {
+    const Slot s = slot_at(sm.slots, g, 0, t2);
+    const int blk = init_block(me, t2, CL);
+    for (int t = threadIdx.x; t < g.bs * g.ld; t += blockDim.x) {
+      const int c = t / g.ld, i = t - c * g.ld;
+      const int j = blk * g.bs + c;
+      s.w[t] = (j < rank && i < gdim) ? X[i + (int64_t)j * gdim] : 0.0;
+    }
+    for (int c = threadIdx.x; c < g.bse; c += blockDim.x) {
+      s.id[c] = (double)(c < g.bs ? blk * g.bs + c : 1 << 30);
+      s.nrm[c] = 0.0;
+    }
+  }
+  setup<CL>(cl, sm);
+  int set = 0;
+  const int sweeps = run_sweeps<CL, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
+                                         2.220446049250313e-16 * (double)max(gdim, 16),
+                                         max_sweeps);
+  // lambda = squared norms (ids >= rank are zero columns)
+  double lam0 = 0.0;
+  for (int i = 0; i < gdim; ++i) lam0 = fmax(lam0, sm.gnorm[i]);
+  const double dust = 1e-12 * fmax(lam0, 2.2250738585072014e-308);  // matcore.py:26
+  const double s0 = lam0 <= dust ? 0.0 : sqrt(lam0);
+  int rk = 0;
+  if (s0 > 0.0) {
+    const double thr = 1e-14 * s0;  // matcore.py:20
+    for (int i = 0; i < gdim; ++i) {
+      const double lam = sm.gnorm[i];
+      rk += (lam <= dust ? 0.0 : sqrt(lam)) > thr;
+    }
+  }
+  const int keep = min(r, rk);
+  if (me == 0 && threadIdx.x == 0) {
+    info[0] = rk;
+    info[1] = keep;
+    info[2] = sweeps;
+  }
+  for (int t2 = 0; t2 < 2; ++t2) {
+    const Slot s = slot_at(sm.slots, g, set, t2);
+    for (int c = 0; c < g.bs; ++c) {
+      const int id = (int)s.id[c];
+      if (id >= gdim) continue;
+      const int k = rank_of(sm.gnorm, gdim, id);
+      const double lam = sm.gnorm[id];
+      const double sg = lam <= dust ? 0.0 : sqrt(lam);
+      if (threadIdx.x == 0) sigma_out[k] = sg;
+      if (k >= r) continue;
+      const double* w = s.w + (size_t)c * g.ld;
+      const double nrm = sqrt(lam);
+      for (int i = threadIdx.x; i < gdim; i += blockDim.x)
+        T[piv[i] + (int64_t)k * ldt] = (k < keep) ? w[i] / nrm / sg : 0.0;
+    }
+  }
+  if (me == 0)  // output columns beyond g (only when r > g)
+    for (int t = threadIdx.x; t < (r > gdim ? r - gdim : 0) * gdim; t += blockDim.x) {
+      const int k = gdim + t / gdim, i = t % gdim;
+      T[i + (int64_t)k * ldt] = 0.0;
+    }
+  cluster_barrier();
+}
+
+// ------------------------------------------------------------- svd small --
+template <int CL, int RPL>
+__global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
+    svd_kernel(const double* __restrict__ A, int64_t lda, int nr, int nc, double* __restrict__ U,
+               int64_t ldu, double* __restrict__ sigma, double* __restrict__ V, int64_t ldv,
+               int64_t* __restrict__ info, int max_sweeps) {
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double smem_bj[];
+  const Geo g(nc, nr, V ? nc : 0, CL);
+  const Smem<CL> sm = carve<CL>(smem_bj, g);
+  const int me = (int)cl.block_rank();
+  for (int t2 = 0; t2 < 2; ++t2) {
+    const Slot s = slot_at(sm.slots, g, 0, t2);
+    const int blk = init_block(me, t2, CL);
+    for (int t = threadIdx.x; t < g.bs * g.ld; t += blockDim.x) {
+      const int c = t / g.ld, i = t - c * g.ld;
+      const int j = blk * g.bs + c;
+      s.w[t] = (j < nc && i < nr) ? A[i + (int64_t)j * lda] : 0.0;
+    }
+    if (V)
+      for (int t = threadIdx.x; t < g.bs * g.ldj; t += blockDim.x) {
+        const int c = t / g.ldj, i = t - c * g.ldj;
+        const int j = blk * g.bs + c;
+        s.j[t] = (j < nc && i == j) ? 1.0 : 0.0;
+      }
+    for (int c = threadIdx.x; c < g.bse; c += blockDim.x) {
+      s.id[c] = (double)(c < g.bs ? blk * g.bs + c : 1 << 30);
+      s.nrm[c] = 0.0;
+    }
+  }
+  setup<CL>(cl, sm);
+  int set = 0;
+  const int sweeps = run_sweeps<CL, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
+                                         2.220446049250313e-16 * (double)max(nr, 16), max_sweeps);
+  if (me == 0 && threadIdx.x == 0) info[0] = sweeps;
+  for (int t2 = 0; t2 < 2; ++t2) {
+    const Slot s = slot_at(sm.slots, g, set, t2);
+    for (int c = 0; c < g.bs; ++c) {
+      const int id = (int)s.id[c];
+      if (id >= nc) continue;
+      const int k = rank_of(sm.gnorm, nc, id);
+      const double sg = sqrt(sm.gnorm[id]);
+      if (threadIdx.x == 0) sigma[k] = sg;
+      if (U) {
+        const double* w = s.w + (size_t)c * g.ld;
+        for (int i = threadIdx.x; i < nr; i += blockDim.x)
+          U[i + (int64_t)k * ldu] = sg > 0.0 ? w[i] / sg : 0.0;
+      }
+      if (V) {
+        const double* j = s.j + (size_t)c * g.ldj;
+        for (int i = threadIdx.x; i < nc; i += blockDim.x) V[i + (int64_t)k * ldv] = j[i];
+      }
+    }
+  }
+  cluster_barrier();
+}
+
+// ----------------------------------------------------------------- host ---
+static int set_smem(const void* fn) {
+  static const void* fns[32];
+  static int nf = 0;
+  for (int i = 0; i < nf; ++i)
+    if (fns[i] == fn) return POD_OK;
+  cudaError_t e =
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_CAP);
+  if (e != cudaSuccess) return cuda_status(e, "block jacobi smem attr");
+  if (nf < 32) fns[nf++] = fn;
+  return POD_OK;
+}
+
+template <typename K, typename... Args>
+static int launch(K kernel, int cl, int threads, size_t smem, cudaStream_t stream, Args... args) {
+  int st = set_smem((const void*)kernel);
+  if (st) return st;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, args...);
+  return e == cudaSuccess ? POD_OK : cuda_status(e, "block jacobi launch");
+}
+
+// Lanes per column pair: a power of two near nrows/12 (4..32) -- fewer lanes
+// mean fewer shuffle levels on the per-sub-round critical path, more rows
+// per lane in registers.  Threads = bs pairs x lanes, whole warps, <= 512.
+static int lanes_for(const Geo& g) {
+  static int div = -1;
+  if (div < 0) {  // POD_BJ_ROWS_PER_LANE: tuning override of the target rows per lane
+    const char* e = getenv("POD_BJ_ROWS_PER_LANE");
+    div = e ? std::max(1, atoi(e)) : 4;
+  }
+  int want = std::max(4, std::min(32, g.nrows / div));
+  int tpp = 4;
+  while (tpp * 2 <= want) tpp *= 2;
+  while (tpp > 1 && g.bs * tpp > 384) tpp /= 2;
+  return tpp;
+}
+static int threads_for(const Geo& g) {
+  const int t = g.bs * lanes_for(g);
+  return std::max(32, std::min(384, ((t + 31) / 32) * 32));
+}
+static int pow2_floor_h(int v) {
+  int p = 1;
+  while (p * 2 <= v) p *= 2;
+  return p;
+}
+// rows per lane over both phases (the device derives lanes from blockDim)
+static int rpl_for(const Geo& g, int threads) {
+  const int pi = g.bs + (g.bs & 1);
+  const int t_inter = std::min(32, pow2_floor_h(std::max(1, threads / g.bs)));
+  const int t_intra = std::min(32, pow2_floor_h(std::max(1, threads / pi)));
+  const int tpp = std::min(t_inter, t_intra);
+  return (g.nrows + tpp - 1) / tpp;
+}
+
+}  // namespace bj
+
+constexpr int BJ_CL = 8;
+static const int BJ_NOT_APPLICABLE = -1;
+
+static bool bj_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_JACOBI");
+    v = (e && e[0] == 'c') ? 0 : 1;  // POD_JACOBI=cluster: row-distributed solver
+  }
+  return v == 1;
+}
+
+int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
+                  int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
+                  int64_t ldt, int64_t tcols, double* sig_new, int64_t* info,
+                  cudaStream_t stream) {
+  if (!bj_enabled()) return BJ_NOT_APPLICABLE;
+  const int n = (int)(l1 + l2);
+  const bj::Geo g(n, n, 0, BJ_CL);
+  const size_t bytes = g.smem_bytes(BJ_CL);
+  if (bytes > bj::SMEM_CAP || n < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
+  const int th = bj::threads_for(g);
+  const int rpl = bj::rpl_for(g, th);
+#define BJ_MC(R_) bj::launch(bj::merge_core_kernel<BJ_CL, R_>, BJ_CL, th, bytes, stream, sig1, \
+                             (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, \
+                             (int)tcols, sig_new, info, 60)
+  if (rpl <= 4) return BJ_MC(4);
+  if (rpl <= 8) return BJ_MC(8);
+  if (rpl <= 16) return BJ_MC(16);
+  if (rpl <= 24) return BJ_MC(24);
+  if (rpl <= 32) return BJ_MC(32);
+  return BJ_MC(0);
+#undef BJ_MC
+}
+
+int bj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t gd, int64_t r,
+                 double* sigma, double* T, int64_t ldt, int64_t* info, cudaStream_t stream) {
+  if (!bj_enabled()) return BJ_NOT_APPLICABLE;
+  const bj::Geo g((int)gd, (int)gd, 0, BJ_CL);
+  const size_t bytes = g.smem_bytes(BJ_CL);
+  if (bytes > bj::SMEM_CAP || gd < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
+  const int th = bj::threads_for(g);
+  const int rpl = bj::rpl_for(g, th);
+#define BJ_GE(R_) bj::launch(bj::gram_eigh_kernel<BJ_CL, R_>, BJ_CL, th, bytes, stream, X, piv, \
+                             rank, (int)gd, (int)r, sigma, T, ldt, info, 60)
+  if (rpl <= 4) return BJ_GE(4);
+  if (rpl <= 8) return BJ_GE(8);
+  if (rpl <= 16) return BJ_GE(16);
+  if (rpl <= 24) return BJ_GE(24);
+  if (rpl <= 32) return BJ_GE(32);
+  return BJ_GE(0);
+#undef BJ_GE
+}
+
+int bj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int64_t ldu,
+           double* sigma, double* V, int64_t ldv, int64_t* info, cudaStream_t stream) {
+  if (!bj_enabled()) return BJ_NOT_APPLICABLE;
+  const bj::Geo g((int)nc, (int)nr, V ? (int)nc : 0, BJ_CL);
+  const size_t bytes = g.smem_bytes(BJ_CL);
+  if (bytes > bj::SMEM_CAP || nc < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
+  const int th = bj::threads_for(g);
+  const int rpl = bj::rpl_for(g, th);
+#define BJ_SV(R_) bj::launch(bj::svd_kernel<BJ_CL, R_>, BJ_CL, th, bytes, stream, A, lda, (int)nr, \
+                             (int)nc, U, ldu, sigma, V, ldv, info, 60)
+  if (rpl <= 4) return BJ_SV(4);
+  if (rpl <= 8) return BJ_SV(8);
+  if (rpl <= 16) return BJ_SV(16);
+  if (rpl <= 24) return BJ_SV(24);
+  if (rpl <= 32) return BJ_SV(32);
+  return BJ_SV(0);
+#undef BJ_SV
+}
+
+}  // namespace pod
+
+#ifdef POD_BJ_TIMING
+extern "C" int pod_debug_bj_phase(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, pod::bj::g_bj_phase, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(pod::bj::g_bj_phase, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

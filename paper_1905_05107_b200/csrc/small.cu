@@ -338,6 +338,13 @@ static int set_smem(const void* fn, size_t bytes) {
 
 static size_t cholqr_bytes(int64_t l) { return (size_t)3 * l * l * 8 + (size_t)l * 8 + 64; }
 
+int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
+                  int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
+                  int64_t ldt, int64_t tcols, double* sig_new, int64_t* info, cudaStream_t stream);
+int bj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t g, int64_t r,
+                 double* sigma, double* T, int64_t ldt, int64_t* info, cudaStream_t stream);
+int bj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int64_t ldu,
+           double* sigma, double* V, int64_t ldv, int64_t* info, cudaStream_t stream);
 int cj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
                   int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
                   int64_t ldt, int64_t tcols, double* sig_new, int64_t* info, cudaStream_t stream);
@@ -381,6 +388,10 @@ extern "C" int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r,
     pivchol_kernel<false><<<1, SMALL_THREADS, 0, s>>>(G, ldg, (int)g, X, piv, rank, scratch);
   }
   POD_CHECK_LAUNCH("pivoted cholesky");
+  {
+    const int bst = bj_gram_eigh(X, piv, rank, g, r, sigma, T, ldt, info, s);
+    if (bst != -1) return bst;  // -1: size not handled by the block solver
+  }
   return cj_gram_eigh(X, piv, rank, g, r, sigma, T, ldt, info, s);
 }
 
@@ -414,6 +425,9 @@ extern "C" int pod_merge_core(const double* sig1, int64_t l1, const double* M, i
               "pod_merge_core: bad shape");
   (void)ws;
   (void)ws_bytes;
+  const int bst = bj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols,
+                                sig_new, info, (cudaStream_t)stream);
+  if (bst != -1) return bst;  // -1: size not handled by the block solver
   return cj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info,
                        (cudaStream_t)stream);
 }
@@ -424,6 +438,8 @@ extern "C" int pod_svd_small(const double* A, int64_t lda, int64_t nr, int64_t n
   POD_REQUIRE(nr >= 1 && nc >= 1 && lda >= nr && nr >= nc, "pod_svd_small: bad shape");
   (void)ws;
   (void)ws_bytes;
+  const int bst = bj_svd(A, lda, nr, nc, U, ldu, sigma, V, ldv, info, (cudaStream_t)stream);
+  if (bst != -1) return bst;  // -1: size not handled by the block solver
   return cj_svd(A, lda, nr, nc, U, ldu, sigma, V, ldv, info, (cudaStream_t)stream);
 }
 
