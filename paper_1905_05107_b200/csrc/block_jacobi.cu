@@ -201,9 +201,10 @@ struct PairRef {
   double* ny;
 };
 
-template <int RPL>
-__device__ __forceinline__ bool rotate_pair(const PairRef& pr, bool live, int gl, int tpp,
-                                            int nrows, int njrows, double tol2) {
+template <int TPP, int RPL>
+__device__ __forceinline__ bool rotate_pair(const PairRef& pr, bool live, int gl, int nrows,
+                                            int njrows, double tol2) {
+  constexpr int tpp = TPP;
   double g = 0.0;
   double xa[RPL > 0 ? RPL : 1], xb[RPL > 0 ? RPL : 1];
   if (RPL > 0) {
@@ -221,6 +222,7 @@ __device__ __forceinline__ bool rotate_pair(const PairRef& pr, bool live, int gl
   // norms are read before the (synchronising) shuffles; lane 0 rewrites them
   // only after its group has passed the shuffles
   const double al = live ? *pr.nx : 0.0, be = live ? *pr.ny : 0.0;
+#pragma unroll
   for (int o = tpp / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o, tpp);
   if (!live) return false;
   if (!(g * g > tol2 * al * be && al > 0.0 && be > 0.0)) return false;
@@ -265,10 +267,10 @@ __device__ __forceinline__ int pow2_floor(int v) {
 
 // One sub-round: P disjoint pairs in parallel; pairs produced by `pick(k,
 // &x_slot, &x_col, &y_slot, &y_col)`; returns whether this thread's pair rotated.
-template <int RPL, typename Pick>
+template <int TPP, int RPL, typename Pick>
 __device__ bool sub_round(const Slot& c0, const Slot& c1, const Geo& g, int P, double tol2,
                           Pick pick) {
-  const int tpp = min(32, pow2_floor(max(1, (int)blockDim.x / max(P, 1))));
+  constexpr int tpp = TPP;
   const int grp = threadIdx.x / tpp, gl = threadIdx.x % tpp;
   const int ngrp = blockDim.x / tpp;
   bool rot = false;
@@ -287,7 +289,7 @@ __device__ bool sub_round(const Slot& c0, const Slot& c1, const Geo& g, int P, d
     pr.jy = g.ldj ? sy.j + (size_t)yc * g.ldj : nullptr;
     pr.nx = sx.nrm + xc;
     pr.ny = sy.nrm + yc;
-    rot |= rotate_pair<RPL>(pr, live, gl, tpp, g.nrows, g.njrows, tol2);
+    rot |= rotate_pair<TPP, RPL>(pr, live, gl, g.nrows, g.njrows, tol2);
   }
   __syncthreads();
   return rot;
@@ -296,10 +298,10 @@ __device__ bool sub_round(const Slot& c0, const Slot& c1, const Geo& g, int P, d
 // One tournament step's inter-block pairs: group k keeps top column k (rows
 // in registers when RPL > 0, norm in a register) and meets bottom columns
 // k, k+1, ... (mod bs) in bs sub-rounds.
-template <int RPL>
+template <int TPP, int RPL>
 __device__ bool inter_step(const Slot& c0, const Slot& c1, const Geo& g, double tol2) {
   const int bs = g.bs;
-  const int tpp = min(32, pow2_floor(max(1, (int)blockDim.x / bs)));
+  constexpr int tpp = TPP;
   const int grp = threadIdx.x / tpp, gl = threadIdx.x % tpp;
   const bool has = grp < bs;
   uint32_t m1 = 0;
@@ -344,6 +346,7 @@ __device__ bool inter_step(const Slot& c0, const Slot& c1, const Geo& g, double 
     }
     const double be = live ? c1.nrm[yc] : 0.0;  // read before the shuffles
     BJ_TI(8);
+#pragma unroll
     for (int o = tpp / 2; o > 0; o >>= 1) gam += __shfl_xor_sync(0xffffffffu, gam, o, tpp);
     BJ_TI(9);
     if (live && gam * gam > tol2 * al * be && al > 0.0 && be > 0.0) {
@@ -404,7 +407,7 @@ __device__ __forceinline__ bool col_live(const Slot& s, int c, int n) {
 // Runs the sweeps.  On return the CURRENT set holds the converged blocks
 // (exact squared norms in nrm) and every CTA's gnorm[id] holds all n squared
 // norms.  Returns the sweep count.
-template <int CL, int RPL>
+template <int CL, int TPP, int RPL>
 __device__ int run_sweeps(cg::cluster_group& cl, const Geo& g, double* slots, uint64_t* mbar,
                           double* flags, double* gnorm, int& cur_set, double tol,
                           int max_sweeps) {
@@ -450,7 +453,7 @@ __device__ int run_sweeps(cg::cluster_group& cl, const Geo& g, double* slots, ui
       const int B = bs + (bs & 1);
       for (int step = 0; step < B - 1; ++step) {
         const int half = B / 2;
-        rot |= sub_round<RPL>(c0, c1, g, 2 * half, tol2, [&](int k, int& xs, int& xc, int& ys, int& yc) {
+        rot |= sub_round<TPP, RPL>(c0, c1, g, 2 * half, tol2, [&](int k, int& xs, int& xc, int& ys, int& yc) {
           const int blk = k / half, pr = k % half;
           int a, b;
           if (pr == 0) { a = 0; b = 1 + step; }
@@ -470,7 +473,7 @@ __device__ int run_sweeps(cg::cluster_group& cl, const Geo& g, double* slots, ui
     BJ_T(2);
     for (int st = 0; st < NB - 1; ++st) {
       // inter phase: all bs^2 pairs (top col i, bottom col (i + t) % bs)
-      rot |= inter_step<RPL>(c0, c1, g, tol2);
+      rot |= inter_step<TPP, RPL>(c0, c1, g, tol2);
       BJ_T(3);
       const bool last = (st == NB - 2);
       if (last) {
@@ -579,8 +582,8 @@ __device__ __forceinline__ int rank_of(const double* key, int n, int j) {
 }
 
 // ------------------------------------------------------------ merge core --
-template <int CL, int RPL>
-__global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
+template <int CL, int TPP, int RPL>
+__global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
     merge_core_kernel(const double* __restrict__ sig1, int l1, const double* __restrict__ M,
                       int64_t ldm, const double* __restrict__ Rm, int64_t ldr,
                       const double* __restrict__ sig2, int l2, int r, int rcap,
@@ -620,7 +623,7 @@ __global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
   }
   setup<CL>(cl, sm);
   int set = 0;
-  const int sweeps = run_sweeps<CL, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
+  const int sweeps = run_sweeps<CL, TPP, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
                                          2.220446049250313e-16 * (double)max(n, 16), max_sweeps);
   // sigma, keep (identical in every CTA)
   double s0 = 0.0;
@@ -666,8 +669,8 @@ __global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
 }
 
 // ------------------------------------------------------------- gram eigh --
-template <int CL, int RPL>
-__global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
+template <int CL, int TPP, int RPL>
+__global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
     gram_eigh_kernel(const double* __restrict__ X, const int* __restrict__ piv,
                      const int64_t* __restrict__ rank_in, int gdim, int r,
                      double* __restrict__ sigma_out, double* __restrict__ T, int64_t ldt,
@@ -693,7 +696,7 @@ __global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
   }
   setup<CL>(cl, sm);
   int set = 0;
-  const int sweeps = run_sweeps<CL, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
+  const int sweeps = run_sweeps<CL, TPP, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
                                          2.220446049250313e-16 * (double)max(gdim, 16),
                                          max_sweeps);
   // lambda = squared norms (ids >= rank are zero columns)
@@ -740,8 +743,8 @@ __global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
 }
 
 // ------------------------------------------------------------- svd small --
-template <int CL, int RPL>
-__global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
+template <int CL, int TPP, int RPL>
+__global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
     svd_kernel(const double* __restrict__ A, int64_t lda, int nr, int nc, double* __restrict__ U,
                int64_t ldu, double* __restrict__ sigma, double* __restrict__ V, int64_t ldv,
                int64_t* __restrict__ info, int max_sweeps) {
@@ -771,7 +774,7 @@ __global__ void __launch_bounds__(RPL >= 32 ? 256 : (RPL >= 16 ? 384 : 512))
   }
   setup<CL>(cl, sm);
   int set = 0;
-  const int sweeps = run_sweeps<CL, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
+  const int sweeps = run_sweeps<CL, TPP, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
                                          2.220446049250313e-16 * (double)max(nr, 16), max_sweeps);
   if (me == 0 && threadIdx.x == 0) info[0] = sweeps;
   for (int t2 = 0; t2 < 2; ++t2) {
@@ -829,38 +832,22 @@ static int launch(K kernel, int cl, int threads, size_t smem, cudaStream_t strea
   return e == cudaSuccess ? POD_OK : cuda_status(e, "block jacobi launch");
 }
 
-// Lanes per column pair: a power of two near nrows/12 (4..32) -- fewer lanes
+// Lanes per column pair: a power of two near nrows/4 (8..32) -- fewer lanes
 // mean fewer shuffle levels on the per-sub-round critical path, more rows
-// per lane in registers.  Threads = bs pairs x lanes, whole warps, <= 512.
+// per lane in registers.  Threads = bs pairs x lanes in whole warps.
 static int lanes_for(const Geo& g) {
   static int div = -1;
   if (div < 0) {  // POD_BJ_ROWS_PER_LANE: tuning override of the target rows per lane
     const char* e = getenv("POD_BJ_ROWS_PER_LANE");
     div = e ? std::max(1, atoi(e)) : 4;
   }
-  int want = std::max(4, std::min(32, g.nrows / div));
-  int tpp = 4;
+  const int want = std::max(8, std::min(32, g.nrows / div));
+  int tpp = 8;
   while (tpp * 2 <= want) tpp *= 2;
-  while (tpp > 1 && g.bs * tpp > 384) tpp /= 2;
+  while (tpp > 8 && g.bs * tpp > 384) tpp /= 2;
   return tpp;
 }
-static int threads_for(const Geo& g) {
-  const int t = g.bs * lanes_for(g);
-  return std::max(32, std::min(384, ((t + 31) / 32) * 32));
-}
-static int pow2_floor_h(int v) {
-  int p = 1;
-  while (p * 2 <= v) p *= 2;
-  return p;
-}
-// rows per lane over both phases (the device derives lanes from blockDim)
-static int rpl_for(const Geo& g, int threads) {
-  const int pi = g.bs + (g.bs & 1);
-  const int t_inter = std::min(32, pow2_floor_h(std::max(1, threads / g.bs)));
-  const int t_intra = std::min(32, pow2_floor_h(std::max(1, threads / pi)));
-  const int tpp = std::min(t_inter, t_intra);
-  return (g.nrows + tpp - 1) / tpp;
-}
+static int threads_for(const Geo& g, int tpp) { return ((g.bs * tpp + 31) / 32) * 32; }
 
 }  // namespace bj
 
@@ -885,18 +872,22 @@ int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, 
   const bj::Geo g(n, n, 0, BJ_CL);
   const size_t bytes = g.smem_bytes(BJ_CL);
   if (bytes > bj::SMEM_CAP || n < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
-  const int th = bj::threads_for(g);
-  const int rpl = bj::rpl_for(g, th);
-#define BJ_MC(R_) bj::launch(bj::merge_core_kernel<BJ_CL, R_>, BJ_CL, th, bytes, stream, sig1, \
-                             (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, \
-                             (int)tcols, sig_new, info, 60)
-  if (rpl <= 4) return BJ_MC(4);
-  if (rpl <= 8) return BJ_MC(8);
-  if (rpl <= 16) return BJ_MC(16);
-  if (rpl <= 24) return BJ_MC(24);
-  if (rpl <= 32) return BJ_MC(32);
-  return BJ_MC(0);
-#undef BJ_MC
+  const int tpp = bj::lanes_for(g);
+  const int th = bj::threads_for(g, tpp);
+  const int rpl = (g.nrows + tpp - 1) / tpp;
+  if (th > 512 || (rpl > 8 && th > 384)) return BJ_NOT_APPLICABLE;
+#define BJ_L(T_, R_) bj::launch(bj::merge_core_kernel<BJ_CL, T_, R_>, BJ_CL, th, bytes, stream, sig1, (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new, info, 60)
+#define BJ_R(T_)                         \
+  if (rpl <= 4) return BJ_L(T_, 4);      \
+  if (rpl <= 8) return BJ_L(T_, 8);      \
+  if (rpl <= 16) return BJ_L(T_, 16);    \
+  if (rpl <= 24) return BJ_L(T_, 24);    \
+  return BJ_L(T_, 0);
+  if (tpp == 8) { BJ_R(8) }
+  if (tpp == 16) { BJ_R(16) }
+  BJ_R(32)
+#undef BJ_R
+#undef BJ_L
 }
 
 int bj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t gd, int64_t r,
@@ -905,17 +896,22 @@ int bj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t g
   const bj::Geo g((int)gd, (int)gd, 0, BJ_CL);
   const size_t bytes = g.smem_bytes(BJ_CL);
   if (bytes > bj::SMEM_CAP || gd < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
-  const int th = bj::threads_for(g);
-  const int rpl = bj::rpl_for(g, th);
-#define BJ_GE(R_) bj::launch(bj::gram_eigh_kernel<BJ_CL, R_>, BJ_CL, th, bytes, stream, X, piv, \
-                             rank, (int)gd, (int)r, sigma, T, ldt, info, 60)
-  if (rpl <= 4) return BJ_GE(4);
-  if (rpl <= 8) return BJ_GE(8);
-  if (rpl <= 16) return BJ_GE(16);
-  if (rpl <= 24) return BJ_GE(24);
-  if (rpl <= 32) return BJ_GE(32);
-  return BJ_GE(0);
-#undef BJ_GE
+  const int tpp = bj::lanes_for(g);
+  const int th = bj::threads_for(g, tpp);
+  const int rpl = (g.nrows + tpp - 1) / tpp;
+  if (th > 512 || (rpl > 8 && th > 384)) return BJ_NOT_APPLICABLE;
+#define BJ_L(T_, R_) bj::launch(bj::gram_eigh_kernel<BJ_CL, T_, R_>, BJ_CL, th, bytes, stream, X, piv, rank, (int)gd, (int)r, sigma, T, ldt, info, 60)
+#define BJ_R(T_)                         \
+  if (rpl <= 4) return BJ_L(T_, 4);      \
+  if (rpl <= 8) return BJ_L(T_, 8);      \
+  if (rpl <= 16) return BJ_L(T_, 16);    \
+  if (rpl <= 24) return BJ_L(T_, 24);    \
+  return BJ_L(T_, 0);
+  if (tpp == 8) { BJ_R(8) }
+  if (tpp == 16) { BJ_R(16) }
+  BJ_R(32)
+#undef BJ_R
+#undef BJ_L
 }
 
 int bj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int64_t ldu,
@@ -924,17 +920,22 @@ int bj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int6
   const bj::Geo g((int)nc, (int)nr, V ? (int)nc : 0, BJ_CL);
   const size_t bytes = g.smem_bytes(BJ_CL);
   if (bytes > bj::SMEM_CAP || nc < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
-  const int th = bj::threads_for(g);
-  const int rpl = bj::rpl_for(g, th);
-#define BJ_SV(R_) bj::launch(bj::svd_kernel<BJ_CL, R_>, BJ_CL, th, bytes, stream, A, lda, (int)nr, \
-                             (int)nc, U, ldu, sigma, V, ldv, info, 60)
-  if (rpl <= 4) return BJ_SV(4);
-  if (rpl <= 8) return BJ_SV(8);
-  if (rpl <= 16) return BJ_SV(16);
-  if (rpl <= 24) return BJ_SV(24);
-  if (rpl <= 32) return BJ_SV(32);
-  return BJ_SV(0);
-#undef BJ_SV
+  const int tpp = bj::lanes_for(g);
+  const int th = bj::threads_for(g, tpp);
+  const int rpl = (g.nrows + tpp - 1) / tpp;
+  if (th > 512 || (rpl > 8 && th > 384)) return BJ_NOT_APPLICABLE;
+#define BJ_L(T_, R_) bj::launch(bj::svd_kernel<BJ_CL, T_, R_>, BJ_CL, th, bytes, stream, A, lda, (int)nr, (int)nc, U, ldu, sigma, V, ldv, info, 60)
+#define BJ_R(T_)                         \
+  if (rpl <= 4) return BJ_L(T_, 4);      \
+  if (rpl <= 8) return BJ_L(T_, 8);      \
+  if (rpl <= 16) return BJ_L(T_, 16);    \
+  if (rpl <= 24) return BJ_L(T_, 24);    \
+  return BJ_L(T_, 0);
+  if (tpp == 8) { BJ_R(8) }
+  if (tpp == 16) { BJ_R(16) }
+  BJ_R(32)
+#undef BJ_R
+#undef BJ_L
 }
 
 }  // namespace pod
