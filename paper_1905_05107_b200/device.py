@@ -62,8 +62,18 @@ class ColMat:
 
     def to_numpy(self, ncols=None):
         nc = self.ncols if ncols is None else ncols
-        blk = self.t[self.col0:self.col0 + nc, :self.m]
-        return np.asfortranarray(blk.cpu().numpy().T)
+        return d2h_colmajor(self.t[self.col0:self.col0 + nc, :self.m])
+
+
+def d2h_colmajor(blk):
+    """(ncols, m) device block (rows = columns of the matrix) -> F-ordered
+    (m, ncols) numpy array.  The copy lands in page-locked memory from torch's
+    caching host allocator (DMA at full PCIe rate, no staging copy); the
+    returned array keeps that block alive and releases it to the cache."""
+    host = torch.empty(tuple(blk.shape), dtype=blk.dtype, pin_memory=True)
+    host.copy_(blk, non_blocking=True)
+    torch.cuda.current_stream(blk.device).synchronize()
+    return host.numpy().T
 
 
 class Ctx:

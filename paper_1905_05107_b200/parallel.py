@@ -100,6 +100,10 @@ def gather_row_shards(local, m_total, comm):
 
     l, m_local = local.shape
     if not comm.active:
+        if local.is_cuda:
+            from .device import d2h_colmajor
+
+            return d2h_colmajor(local)
         return np.asfortranarray(local.cpu().numpy().T)
     mmax = max(shard_rows(m_total, comm.world, w)[1] - shard_rows(m_total, comm.world, w)[0]
                for w in range(comm.world))
