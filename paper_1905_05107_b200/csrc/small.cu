@@ -54,28 +54,45 @@ __device__ __forceinline__ void rank_sort_desc(const double* key, int n, int* pe
 // of matcore.py:26).  Writes X = R^T (g x g, zero columns >= rank), piv and
 // rank.  Stage 2 (cluster_jacobi.cu) runs one-sided Jacobi on X's columns:
 // X J = V' Sigma, so convergence is that of an SVD of the sampled block.
-template <bool SMEM>
-__global__ void __launch_bounds__(SMALL_THREADS) pivchol_kernel(
+constexpr int PIVCHOL_THREADS = 512;
+// Right-looking pivoted Cholesky without physical row/column swaps: W keeps
+// the Schur complement in the ORIGINAL index order, row j of R is stored by
+// original index in Rq (Rq[j + q g]) and X = R^T in pivoted order is
+// assembled at the end (X[i, j] = Rq[j, piv[i]]).  W is symmetric and kept
+// as its packed lower triangle (column b holds rows b..g-1 at off(b) =
+// b g - b (b - 1) / 2), so g <= 231 fits in shared memory.  Per step: (A) all threads
+// form r_j; (B) warp 0 updates its register copy of the remaining diagonal
+// and picks the NEXT pivot while warps 1.. apply the rank-1 update, each lane
+// holding its RK rows' r values and done flags in registers (loads of a
+// column are all issued before its stores).  Two barriers per step.
+template <bool SMEM, int RK>
+__global__ void __launch_bounds__(PIVCHOL_THREADS) pivchol_kernel(
     const double* __restrict__ G, int64_t ldg, int g, double* __restrict__ Xout,
-    int* __restrict__ piv_out, int64_t* __restrict__ rank_out, double* gws) {
+    int* __restrict__ piv_out, int64_t* __restrict__ rank_out, double* gws,
+    double* __restrict__ Rq) {
   extern __shared__ __align__(16) double sm[];
-  double* W = SMEM ? sm : gws;
-  __shared__ double s_dmax0, s_red[32];
-  __shared__ int s_ired[32], s_rank, s_piv[1024];
-  int* piv = s_piv;
-  for (int64_t t = threadIdx.x; t < (int64_t)g * g; t += blockDim.x) {
-    const int64_t j = t / g, i = t - j * g;
-    W[t] = G[i + j * ldg];
-  }
-  for (int i = threadIdx.x; i < g; i += blockDim.x) piv[i] = i;
+  double* __restrict__ W = SMEM ? sm : gws;
+  __shared__ double s_d0, s_d, s_rv[512];
+  __shared__ int s_p, s_done[512], s_piv[512];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarp = blockDim.x >> 5;
+  auto off = [g](int b) { return (int64_t)b * g - (int64_t)b * (b - 1) / 2; };
+  auto at = [&](int a, int b) -> double& {  // symmetric element, packed lower storage
+    return a >= b ? W[off(b) + (a - b)] : W[off(a) + (b - a)];
+  };
+  for (int b = warp; b < g; b += nwarp)
+    for (int a = b + lane; a < g; a += 32) W[off(b) + (a - b)] = G[a + b * ldg];
+  for (int q = threadIdx.x; q < g; q += blockDim.x) s_done[q] = 0;
   __syncthreads();
-  int rank = g;
-  for (int j = 0; j < g; ++j) {
+  double diag[RK];  // warp 0: remaining diagonal of rows lane + 32 k
+  uint32_t dmask = 0;  // warp 0: eliminated rows among lane + 32 k
+  auto pick = [&](int j) {  // warp 0: argmax of the remaining diagonal
     double bv = -1.0;
-    int bi = j;
-    for (int i = j + threadIdx.x; i < g; i += blockDim.x) {
-      const double d = W[i + (int64_t)i * g];
-      if (d > bv) { bv = d; bi = i; }
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < RK; ++k) {
+      const int q = lane + 32 * k;
+      if (q < g && !((dmask >> k) & 1u) && diag[k] > bv) { bv = diag[k]; bi = q; }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -83,53 +100,93 @@ __global__ void __launch_bounds__(SMALL_THREADS) pivchol_kernel(
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    if ((threadIdx.x & 31) == 0) { s_red[threadIdx.x >> 5] = bv; s_ired[threadIdx.x >> 5] = bi; }
+    if (lane == 0) {
+      if (j == 0) s_d0 = bv;
+      s_d = bv;
+      s_p = bi;
+    }
+  };
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < RK; ++k) {
+      const int q = lane + 32 * k;
+      diag[k] = q < g ? W[off(q)] : 0.0;
+    }
+    pick(0);
+  }
+  __syncthreads();
+  int rank = g;
+  for (int j = 0; j < g; ++j) {
+    const double d = s_d;
+    if (!(d > 1e-15 * s_d0 && d > 0.0)) {  // remaining block negligible
+      rank = j;
+      break;
+    }
+    const int p = s_p;
+    const double rjj = sqrt(d);
+    // (A) r_j by original index
+    for (int q = threadIdx.x; q < g; q += blockDim.x) {
+      double v = 0.0;
+      if (!s_done[q]) v = (q == p) ? rjj : at(p, q) / rjj;
+      s_rv[q] = (q == p) ? 0.0 : v;  // p leaves the Schur complement
+      Rq[j + (int64_t)q * g] = v;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      double v = s_red[0];
-      int ix = s_ired[0];
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-        if (s_red[w] > v || (s_red[w] == v && s_ired[w] < ix)) { v = s_red[w]; ix = s_ired[w]; }
-      if (j == 0) s_dmax0 = v;
-      s_ired[0] = ix;
-      s_rank = (v > 1e-15 * s_dmax0 && v > 0.0) ? g : j;
+      s_done[p] = 1;
+      s_piv[j] = p;
     }
-    __syncthreads();
-    if (s_rank == j) { rank = j; break; }
-    const int p = s_ired[0];
-    if (p != j) {  // symmetric swap of rows/cols j and p, and of piv
-      for (int i = threadIdx.x; i < g; i += blockDim.x) {
-        double t = W[j + (int64_t)i * g];
-        W[j + (int64_t)i * g] = W[p + (int64_t)i * g];
-        W[p + (int64_t)i * g] = t;
+    if (warp == 0) {  // (B0) next pivot from the updated diagonal
+#pragma unroll
+      for (int k = 0; k < RK; ++k) {
+        const int q = lane + 32 * k;
+        if (q == p) dmask |= 1u << k;
+        if (q < g) {
+          const double rv = s_rv[q];
+          diag[k] -= rv * rv;
+        }
       }
-      __syncthreads();
-      for (int i = threadIdx.x; i < g; i += blockDim.x) {
-        double t = W[i + (int64_t)j * g];
-        W[i + (int64_t)j * g] = W[i + (int64_t)p * g];
-        W[i + (int64_t)p * g] = t;
+      pick(j + 1);
+    } else {  // (B) rank-1 update of the remaining block
+      double rva[RK];
+      uint32_t live = 0;
+#pragma unroll
+      for (int k = 0; k < RK; ++k) {
+        const int a = lane + 32 * k;
+        rva[k] = a < g ? s_rv[a] : 0.0;
+        if (a < g && !s_done[a] && a != p) live |= 1u << k;
       }
-      if (threadIdx.x == 0) { int t = piv[j]; piv[j] = piv[p]; piv[p] = t; }
-      __syncthreads();
-    }
-    const double rjj = sqrt(W[j + (int64_t)j * g]);
-    __syncthreads();
-    for (int k = j + threadIdx.x; k < g; k += blockDim.x)
-      W[j + (int64_t)k * g] = (k == j) ? rjj : W[j + (int64_t)k * g] / rjj;
-    __syncthreads();
-    const int rem = g - j - 1;
-    for (int64_t t = threadIdx.x; t < (int64_t)rem * rem; t += blockDim.x) {
-      const int kk = j + 1 + (int)(t / rem), ii = j + 1 + (int)(t % rem);
-      W[ii + (int64_t)kk * g] -= W[j + (int64_t)ii * g] * W[j + (int64_t)kk * g];
+      for (int b = warp - 1; b < g; b += nwarp - 1) {
+        if (b == p || s_done[b]) continue;
+        const double rb = s_rv[b];
+        double* col = W + off(b) - b;  // col[a] = W(a, b) for a >= b
+        double w[RK];
+#pragma unroll
+        for (int k = 0; k < RK; ++k) {
+          const int a = lane + 32 * k;
+          w[k] = (((live >> k) & 1u) && a >= b) ? col[a] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < RK; ++k) {
+          const int a = lane + 32 * k;
+          if (((live >> k) & 1u) && a >= b) col[a] = w[k] - rva[k] * rb;
+        }
+      }
     }
     __syncthreads();
   }
-  // X[i][j] = R[j][i] for j < rank, i >= j; zero elsewhere
-  for (int64_t t = threadIdx.x; t < (int64_t)g * g; t += blockDim.x) {
-    const int j = (int)(t / g), i = (int)(t - (int64_t)j * g);
-    Xout[t] = (j < rank && i >= j) ? W[j + (int64_t)i * g] : 0.0;
+  // pivot order of the never-eliminated indices (after rank): ascending
+  if (threadIdx.x == 0) {
+    int k = rank;
+    for (int q = 0; q < g; ++q)
+      if (!s_done[q]) s_piv[k++] = q;
   }
-  for (int i = threadIdx.x; i < g; i += blockDim.x) piv_out[i] = piv[i];
+  __syncthreads();
+  // X[i][j] = R[j][piv[i]] for j < rank, i >= j; zero elsewhere
+  for (int jj = warp; jj < g; jj += nwarp)
+    for (int i = lane; i < g; i += 32)
+      Xout[i + (int64_t)jj * g] = (jj < rank && i >= jj) ? Rq[jj + (int64_t)s_piv[i] * g] : 0.0;
+  for (int i = threadIdx.x; i < g; i += blockDim.x) piv_out[i] = s_piv[i];
   if (threadIdx.x == 0) *rank_out = rank;
 }
 
@@ -360,7 +417,7 @@ using namespace pod;
 static size_t gram_ws_bytes(int64_t g) {
   // X (g x g) + piv (g int) + rank, then the pivoted Cholesky's matrix when
   // it does not fit in shared memory
-  return (size_t)g * g * 8 + (size_t)g * 4 + 64 + (size_t)g * g * 8;
+  return (size_t)g * g * 8 + (size_t)g * 4 + 64 + 2 * (size_t)g * g * 8;
 }
 
 extern "C" size_t pod_small_ws_bytes(int64_t n) {
@@ -378,14 +435,23 @@ extern "C" int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r,
   int* piv = (int*)(X + (size_t)g * g);
   int64_t* rank = (int64_t*)(((uintptr_t)(piv + g) + 15) & ~(uintptr_t)15);
   double* scratch = (double*)(((uintptr_t)(rank + 1) + 15) & ~(uintptr_t)15);
-  const size_t bytes = (size_t)g * g * 8;
+  const size_t bytes = (size_t)g * (g + 1) / 2 * 8;  // packed lower triangle
   const int use_smem = bytes <= SMALL_SMEM_CAP;
   if (use_smem) {
-    int st = set_smem((const void*)pivchol_kernel<true>, bytes);
-    if (st) return st;
-    pivchol_kernel<true><<<1, SMALL_THREADS, bytes, s>>>(G, ldg, (int)g, X, piv, rank, scratch);
+    if (g <= 128) {
+      int st = set_smem((const void*)pivchol_kernel<true, 4>, bytes);
+      if (st) return st;
+      pivchol_kernel<true, 4><<<1, PIVCHOL_THREADS, bytes, s>>>(G, ldg, (int)g, X, piv, rank,
+                                                                scratch, scratch + (size_t)g * g);
+    } else {  // g <= 225 here
+      int st = set_smem((const void*)pivchol_kernel<true, 8>, bytes);
+      if (st) return st;
+      pivchol_kernel<true, 8><<<1, PIVCHOL_THREADS, bytes, s>>>(G, ldg, (int)g, X, piv, rank,
+                                                                scratch, scratch + (size_t)g * g);
+    }
   } else {
-    pivchol_kernel<false><<<1, SMALL_THREADS, 0, s>>>(G, ldg, (int)g, X, piv, rank, scratch);
+    pivchol_kernel<false, 16><<<1, PIVCHOL_THREADS, 0, s>>>(G, ldg, (int)g, X, piv, rank, scratch,
+                                                            scratch + (size_t)g * g);
   }
   POD_CHECK_LAUNCH("pivoted cholesky");
   {
@@ -474,3 +540,4 @@ extern "C" int pod_maxabs(const double* A, int64_t lda, int64_t p, int64_t q, do
   POD_CHECK_LAUNCH("maxabs");
   return POD_OK;
 }
+
