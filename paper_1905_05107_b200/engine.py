@@ -419,8 +419,10 @@ class IsmaEngine(MergeWorkspace):
         if not self.use_graphs or self.ctx.prof is not None or self.comm.active:
             self.round_ops(mode, cur, ub, pipelined, rowsrc)
             return
-        key = (mode, cur, ub, pipelined, rowsrc)
-        if self.graphs and self.graph_epoch != self.ctx.ws_epoch:
+        # graphs bake the matrix pointer into their launches: one set per A buffer
+        key = (self.A.t.data_ptr() + 8 * self.A.ld * self.A.col0, mode, cur, ub, pipelined,
+               rowsrc)
+        if self.graphs and (self.graph_epoch != self.ctx.ws_epoch or len(self.graphs) > 64):
             self.graphs.clear()  # a workspace was reallocated since these were captured
         gr = self.graphs.get(key)
         if gr is None:
@@ -601,25 +603,36 @@ class IsmaEngine(MergeWorkspace):
 
 
 _ENGINE_CACHE = {}
+ENGINE_CACHE_SIZE = 2  # per device: e.g. the two block widths of a column-block stream
 
 
 def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=0, m_total=None,
                w=0):
-    """Reuse the engine (buffers + captured round graphs) of the previous run
-    when the matrix buffer, shape and configuration match; one engine is
-    cached per device.  Graph replay reads A and the staged uniforms at
-    replay time, so a reused engine is valid for new contents of A."""
+    """Reuse an engine (buffers + captured round graphs) of an earlier run
+    when the matrix shape and configuration match (LRU, two per device).
+    The graphs are kept per matrix buffer (they bake its pointer in) and read
+    A and the staged uniforms at replay time, so a reused engine is valid for
+    new contents of a buffer it has seen."""
     world = 1 if comm is None else comm.world
-    key = (A.t.data_ptr() + 8 * A.ld * A.col0, A.m, A.ncols, A.ld, int(k), int(r), int(c),
-           criterion, bool(use_graphs), ctx.device.index, world, int(row_offset), m_total, int(w))
-    eng = _ENGINE_CACHE.get(ctx.device.index)
-    if eng is not None and eng.key == key:
-        eng.A = A
-        eng.reset()
-        return eng
-    _ENGINE_CACHE.pop(ctx.device.index, None)
-    eng = IsmaEngine(ctx, A, k=k, r=r, c=c, criterion=criterion, use_graphs=use_graphs,
-                     comm=comm, row_offset=row_offset, m_total=m_total, w=w)
+    key = (A.m, A.ncols, A.ld, int(k), int(r), int(c), criterion, bool(use_graphs),
+           ctx.device.index, world, int(row_offset), m_total, int(w))
+    lru = _ENGINE_CACHE.setdefault(ctx.device.index, [])
+    for i, eng in enumerate(lru):
+        if eng.key == key:
+            lru.append(lru.pop(i))  # most recently used last
+            eng.A = A
+            eng.reset()
+            return eng
+    while len(lru) >= ENGINE_CACHE_SIZE:
+        lru.pop(0)
+    try:
+        eng = IsmaEngine(ctx, A, k=k, r=r, c=c, criterion=criterion, use_graphs=use_graphs,
+                         comm=comm, row_offset=row_offset, m_total=m_total, w=w)
+    except torch.OutOfMemoryError:
+        lru.clear()  # cached engines hold their buffers: drop them and retry once
+        torch.cuda.empty_cache()
+        eng = IsmaEngine(ctx, A, k=k, r=r, c=c, criterion=criterion, use_graphs=use_graphs,
+                         comm=comm, row_offset=row_offset, m_total=m_total, w=w)
     eng.key = key
-    _ENGINE_CACHE[ctx.device.index] = eng
+    lru.append(eng)
     return eng

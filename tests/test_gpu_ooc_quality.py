@@ -123,3 +123,26 @@ def test_angles_match_oracle():
     ma = pod.mode_angles(fe, fx, 8)
     np.testing.assert_allclose(ma, np.degrees(np.arccos(np.clip(np.abs(np.sum(e * x, 0)), 0, 1))),
                                atol=1e-9)
+
+
+def test_duck_typed_reader_streams_like_block_reader(tmp_path):
+    """incremental_pod accepts any object with block_count / read_block
+    (ooc.py:105-148 duck typing); the prefetching stream gives the same
+    factor as the PODM BlockReader path."""
+    a = make_noisy_low_rank(120, 45, 4, np.random.default_rng(6), noise=0.05)
+    cfg = pod.IsmaConfig(k=4, c=12, tau=0.999, strategy="l2n", seed=2)
+
+    class ListReader:
+        def __init__(self, blocks):
+            self.blocks = list(blocks)
+            self.block_count = len(self.blocks)
+
+        def read_block(self):
+            return self.blocks.pop(0) if self.blocks else None
+
+    with pod.BlockReader(_podm(tmp_path, a), 3) as rd:
+        f1, t1 = pod.incremental_pod(rd, cfg)
+    f2, t2 = pod.incremental_pod(ListReader(orc.column_blocks(a, 3)), cfg)
+    assert [t.remaining for t in t1] == [t.remaining for t in t2]
+    np.testing.assert_array_equal(f1.sigma, f2.sigma)
+    np.testing.assert_array_equal(f1.u, f2.u)
