@@ -283,3 +283,19 @@ def test_pipelined_equals_unpipelined_bitwise():
     f1, t1 = pod.isma_run(a, cfg)  # numpy Generator -> pipelined
     f2, t2 = pod.isma_run(a, cfg, rng=Recorder(7))  # plain object -> not pipelined
     assert np.array_equal(f1.u, f2.u) and np.array_equal(f1.sigma, f2.sigma)
+
+
+def test_config3_proxy_matches_oracle():
+    """BASELINE config 3 generator (power-law rank 200 + noise) at proxy size
+    with config 3's k = 50, r = 150, c = 200: the 300-column E-SVD and the
+    200-column Gram eigensolve of the block-Jacobi solver, 192-column NN tiles,
+    against the oracle on the same seeded matrix."""
+    a = workloads.config3(seed=0, m=12000, n=1400)
+    cfg = pod.IsmaConfig(k=50, r=150, c=200, tau=1 - 1e-8, strategy="l2n", seed=7)
+    f, tr = pod.isma_run(a, cfg)
+    o = orc.run(a, 50, r=150, c=200, tau=1 - 1e-8, strategy="l2n", seed=7)
+    assert [t.remaining for t in tr] == [t["remaining"] for t in o["trace"]]
+    assert sigma_relerr(f.sigma, o["sigma"]) <= SIGMA_RTOL
+    assert principal_angles_sin(f.u, o["u"]).max() <= ANGLE_TOL_RAD
+    assert principal_angles_sin(f.v, o["v"]).max() <= ANGLE_TOL_RAD
+    f.validate(1e-10)
