@@ -31,6 +31,12 @@
 extern "C" {
 #endif
 
+/* operand storage types of the typed entry points (fp32 storage is converted
+ * exactly to fp64 inside the kernels: results equal the fp64 path on the
+ * upcast operand, as the reference's as_dense upcast, matcore.py:49) */
+#define POD_F64 0
+#define POD_F32 1
+
 #define POD_OK 0
 #define POD_EPARAM 2
 #define POD_EFORMAT 3
@@ -48,6 +54,10 @@ const char* pod_last_error(void);
  * (einsum "ij,ij->j").  nonfinite is set to 1 if any entry is NaN/Inf. */
 int pod_colnorms2_f64(const double* A, int64_t m, int64_t n, int64_t lda, double* norms2,
                       int32_t* nonfinite, void* stream);
+/* Same for a POD_F64 or POD_F32 stored A (fp64 accumulation of the exactly
+ * upcast values, as_dense's astype(float64), matcore.py:49). */
+int pod_colnorms2(int atype, const void* A, int64_t m, int64_t n, int64_t lda, double* norms2,
+                  int32_t* nonfinite, void* stream);
 
 /* Inverse-CDF draw with replacement + unique/counts + retirement.
  * Replaces sampling.py:204-222 (sample_with_replacement) together with the
@@ -76,9 +86,10 @@ int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n, const do
  * leverage scores of the top-k basis (sampling.py:190-201, div k); and the dedup-scaled row block
  * Y[i, :] = A[rows[i], cols] sqrt(cnt[i] / (w p[i])) (scale_sampled_rows,
  * sampling.py:248-258) for i < *hdev. */
-int pod_rownorms2(const double* X, int64_t m, int64_t ncols, int64_t ldx, const int32_t* cols,
-                  double div, const double* div_dev, double* out, void* stream);
-int pod_gather_scale_rows(const double* A, int64_t lda, const int32_t* cols, int64_t g,
+int pod_rownorms2(int xtype, const void* X, int64_t m, int64_t ncols, int64_t ldx,
+                  const int32_t* cols, double div, const double* div_dev, double* out,
+                  void* stream);
+int pod_gather_scale_rows(int atype, const void* A, int64_t lda, const int32_t* cols, int64_t g,
                           const int32_t* rows, const int64_t* cnt, const double* p, double w,
                           int64_t hcap, const int64_t* hdev, double* Y, int64_t ldy,
                           void* stream);
@@ -88,9 +99,10 @@ int pod_gather_scale_rows(const double* A, int64_t lda, const int32_t* cols, int
  * from pod_gemm_tn_f64), U m x r.  The residual is never materialised.
  * Replaces sampling.py:175-176 (residual_distribution, strategy "ort"). */
 size_t pod_resid_ws_bytes(int64_t m, int64_t n);
-int pod_resid_colnorms2(int64_t m, int64_t n, const double* A, int64_t lda, const int32_t* cols,
-                        const double* U, int64_t ldu, int64_t r, const double* C, int64_t ldc,
-                        double* out, void* ws, size_t ws_bytes, void* stream);
+int pod_resid_colnorms2(int atype, int64_t m, int64_t n, const void* A, int64_t lda,
+                        const int32_t* cols, const double* U, int64_t ldu, int64_t r,
+                        const double* C, int64_t ldc, double* out, void* ws, size_t ws_bytes,
+                        void* stream);
 
 /* Gates: every compute entry point below that takes `gate` (device int32,
  * nullable) does nothing when *gate == 0, so a round's launch sequence is
@@ -108,6 +120,12 @@ int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double*
                     const int32_t* xcols, const double* Y, int64_t ldy, const int32_t* ycols,
                     double* C, int64_t ldc, void* ws, size_t ws_bytes, const int32_t* gate,
                     void* stream);
+/* Typed operands: X and Y each stored as POD_F64 or POD_F32, exact fp64
+ * arithmetic on the upcast values; C fp64. */
+int pod_gemm_tn(int xtype, int ytype, int64_t m, int64_t p, int64_t q, double alpha,
+                const void* X, int64_t ldx, const int32_t* xcols, const void* Y, int64_t ldy,
+                const int32_t* ycols, double* C, int64_t ldc, void* ws, size_t ws_bytes,
+                const int32_t* gate, void* stream);
 
 /* Y (m x q) = alpha X T + beta Z, X m x p (optionally column-gathered),
  * T p x q small, q <= 192.  FP64 DMMA.8x8x4.  One CTA owns all q output
@@ -118,6 +136,11 @@ int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double*
                     const int32_t* xcols, const double* T, int64_t ldt, double beta,
                     const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* gate,
                     void* stream);
+/* Typed X (POD_F64 or POD_F32 storage, exact fp64 arithmetic); T, Z, Y fp64. */
+int pod_gemm_nn(int xtype, int64_t m, int64_t p, int64_t q, double alpha, const void* X,
+                int64_t ldx, const int32_t* xcols, const double* T, int64_t ldt, double beta,
+                const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* gate,
+                void* stream);
 
 /* Workspace (bytes) sufficient for any small solve of dimension <= n. */
 size_t pod_small_ws_bytes(int64_t n);

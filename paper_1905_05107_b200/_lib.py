@@ -34,20 +34,25 @@ SIGNATURES = {
     "pod_abi_version": (_i32, []),
     "pod_last_error": (ctypes.c_char_p, []),
     "pod_colnorms2_f64": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "pod_colnorms2": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "pod_draw_ws_bytes": (_sz, [_i64]),
     "pod_draw": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp, _f64,
                         _vp, _vp]),
-    "pod_rownorms2": (_i32, [_vp, _i64, _i64, _i64, _vp, _f64, _vp, _vp, _vp]),
-    "pod_gather_scale_rows": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _f64, _i64, _vp, _vp,
-                                     _i64, _vp]),
+    "pod_rownorms2": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _f64, _vp, _vp, _vp]),
+    "pod_gather_scale_rows": (_i32, [_i32, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _f64, _i64, _vp,
+                                     _vp, _i64, _vp]),
     "pod_resid_ws_bytes": (_sz, [_i64, _i64]),
-    "pod_resid_colnorms2": (_i32, [_i64, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64, _vp,
-                                   _vp, _sz, _vp]),
+    "pod_resid_colnorms2": (_i32, [_i32, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64,
+                                   _vp, _vp, _sz, _vp]),
     "pod_gemm_tn_ws_bytes": (_sz, [_i64, _i64, _i64]),
     "pod_gemm_tn_f64": (_i32, [_i64, _i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                                _vp, _sz, _vp, _vp]),
     "pod_gemm_nn_f64": (_i32, [_i64, _i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _f64, _vp, _i64,
                                _vp, _i64, _vp, _vp]),
+    "pod_gemm_tn": (_i32, [_i32, _i32, _i64, _i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _vp, _vp,
+                           _i64, _vp, _sz, _vp, _vp]),
+    "pod_gemm_nn": (_i32, [_i32, _i64, _i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _f64, _vp,
+                           _i64, _vp, _i64, _vp, _vp]),
     "pod_small_ws_bytes": (_sz, [_i64]),
     "pod_gram_eigh": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "pod_cholqr_factor": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp,

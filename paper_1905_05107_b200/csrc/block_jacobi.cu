@@ -816,6 +816,11 @@ template <typename K, typename... Args>
 static int launch(K kernel, int cl, int threads, size_t smem, cudaStream_t stream, Args... args) {
   int st = set_smem((const void*)kernel);
   if (st) return st;
+  if (cl > 8) {  // 16-CTA clusters are a non-portable size on sm_100a
+    cudaError_t e =
+        cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return cuda_status(e, "block jacobi cluster attr");
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cl, 1, 1);
   cfg.blockDim = dim3(threads, 1, 1);
@@ -869,6 +874,31 @@ int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, 
                   cudaStream_t stream) {
   if (!bj_enabled()) return BJ_NOT_APPLICABLE;
   const int n = (int)(l1 + l2);
+  {
+    // E too large for two blocks per CTA at 8 CTAs (2r > ~330): a 16-CTA
+    // cluster halves the block size
+    const bj::Geo g16(n, n, 0, 16);
+    const bj::Geo g8(n, n, 0, BJ_CL);
+    if (g8.smem_bytes(BJ_CL) > bj::SMEM_CAP && g16.smem_bytes(16) <= bj::SMEM_CAP) {
+      const size_t bytes = g16.smem_bytes(16);
+      const int tpp = bj::lanes_for(g16);
+      const int th = bj::threads_for(g16, tpp);
+      const int rpl = (g16.nrows + tpp - 1) / tpp;
+      if (th > 384) return BJ_NOT_APPLICABLE;
+#define BJ_L16(T_, R_) bj::launch(bj::merge_core_kernel<16, T_, R_>, 16, th, bytes, stream, sig1, (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new, info, 60)
+      if (tpp == 32) {
+        if (rpl <= 16) return BJ_L16(32, 16);
+        if (rpl <= 24) return BJ_L16(32, 24);
+        return BJ_L16(32, 0);
+      }
+      if (tpp == 16) {
+        if (rpl <= 24) return BJ_L16(16, 24);
+        return BJ_L16(16, 0);
+      }
+#undef BJ_L16
+      return BJ_NOT_APPLICABLE;
+    }
+  }
   const bj::Geo g(n, n, 0, BJ_CL);
   const size_t bytes = g.smem_bytes(BJ_CL);
   if (bytes > bj::SMEM_CAP || n < 2 * BJ_CL) return BJ_NOT_APPLICABLE;

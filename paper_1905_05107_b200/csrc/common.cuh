@@ -66,6 +66,18 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool val
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem),
                "r"(src_bytes));
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
+  unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int src_bytes = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(src_bytes));
+}
+// one element of T (float or double) with zero fill
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem, bool valid) {
+  if constexpr (sizeof(T) == 8) cp_async8(smem, gmem, valid);
+  else cp_async4(smem, gmem, valid);
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   unsigned saddr = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   int src_bytes = valid ? 16 : 0;

@@ -103,21 +103,28 @@ namespace tn {
 constexpr int BP = 64, BQ = 64, BK = 32, LDS = BK + 4;  // LDS % 16 == 4: conflict-free frags
 constexpr int THREADS = 256;
 constexpr int STAGES = 3;
-constexpr int TILE_DBL = BP * LDS;  // doubles per operand tile
-constexpr size_t SMEM = size_t(STAGES) * 2 * TILE_DBL * sizeof(double);
+constexpr int TILE_DBL = BP * LDS;  // elements per operand tile
+// operand tiles are stored in the operands' own type (fp32 storage is
+// converted exactly to fp64 at the fragment loads)
+template <typename TX, typename TY>
+constexpr size_t smem_bytes() {
+  return size_t(STAGES) * TILE_DBL * (sizeof(TX) + sizeof(TY));
+}
+constexpr size_t SMEM = smem_bytes<double, double>();
 
-__device__ __forceinline__ const double* colptr(const double* base, int64_t ld,
-                                                const int32_t* cols, int c) {
+template <typename T>
+__device__ __forceinline__ const T* colptr(const T* base, int64_t ld, const int32_t* cols, int c) {
   return base + (cols ? (int64_t)cols[c] : (int64_t)c) * ld;
 }
 
+template <typename TX, typename TY>
 __global__ void __launch_bounds__(THREADS) partial_kernel(
-    int64_t m, int p, int q, const double* __restrict__ X, int64_t ldx,
-    const int32_t* __restrict__ xcols, const double* __restrict__ Y, int64_t ldy,
+    int64_t m, int p, int q, const TX* __restrict__ X, int64_t ldx,
+    const int32_t* __restrict__ xcols, const TY* __restrict__ Y, int64_t ldy,
     const int32_t* __restrict__ ycols, int64_t rows_per_split, double* __restrict__ ws,
     const int32_t* __restrict__ gate, int sym) {
   if (gate && *gate == 0) return;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tiles_p = (p + BP - 1) / BP;
   int tp, tq;
   if (sym) {  // symmetric product (X == Y): upper-triangular tiles tp <= tq only
@@ -135,8 +142,8 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   // Each thread loads row (r + lane) of 8 columns per operand per stage.
-  const double* xp[8];
-  const double* yp[8];
+  const TX* xp[8];
+  const TY* yp[8];
   bool xv[8], yv[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -147,16 +154,18 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
     xp[i] = xv[i] ? colptr(X, ldx, xcols, cx) : X;
     yp[i] = yv[i] ? colptr(Y, ldy, ycols, cy) : Y;
   }
+  TX* const xs0 = reinterpret_cast<TX*>(smem_raw);
+  TY* const ys0 = reinterpret_cast<TY*>(smem_raw + size_t(STAGES) * TILE_DBL * sizeof(TX));
   auto load_stage = [&](int st, int64_t rb) {
-    double* xs = smem + (size_t)st * 2 * TILE_DBL;
-    double* ys = xs + TILE_DBL;
+    TX* xs = xs0 + (size_t)st * TILE_DBL;
+    TY* ys = ys0 + (size_t)st * TILE_DBL;
     const int64_t row = rb + lane;
     const bool rv = row < r1;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int c = warp + 8 * i;
-      cp_async8(xs + c * LDS + lane, xv[i] && rv ? xp[i] + row : X, xv[i] && rv);
-      cp_async8(ys + c * LDS + lane, yv[i] && rv ? yp[i] + row : Y, yv[i] && rv);
+      cp_async_elem(xs + c * LDS + lane, xv[i] && rv ? xp[i] + row : X, xv[i] && rv);
+      cp_async_elem(ys + c * LDS + lane, yv[i] && rv ? yp[i] + row : Y, yv[i] && rv);
     }
   };
 
@@ -179,17 +188,17 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
     cp_async_commit();
     cp_async_wait<STAGES - 1>();
     __syncthreads();
-    const double* xs = smem + (size_t)(kb % STAGES) * 2 * TILE_DBL;
-    const double* ys = xs + TILE_DBL;
+    const TX* xs = xs0 + (size_t)(kb % STAGES) * TILE_DBL;
+    const TY* ys = ys0 + (size_t)(kb % STAGES) * TILE_DBL;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       double a[4], b[2];
 #pragma unroll
       for (int f = 0; f < 4; ++f)
-        a[f] = xs[(wp * 32 + f * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+        a[f] = (double)xs[(wp * 32 + f * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
 #pragma unroll
       for (int g = 0; g < 2; ++g)
-        b[g] = ys[(wq * 16 + g * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+        b[g] = (double)ys[(wq * 16 + g * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
 #pragma unroll
       for (int f = 0; f < 4; ++f)
 #pragma unroll
@@ -496,34 +505,44 @@ constexpr int THREADS = 256;
 constexpr int BK = 16;
 constexpr int LDT = BK + 4;  // T chunk stored [j][k]
 
-template <int BN>
+template <int BN, typename TX = double>
 struct Cfg {
   static constexpr int STAGES = (BN == 128) ? 3 : 4;
   static constexpr int BM = (BN == 64) ? 128 : 64;  // rows per block (T reuse)
-  static constexpr int LDX = BM + 4;                // X chunk stored [k][row]
+  // X chunk stored [k][row] in X's own type (fp32 storage converted exactly
+  // at the fragment loads); padding keeps the fragment loads conflict-free
+  static constexpr int LDX = BM + (sizeof(TX) == 8 ? 4 : 8);
   static constexpr int WM = BM / 32;  // warps along M
   static constexpr int WN = 8 / WM;   // 4 warps along N
   static constexpr int FN = BN / WN / 8;
   static constexpr int XT = BK * LDX, TT = BN * LDT;
-  static constexpr size_t SMEM = size_t(STAGES) * (XT + TT) * sizeof(double);
+  static constexpr size_t XBYTES = size_t(XT) * sizeof(TX);  // multiple of 16
+  static constexpr size_t SMEM = size_t(STAGES) * (XBYTES + size_t(TT) * sizeof(double));
   static constexpr int PER_SM = (BN == 192) ? 1 : 2;
 };
 // blockIdx.y selects a group of BN output columns (q0 = blockIdx.y * BN); more
 // than one group only when Y aliases neither X nor Z (a group writes its
 // columns of a row block while another group may still be reading X there).
 
-template <int BN>
+template <int BN, typename TX = double>
 __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, double alpha,
-                                                  const double* X, int64_t ldx,
+                                                  const TX* X, int64_t ldx,
                                                   const int32_t* __restrict__ xcols,
                                                   const double* __restrict__ T, int64_t ldT,
                                                   double beta, const double* Z, int64_t ldz,
                                                   double* Y, int64_t ldy,
                                                   const int32_t* __restrict__ gate, int vx, int vt) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, TX>;
   constexpr int ST = C::STAGES;
   if (gate && *gate == 0) return;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto stage_x = [&](int st) {
+    return reinterpret_cast<TX*>(smem_raw + (size_t)st * (C::XBYTES + C::TT * sizeof(double)));
+  };
+  auto stage_t = [&](int st) {
+    return reinterpret_cast<double*>(smem_raw + (size_t)st * (C::XBYTES + C::TT * sizeof(double)) +
+                                     C::XBYTES);
+  };
   {
     const int q0 = blockIdx.y * BN;
     T += (int64_t)q0 * ldT;
@@ -544,8 +563,8 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
   int64_t l_r0 = (int64_t)blockIdx.x * C::BM;
   int l_kb = 0;
   auto load_stage = [&](int st) {
-    double* xs = smem + (size_t)st * (C::XT + C::TT);
-    double* ts = xs + C::XT;
+    TX* xs = stage_x(st);
+    double* ts = stage_t(st);
     const int k0 = l_kb * BK;
     const int64_t r0 = l_r0;
     if (++l_kb == nkb) {
@@ -563,13 +582,14 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
         col = xcols[c];
         cv = col >= 0;  // index -1: zero column
       }
-      double* dst = xs + cl * C::LDX + i2;
-      const double* src = X + col * ldx + row;
+      TX* dst = xs + cl * C::LDX + i2;
+      const TX* src = X + col * ldx + row;
       if (cv && vx && row + 1 < m) {
-        cp_async16(dst, src, true);
+        if constexpr (sizeof(TX) == 8) cp_async16(dst, src, true);
+        else cp_async8(dst, src, true);
       } else {
-        cp_async8(dst, cv && row < m ? src : X, cv && row < m);
-        cp_async8(dst + 1, cv && row + 1 < m ? src + 1 : X, cv && row + 1 < m);
+        cp_async_elem(dst, cv && row < m ? src : X, cv && row < m);
+        cp_async_elem(dst + 1, cv && row + 1 < m ? src + 1 : X, cv && row + 1 < m);
       }
     }
     // T: rows k0..k0+BK, all BN cols, k pairs
@@ -609,8 +629,8 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
 #pragma unroll
         for (int g = 0; g < C::FN; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
     }
-    const double* xs = smem + (size_t)st_c * (C::XT + C::TT);
-    const double* ts = xs + C::XT;
+    const TX* xs = stage_x(st_c);
+    const double* ts = stage_t(st_c);
     if (++st_c == ST) st_c = 0;
 
 #pragma unroll
@@ -618,7 +638,7 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
       double a[4], b[C::FN];
 #pragma unroll
       for (int f = 0; f < 4; ++f)
-        a[f] = xs[(kk * 4 + (lane & 3)) * C::LDX + wm * 32 + f * 8 + (lane >> 2)];
+        a[f] = (double)xs[(kk * 4 + (lane & 3)) * C::LDX + wm * 32 + f * 8 + (lane >> 2)];
 #pragma unroll
       for (int g = 0; g < C::FN; ++g)
         b[g] = ts[(wn * (BN / C::WN) + g * 8 + (lane >> 2)) * LDT + kk * 4 + (lane & 3)];
@@ -660,8 +680,20 @@ static bool nn_streamed_enabled() {
 }
 static int ensure_attrs() {
   if (g_attr_done) return POD_OK;
-  cudaError_t e = cudaFuncSetAttribute(tn::partial_kernel,
+  cudaError_t e = cudaFuncSetAttribute(tn::partial_kernel<double, double>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tn::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "tn attr");
+  e = cudaFuncSetAttribute(tn::partial_kernel<float, float>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tn::smem_bytes<float, float>());
+  if (e != cudaSuccess) return cuda_status(e, "tn attr");
+  e = cudaFuncSetAttribute(tn::partial_kernel<float, double>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tn::smem_bytes<float, double>());
+  if (e != cudaSuccess) return cuda_status(e, "tn attr");
+  e = cudaFuncSetAttribute(tn::partial_kernel<double, float>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tn::smem_bytes<double, float>());
   if (e != cudaSuccess) return cuda_status(e, "tn attr");
   e = cudaFuncSetAttribute(nn::kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)nn::Cfg<64>::SMEM);
@@ -687,6 +719,9 @@ static int ensure_attrs() {
   e = cudaFuncSetAttribute(nns::kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)nns::Cfg<192>::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "nns attr");
+  e = cudaFuncSetAttribute(nns::kernel<64, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)nns::Cfg<64, float>::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "nns attr");
   g_attr_done = true;
   return POD_OK;
 }
@@ -701,26 +736,41 @@ extern "C" size_t pod_gemm_tn_ws_bytes(int64_t m, int64_t p, int64_t q) {
   return (size_t)std::max(a.splits, b.splits) * p * q * sizeof(double);
 }
 
-extern "C" int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
-                               int64_t ldx, const int32_t* xcols, const double* Y, int64_t ldy,
-                               const int32_t* ycols, double* C, int64_t ldc, void* ws,
-                               size_t ws_bytes, const int32_t* gate, void* stream) {
-  POD_REQUIRE(m >= 0 && p >= 0 && q >= 0, "pod_gemm_tn_f64: negative size");
-  POD_REQUIRE(ldc >= p, "pod_gemm_tn_f64: ldc < p");
+extern "C" int pod_gemm_tn(int xtype, int ytype, int64_t m, int64_t p, int64_t q, double alpha,
+                           const void* X, int64_t ldx, const int32_t* xcols, const void* Y,
+                           int64_t ldy, const int32_t* ycols, double* C, int64_t ldc, void* ws,
+                           size_t ws_bytes, const int32_t* gate, void* stream) {
+  POD_REQUIRE(m >= 0 && p >= 0 && q >= 0, "pod_gemm_tn: negative size");
+  POD_REQUIRE(ldc >= p, "pod_gemm_tn: ldc < p");
+  POD_REQUIRE((xtype == POD_F64 || xtype == POD_F32) && (ytype == POD_F64 || ytype == POD_F32),
+              "pod_gemm_tn: bad operand type");
   if (p == 0 || q == 0) return POD_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  POD_REQUIRE(m > 0, "pod_gemm_tn_f64: m must be >= 1");
+  POD_REQUIRE(m > 0, "pod_gemm_tn: m must be >= 1");
   int st = ensure_attrs();
   if (st) return st;
-  const int sym = (X == Y && ldx == ldy && xcols == ycols && p == q) ? 1 : 0;
+  const int sym = (X == Y && ldx == ldy && xcols == ycols && p == q && xtype == ytype) ? 1 : 0;
   tn::Plan pl = tn::plan(m, p, q, sym != 0);
   POD_REQUIRE(ws_bytes >= (size_t)pl.splits * p * q * sizeof(double),
-              "pod_gemm_tn_f64: workspace too small (%zu < %zu)", ws_bytes,
+              "pod_gemm_tn: workspace too small (%zu < %zu)", ws_bytes,
               (size_t)pl.splits * p * q * sizeof(double));
   dim3 grid(pl.tiles, pl.splits);
-  tn::partial_kernel<<<grid, tn::THREADS, tn::SMEM, s>>>(m, (int)p, (int)q, X, ldx, xcols, Y, ldy,
-                                                         ycols, pl.rows_per_split, (double*)ws,
-                                                         gate, sym);
+  if (xtype == POD_F64 && ytype == POD_F64)
+    tn::partial_kernel<double, double><<<grid, tn::THREADS, tn::SMEM, s>>>(
+        m, (int)p, (int)q, (const double*)X, ldx, xcols, (const double*)Y, ldy, ycols,
+        pl.rows_per_split, (double*)ws, gate, sym);
+  else if (xtype == POD_F64)
+    tn::partial_kernel<double, float><<<grid, tn::THREADS, tn::smem_bytes<double, float>(), s>>>(
+        m, (int)p, (int)q, (const double*)X, ldx, xcols, (const float*)Y, ldy, ycols,
+        pl.rows_per_split, (double*)ws, gate, sym);
+  else if (ytype == POD_F32)
+    tn::partial_kernel<float, float><<<grid, tn::THREADS, tn::smem_bytes<float, float>(), s>>>(
+        m, (int)p, (int)q, (const float*)X, ldx, xcols, (const float*)Y, ldy, ycols,
+        pl.rows_per_split, (double*)ws, gate, sym);
+  else
+    tn::partial_kernel<float, double><<<grid, tn::THREADS, tn::smem_bytes<float, double>(), s>>>(
+        m, (int)p, (int)q, (const float*)X, ldx, xcols, (const double*)Y, ldy, ycols,
+        pl.rows_per_split, (double*)ws, gate, sym);
   POD_CHECK_LAUNCH("tn partial");
   int64_t tot = p * q;
   int blocks = (int)std::min<int64_t>(ceil_div(tot, 8), 16 * 148);  // 8 warps = 8 outputs per block
@@ -728,6 +778,52 @@ extern "C" int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
                                            ldc, gate, sym);
   POD_CHECK_LAUNCH("tn reduce");
   return POD_OK;
+}
+
+extern "C" int pod_gemm_tn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
+                               int64_t ldx, const int32_t* xcols, const double* Y, int64_t ldy,
+                               const int32_t* ycols, double* C, int64_t ldc, void* ws,
+                               size_t ws_bytes, const int32_t* gate, void* stream) {
+  return pod_gemm_tn(POD_F64, POD_F64, m, p, q, alpha, X, ldx, xcols, Y, ldy, ycols, C, ldc, ws,
+                     ws_bytes, gate, stream);
+}
+
+// X stored fp32 (exactly converted to fp64 inside): streamed kernel, column
+// groups of 64 (Y is fp64, so it never aliases X)
+static int gemm_nn_x32(int64_t m, int64_t p, int64_t q, double alpha, const float* X, int64_t ldx,
+                       const int32_t* xcols, const double* T, int64_t ldt, double beta,
+                       const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* gate,
+                       cudaStream_t s) {
+  using C = nns::Cfg<64, float>;
+  const int vx = ((reinterpret_cast<uintptr_t>(X) & 7) == 0) && (ldx % 2 == 0);
+  const int vt = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ldt % 2 == 0);
+  const int64_t nblk = ceil_div(m, C::BM);
+  const unsigned gy = (unsigned)ceil_div(q, 64);
+  const int64_t per = std::max<int64_t>(1, C::PER_SM * 148 / gy);
+  const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
+  nns::kernel<64, float><<<grid, nns::THREADS, C::SMEM, s>>>(m, (int)p, (int)q, alpha, X, ldx,
+                                                             xcols, T, ldt, beta, Z, ldz, Y, ldy,
+                                                             gate, vx, vt);
+  POD_CHECK_LAUNCH("nn streamed (fp32 X)");
+  return POD_OK;
+}
+
+extern "C" int pod_gemm_nn(int xtype, int64_t m, int64_t p, int64_t q, double alpha,
+                           const void* X, int64_t ldx, const int32_t* xcols, const double* T,
+                           int64_t ldt, double beta, const double* Z, int64_t ldz, double* Y,
+                           int64_t ldy, const int32_t* gate, void* stream) {
+  POD_REQUIRE(xtype == POD_F64 || xtype == POD_F32, "pod_gemm_nn: bad operand type");
+  if (xtype == POD_F64)
+    return pod_gemm_nn_f64(m, p, q, alpha, (const double*)X, ldx, xcols, T, ldt, beta, Z, ldz, Y,
+                           ldy, gate, stream);
+  POD_REQUIRE(m >= 0 && p >= 0 && q >= 0, "pod_gemm_nn: negative size");
+  if (m == 0 || q == 0) return POD_OK;
+  POD_REQUIRE(ldy >= m, "pod_gemm_nn: ldy < m");
+  POD_REQUIRE(beta == 0.0 || Z != nullptr, "pod_gemm_nn: beta != 0 needs Z");
+  int st = ensure_attrs();
+  if (st) return st;
+  return gemm_nn_x32(m, p, q, alpha, (const float*)X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy,
+                     gate, (cudaStream_t)stream);
 }
 
 extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double* X,

@@ -21,8 +21,9 @@ inline size_t smem_bytes(int r) {
          sizeof(double);
 }
 
+template <typename TA>
 __global__ void __launch_bounds__(THREADS) partial_kernel(
-    int64_t m, int n, int r, const double* __restrict__ A, int64_t lda,
+    int64_t m, int n, int r, const TA* __restrict__ A, int64_t lda,
     const int32_t* __restrict__ cols, const double* __restrict__ U, int64_t ldu,
     const double* __restrict__ Cm, int64_t ldcm, double* __restrict__ part) {
   extern __shared__ __align__(16) double sm[];
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
       double v = 0.0;
       if (j0 + j < n && row < c1) {
         const int64_t col = cols ? (int64_t)cols[j0 + j] : (int64_t)(j0 + j);
-        if (col >= 0) v = A[row + col * lda];
+        if (col >= 0) v = (double)A[row + col * lda];
       }
       as[j * LDA + i] = v;
     }
@@ -127,18 +128,22 @@ extern "C" size_t pod_resid_ws_bytes(int64_t m, int64_t n) {
   return (size_t)ceil_div(m, rsd::ROWS_PER_CTA) * n * sizeof(double) + 64;
 }
 
-extern "C" int pod_resid_colnorms2(int64_t m, int64_t n, const double* A, int64_t lda,
+extern "C" int pod_resid_colnorms2(int atype, int64_t m, int64_t n, const void* A, int64_t lda,
                                    const int32_t* cols, const double* U, int64_t ldu, int64_t r,
                                    const double* C, int64_t ldc, double* out, void* ws,
                                    size_t ws_bytes, void* stream) {
+  POD_REQUIRE(atype == POD_F64 || atype == POD_F32, "pod_resid_colnorms2: bad operand type");
   POD_REQUIRE(m >= 1 && n >= 1 && r >= 1 && r <= 256 && lda >= m && ldu >= m && ldc >= r,
               "pod_resid_colnorms2: bad shape");
   POD_REQUIRE(ws_bytes >= pod_resid_ws_bytes(m, n), "pod_resid_colnorms2: workspace too small");
   const size_t bytes = rsd::smem_bytes((int)r);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(rsd::partial_kernel,
+    cudaError_t e = cudaFuncSetAttribute(rsd::partial_kernel<double>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return cuda_status(e, "resid attr");
+    e = cudaFuncSetAttribute(rsd::partial_kernel<float>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return cuda_status(e, "resid attr");
     attr = true;
   }
@@ -146,8 +151,12 @@ extern "C" int pod_resid_colnorms2(int64_t m, int64_t n, const double* A, int64_
   cudaStream_t s = (cudaStream_t)stream;
   const int nchunk = (int)ceil_div(m, rsd::ROWS_PER_CTA);
   dim3 grid((unsigned)ceil_div(n, rsd::BN), (unsigned)nchunk);
-  rsd::partial_kernel<<<grid, rsd::THREADS, bytes, s>>>(m, (int)n, (int)r, A, lda, cols, U, ldu, C,
-                                                        ldc, (double*)ws);
+  if (atype == POD_F64)
+    rsd::partial_kernel<double><<<grid, rsd::THREADS, bytes, s>>>(
+        m, (int)n, (int)r, (const double*)A, lda, cols, U, ldu, C, ldc, (double*)ws);
+  else
+    rsd::partial_kernel<float><<<grid, rsd::THREADS, bytes, s>>>(
+        m, (int)n, (int)r, (const float*)A, lda, cols, U, ldu, C, ldc, (double*)ws);
   POD_CHECK_LAUNCH("resid partial");
   rsd::reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(nchunk, (int)n, (const double*)ws,
                                                                 out);

@@ -77,6 +77,44 @@ __global__ void __launch_bounds__(256) colnorms_warp_kernel(const double* __rest
   }
 }
 
+// fp32 storage: one CTA per column, float4 loads, fp64 accumulation of the
+// exactly upcast values (as_dense's astype(float64), matcore.py:49)
+__global__ void __launch_bounds__(256) colnorms_f32_kernel(const float* __restrict__ A, int64_t m,
+                                                           int64_t n, int64_t lda, int vec,
+                                                           double* __restrict__ out,
+                                                           int* __restrict__ nonfinite) {
+  __shared__ double red[8];
+  for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
+    const float* col = A + j * lda;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t done = 0;
+    if (vec) {
+      const float4* c4 = reinterpret_cast<const float4*>(col);
+      const int64_t m4 = m >> 2;
+      for (int64_t i = threadIdx.x; i < m4; i += 256) {
+        const float4 v = __ldcs(c4 + i);
+        s0 = fma((double)v.x, (double)v.x, s0);
+        s1 = fma((double)v.y, (double)v.y, s1);
+        s2 = fma((double)v.z, (double)v.z, s2);
+        s3 = fma((double)v.w, (double)v.w, s3);
+      }
+      done = m4 << 2;
+    }
+    for (int64_t i = done + threadIdx.x; i < m; i += 256) {
+      const double v = (double)col[i];
+      s0 = fma(v, v, s0);
+    }
+    double s = block_sum((s0 + s1) + (s2 + s3), red);
+    if (threadIdx.x == 0) out[j] = s;
+    if (!isfinite(s)) {
+      int bad = 0;
+      for (int64_t i = threadIdx.x; i < m; i += 256) bad |= !isfinite(col[i]);
+      bad = __syncthreads_or(bad);
+      if (bad && threadIdx.x == 0) atomicOr(nonfinite, 1);
+    }
+  }
+}
+
 // ------------------------------------------------------------ draw -------
 constexpr int DRAW_THREADS = 1024;
 
@@ -262,6 +300,23 @@ extern "C" int pod_colnorms2_f64(const double* A, int64_t m, int64_t n, int64_t 
   return POD_OK;
 }
 
+extern "C" int pod_colnorms2(int atype, const void* A, int64_t m, int64_t n, int64_t lda,
+                             double* norms2, int32_t* nonfinite, void* stream) {
+  POD_REQUIRE(atype == POD_F64 || atype == POD_F32, "pod_colnorms2: bad operand type");
+  if (atype == POD_F64)
+    return pod_colnorms2_f64((const double*)A, m, n, lda, norms2, nonfinite, stream);
+  POD_REQUIRE(m > 0 && n > 0 && lda >= m, "pod_colnorms2: bad shape m=%lld n=%lld lda=%lld",
+              (long long)m, (long long)n, (long long)lda);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s);
+  if (e != cudaSuccess) return cuda_status(e, "colnorms memset");
+  const int vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 4 == 0);
+  const int grid = (int)std::min<int64_t>(n, 148 * 64);
+  colnorms_f32_kernel<<<grid, 256, 0, s>>>((const float*)A, m, n, lda, vec, norms2, nonfinite);
+  POD_CHECK_LAUNCH("colnorms f32");
+  return POD_OK;
+}
+
 extern "C" size_t pod_draw_ws_bytes(int64_t n) {
   return (size_t)n * (sizeof(double) + sizeof(int32_t)) + 64;
 }
@@ -291,7 +346,8 @@ extern "C" int pod_draw(int mode, const double* weights, uint8_t* live, int64_t 
 namespace pod {
 // out[i] = (sum_j X[i, cols[j]]^2) / div (cols -1: zero column), one thread per
 // row; div = *div_dev when given (a graph-invariant launch with a per-round k)
-__global__ void rownorms2_kernel(const double* __restrict__ X, int64_t m, int ncols, int64_t ldx,
+template <typename TX>
+__global__ void rownorms2_kernel(const TX* __restrict__ X, int64_t m, int ncols, int64_t ldx,
                                  const int32_t* __restrict__ cols, double div,
                                  const double* __restrict__ div_dev, double* __restrict__ out) {
   if (div_dev) div = *div_dev;
@@ -301,7 +357,7 @@ __global__ void rownorms2_kernel(const double* __restrict__ X, int64_t m, int nc
     for (int j = 0; j < ncols; ++j) {
       const int64_t c = cols ? (int64_t)cols[j] : (int64_t)j;
       if (c < 0) continue;
-      const double v = X[i + c * ldx];
+      const double v = (double)X[i + c * ldx];
       s = fma(v, v, s);
     }
     out[i] = s / div;
@@ -309,7 +365,8 @@ __global__ void rownorms2_kernel(const double* __restrict__ X, int64_t m, int nc
 }
 
 // Y[i, j] = A[rows[i], cols[j]] * sqrt(cnt[i] / (w p[i])) for i < h (rows -1: zero)
-__global__ void gather_scale_rows_kernel(const double* __restrict__ A, int64_t lda,
+template <typename TA>
+__global__ void gather_scale_rows_kernel(const TA* __restrict__ A, int64_t lda,
                                          const int32_t* __restrict__ cols, int g,
                                          const int32_t* __restrict__ rows,
                                          const int64_t* __restrict__ cnt,
@@ -325,32 +382,43 @@ __global__ void gather_scale_rows_kernel(const double* __restrict__ A, int64_t l
     if (i < h) {
       const int64_t c = cols ? (int64_t)cols[j] : (int64_t)j;
       const int64_t r = rows[i];
-      if (c >= 0 && r >= 0) v = A[r + c * lda] * sqrt((double)cnt[i] / (w * p[i]));
+      if (c >= 0 && r >= 0) v = (double)A[r + c * lda] * sqrt((double)cnt[i] / (w * p[i]));
     }
     Y[i + (int64_t)j * ldy] = v;
   }
 }
 }  // namespace pod
 
-extern "C" int pod_rownorms2(const double* X, int64_t m, int64_t ncols, int64_t ldx,
+extern "C" int pod_rownorms2(int xtype, const void* X, int64_t m, int64_t ncols, int64_t ldx,
                              const int32_t* cols, double div, const double* div_dev, double* out,
                              void* stream) {
+  POD_REQUIRE(xtype == POD_F64 || xtype == POD_F32, "pod_rownorms2: bad operand type");
   POD_REQUIRE(m >= 1 && ncols >= 0 && ldx >= m, "pod_rownorms2: bad shape");
   const int grid = (int)std::min<int64_t>(ceil_div(m, 256), 148 * 16);
-  rownorms2_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(X, m, (int)ncols, ldx, cols, div,
-                                                                      div_dev, out);
+  if (xtype == POD_F64)
+    rownorms2_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const double*)X, m, (int)ncols, ldx, cols, div, div_dev, out);
+  else
+    rownorms2_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const float*)X, m, (int)ncols, ldx, cols, div, div_dev, out);
   POD_CHECK_LAUNCH("rownorms2");
   return POD_OK;
 }
 
-extern "C" int pod_gather_scale_rows(const double* A, int64_t lda, const int32_t* cols, int64_t g,
+extern "C" int pod_gather_scale_rows(int atype, const void* A, int64_t lda, const int32_t* cols,
+                                     int64_t g,
                                      const int32_t* rows, const int64_t* cnt, const double* p,
                                      double w, int64_t hcap, const int64_t* hdev, double* Y,
                                      int64_t ldy, void* stream) {
   POD_REQUIRE(g >= 1 && hcap >= 1 && ldy >= hcap, "pod_gather_scale_rows: bad shape");
   const int grid = (int)std::min<int64_t>(ceil_div(hcap * g, 256), 148 * 8);
-  gather_scale_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(A, lda, cols, (int)g, rows, cnt,
-                                                                     p, w, (int)hcap, hdev, Y, ldy);
+  POD_REQUIRE(atype == POD_F64 || atype == POD_F32, "pod_gather_scale_rows: bad operand type");
+  if (atype == POD_F64)
+    gather_scale_rows_kernel<double><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const double*)A, lda, cols, (int)g, rows, cnt, p, w, (int)hcap, hdev, Y, ldy);
+  else
+    gather_scale_rows_kernel<float><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        (const float*)A, lda, cols, (int)g, rows, cnt, p, w, (int)hcap, hdev, Y, ldy);
   POD_CHECK_LAUNCH("gather_scale_rows");
   return POD_OK;
 }

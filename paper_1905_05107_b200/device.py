@@ -33,9 +33,13 @@ def _gp(g):
     return ctypes.c_void_p(g.data_ptr())
 
 
+POD_F64, POD_F32 = 0, 1  # include/podsketch_b200.h operand storage types
+
+
 class ColMat:
-    """A column-major float64 device matrix: storage is a torch tensor of
-    shape (cols, ld) whose row j is column j; m <= ld logical rows."""
+    """A column-major device matrix (float64, or float32 storage for the data
+    matrix): storage is a torch tensor of shape (cols, ld) whose row j is
+    column j; m <= ld logical rows."""
 
     __slots__ = ("t", "m", "ncols", "ld", "col0")
 
@@ -58,7 +62,15 @@ class ColMat:
 
     @property
     def ptr(self):
-        return ctypes.c_void_p(self.t.data_ptr() + 8 * self.ld * self.col0)
+        return ctypes.c_void_p(self.t.data_ptr() + self.t.element_size() * self.ld * self.col0)
+
+    @property
+    def code(self):
+        return POD_F32 if self.t.dtype == torch.float32 else POD_F64
+
+    @property
+    def esize(self):
+        return self.t.element_size()
 
     def to_numpy(self, ncols=None):
         nc = self.ncols if ncols is None else ncols
@@ -139,8 +151,8 @@ class Ctx:
 
     # ------------------------------------------------------------ kernels
     def colnorms2(self, A, out, flag):
-        self._call("colnorms2", 1, 2.0 * A.m * A.ncols, 8.0 * A.m * A.ncols, "pod_colnorms2_f64", A.ptr, A.m, A.ncols, A.ld, _ptr(out), _ptr(flag),
-                  self.stream)
+        self._call("colnorms2", 1, 2.0 * A.m * A.ncols, A.esize * A.m * A.ncols, "pod_colnorms2",
+                   A.code, A.ptr, A.m, A.ncols, A.ld, _ptr(out), _ptr(flag), self.stream)
 
     def draw(self, mode, weights, live, n, uniforms, c, idx, cnt, info=None, thr=0.0, p_out=None):
         ws = self.ws("draw", _lib.load().pod_draw_ws_bytes(n))
@@ -150,20 +162,20 @@ class Ctx:
                    _ptr(p_out), self.stream)
 
     def rownorms2(self, X, ncols, out, cols=None, div=1.0, div_dev=None):
-        self._call("rownorms2", 1, 2.0 * X.m * ncols, 8.0 * X.m * ncols, "pod_rownorms2", X.ptr,
-                   X.m, ncols, X.ld, _ptr(cols), float(div), _ptr(div_dev), _ptr(out),
-                   self.stream)
+        self._call("rownorms2", 1, 2.0 * X.m * ncols, X.esize * X.m * ncols, "pod_rownorms2",
+                   X.code, X.ptr, X.m, ncols, X.ld, _ptr(cols), float(div), _ptr(div_dev),
+                   _ptr(out), self.stream)
 
     def gather_scale_rows(self, A, cols, g, rows, cnt, p, w, hcap, hdev, Y):
-        self._call("gather_scale_rows", 1, 0.0, 8.0 * hcap * g, "pod_gather_scale_rows", A.ptr,
-                   A.ld, _ptr(cols), g, _ptr(rows), _ptr(cnt), _ptr(p), float(w), hcap,
-                   _ptr(hdev), Y.ptr, Y.ld, self.stream)
+        self._call("gather_scale_rows", 1, 0.0, (A.esize + 8.0) * hcap * g,
+                   "pod_gather_scale_rows", A.code, A.ptr, A.ld, _ptr(cols), g, _ptr(rows),
+                   _ptr(cnt), _ptr(p), float(w), hcap, _ptr(hdev), Y.ptr, Y.ld, self.stream)
 
     def resid_colnorms2(self, A, n, U, r, C, ldc, out, cols=None):
         ws = self.ws("resid", _lib.load().pod_resid_ws_bytes(A.m, n))
-        self._call("resid_colnorms2", 2, 2.0 * A.m * n * r, 8.0 * A.m * (n + r),
-                   "pod_resid_colnorms2", A.m, n, A.ptr, A.ld, _ptr(cols), U.ptr, U.ld, r, C, ldc,
-                   _ptr(out), _ptr(ws), ws.numel(), self.stream)
+        self._call("resid_colnorms2", 2, 2.0 * A.m * n * r, A.m * (A.esize * n + 8.0 * r),
+                   "pod_resid_colnorms2", A.code, A.m, n, A.ptr, A.ld, _ptr(cols), U.ptr, U.ld,
+                   r, C, ldc, _ptr(out), _ptr(ws), ws.numel(), self.stream)
 
     def tn(self, p, q, alpha, X, Y, C, ldc, xcols=None, ycols=None, m=None, gate=None,
            tag="gemm_tn"):
@@ -174,21 +186,22 @@ class Ctx:
         ws = self.ws("tn", need)
         sym = X.ptr.value == Y.ptr.value and (xcols is ycols)
         flops = float(m) * p * (p + 1) if sym else 2.0 * m * p * q
-        nbytes = 8.0 * m * (p if sym else p + q)
+        nbytes = float(m) * (X.esize * p if sym else X.esize * p + Y.esize * q)
         self._call(tag if gate is None else tag + "[gated]", 2, flops, nbytes,
-                   "pod_gemm_tn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), Y.ptr, Y.ld,
-                  _ptr(ycols), C, ldc, _ptr(ws), ws.numel(), _gp(gate), self.stream)
+                   "pod_gemm_tn", X.code, Y.code, m, p, q, float(alpha), X.ptr, X.ld,
+                   _ptr(xcols), Y.ptr, Y.ld, _ptr(ycols), C, ldc, _ptr(ws), ws.numel(), _gp(gate),
+                   self.stream)
 
     def nn(self, p, q, alpha, X, T, ldt, Y, beta=0.0, Z=None, xcols=None, m=None, gate=None,
            tag="gemm_nn"):
         m = X.m if m is None else m
         if q == 0:
             return
-        nbytes = 8.0 * m * (p + q + (q if beta != 0.0 else 0))
+        nbytes = float(m) * (X.esize * p + 8.0 * (q + (q if beta != 0.0 else 0)))
         self._call(tag if gate is None else tag + "[gated]", 1, 2.0 * m * p * q, nbytes,
-                   "pod_gemm_nn_f64", m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), T, ldt,
-                  float(beta), Z.ptr if Z is not None else ctypes.c_void_p(0),
-                  Z.ld if Z is not None else 1, Y.ptr, Y.ld, _gp(gate), self.stream)
+                   "pod_gemm_nn", X.code, m, p, q, float(alpha), X.ptr, X.ld, _ptr(xcols), T,
+                   ldt, float(beta), Z.ptr if Z is not None else ctypes.c_void_p(0),
+                   Z.ld if Z is not None else 1, Y.ptr, Y.ld, _gp(gate), self.stream)
 
     def small_ws(self, n):
         return self.ws("small", _lib.load().pod_small_ws_bytes(n))
@@ -293,11 +306,13 @@ def get_ctx(device=None):
 
 
 def to_device_colmajor(a, device):
-    """Host array / torch tensor -> ColMat (column-major float64 on device).
+    """Host array / torch tensor -> ColMat (column-major on the device).
 
-    numpy input is made Fortran-ordered float64 (as_dense semantics,
-    matcore.py:49) and copied host->device; a CUDA tensor that is already
-    column-major float64 is used in place.
+    numpy input is made Fortran-ordered (as_dense semantics, matcore.py:49)
+    and copied host->device; float32 data keeps float32 storage (the kernels
+    upcast exactly, so results are those of the reference's float64 upcast),
+    everything else becomes float64.  A CUDA tensor that is already
+    column-major is used in place.
     """
     if isinstance(a, ColMat):
         return a
@@ -307,7 +322,7 @@ def to_device_colmajor(a, device):
 
             raise ParameterError(f"expected a 2-D matrix, got ndim={a.ndim}")
         m, n = a.shape
-        t = a.to(device=device, dtype=torch.float64)
+        t = a.to(device=device, dtype=torch.float32 if a.dtype == torch.float32 else torch.float64)
         if t.stride(0) == 1 and t.stride(1) == max(m, 1):
             st = t.T  # (n, m) contiguous view
         else:
@@ -315,7 +330,9 @@ def to_device_colmajor(a, device):
         return ColMat(st, m, n)
     arr = np.asarray(a)
     m, n = arr.shape
-    arr = np.asarray(arr, dtype=np.float64, order="F")
+    # float32 data stays float32 on the device (half the HBM); the kernels
+    # upcast exactly, so results equal the reference's as_dense float64 run
+    arr = np.asarray(arr, dtype=np.float32 if arr.dtype == np.float32 else np.float64, order="F")
     with warnings.catch_warnings():  # read-only inputs are only read (copied to the device)
         warnings.simplefilter("ignore", UserWarning)
         host = torch.from_numpy(arr.T)  # (n, m) C-contiguous view of F-order data

@@ -420,8 +420,7 @@ class IsmaEngine(MergeWorkspace):
             self.round_ops(mode, cur, ub, pipelined, rowsrc)
             return
         # graphs bake the matrix pointer into their launches: one set per A buffer
-        key = (self.A.t.data_ptr() + 8 * self.A.ld * self.A.col0, mode, cur, ub, pipelined,
-               rowsrc)
+        key = (self.A.ptr.value, self.A.code, mode, cur, ub, pipelined, rowsrc)
         if self.graphs and (self.graph_epoch != self.ctx.ws_epoch or len(self.graphs) > 64):
             self.graphs.clear()  # a workspace was reallocated since these were captured
         gr = self.graphs.get(key)
@@ -614,7 +613,7 @@ def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=
     A and the staged uniforms at replay time, so a reused engine is valid for
     new contents of a buffer it has seen."""
     world = 1 if comm is None else comm.world
-    key = (A.m, A.ncols, A.ld, int(k), int(r), int(c), criterion, bool(use_graphs),
+    key = (A.m, A.ncols, A.ld, A.code, int(k), int(r), int(c), criterion, bool(use_graphs),
            ctx.device.index, world, int(row_offset), m_total, int(w))
     lru = _ENGINE_CACHE.setdefault(ctx.device.index, [])
     for i, eng in enumerate(lru):

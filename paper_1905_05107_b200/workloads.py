@@ -14,6 +14,10 @@ Noise "N(0, x)" is read as variance x.
   cos/sin basis, so it is a GEMM on the device; ``side`` shrinks the grid
   for proxies.
 
+* ``config4`` -- the config-2 generator at 1024 x 1024 (m = 1,048,576),
+  n = 8192, stored float32 (the reference upcasts to float64 in as_dense;
+  the kernels upcast exactly, so the fp64 oracle on the upcast is the
+  parity reference).
 * ``config3`` -- power-law low-rank-plus-noise: A = U diag(i^-1.5) V^T +
   N(0, 1e-6), rank 200, m=1,000,000, n=20,000 (160 GB fp64), generated on
   the device.  U is Haar: G R^-1 with G ~ N(0,1) per 4096-row chunk and R the
@@ -34,6 +38,7 @@ import numpy as np
 CFG1 = dict(m=2000, n=500, k=10, r=30, c=50, tol=1e-8)
 CFG2 = dict(side=512, n=2000, k=20, r=60, c=100, tol=1e-8)
 CFG3 = dict(m=1_000_000, n=20_000, rank=200, k=50, r=150, c=200, tol=1e-8)
+CFG4 = dict(side=1024, n=8192, k=64, r=192, c=256, tol=1e-8)
 
 
 def config1(seed=0, m=2000, n=500, noise_var=1e-6):
@@ -63,7 +68,7 @@ NOISE_CHUNK = 4096  # rows per independently seeded noise chunk (shard-invariant
 
 
 def config2_torch(seed=0, side=512, n=2000, noise_var=1e-4, device="cpu", nmodes=40,
-                  rows=None):
+                  rows=None, dtype=None):
     """BASELINE config 2 snapshot matrix rows [r0, r1) (default: all m rows)
     as a column-major float64 torch tensor: storage (n, r1 - r0), i.e. the
     row block's transpose is contiguous.  The noise of global rows
@@ -84,7 +89,7 @@ def config2_torch(seed=0, side=512, n=2000, noise_var=1e-4, device="cpu", nmodes
     kx = torch.tensor(modes[:, 0], dtype=dt, device=device)
     ky = torch.tensor(modes[:, 1], dtype=dt, device=device)
     sd = math.sqrt(noise_var)
-    at = torch.empty((n, r1 - r0), dtype=dt, device=device)
+    at = torch.empty((n, r1 - r0), dtype=dt if dtype is None else dtype, device=device)
     # every quantity is computed per global 4096-row chunk (identical shapes
     # whatever the row partition), then the requested rows are sliced out
     for c in range(r0 // NOISE_CHUNK, (r1 + NOISE_CHUNK - 1) // NOISE_CHUNK):
@@ -104,10 +109,24 @@ def config2_torch(seed=0, side=512, n=2000, noise_var=1e-4, device="cpu", nmodes
     return at
 
 
-def config2(seed=0, side=512, n=2000, noise_var=1e-4):
+def config2(seed=0, side=512, n=2000, noise_var=1e-4, dtype=None):
     """Host (numpy, F-order) copy of ``config2_torch`` generated on the CPU."""
-    at = config2_torch(seed, side, n, noise_var, device="cpu")
+    at = config2_torch(seed, side, n, noise_var, device="cpu", dtype=dtype)
     return np.asfortranarray(at.numpy().T)
+
+
+def config4_torch(seed=0, side=1024, n=8192, noise_var=1e-4, device="cpu", rows=None):
+    """BASELINE config 4: the config-2 generator on a side x side grid
+    (1024 -> m = 1,048,576), n = 8192, STORED float32 (each 4096-row chunk is
+    generated in float64 and rounded once)."""
+    import torch
+
+    return config2_torch(seed, side, n, noise_var, device=device, rows=rows, dtype=torch.float32)
+
+
+def config4(seed=0, side=64, n=300, noise_var=1e-4):
+    """Host float32 (F-order) config-4 proxy made on the CPU."""
+    return np.asfortranarray(config4_torch(seed, side, n, noise_var, device="cpu").numpy().T)
 
 
 def _chunk_gen(device, seed, c, salt):

@@ -249,9 +249,10 @@ def test_graph_replay_matches_eager_bitwise():
 
 
 def test_large_rank_capacity_paths():
-    """r > 64 exercises the 128/192-column NN tiles and Jacobi on >128 columns."""
+    """r > 64 exercises the 128/192-column NN tiles and Jacobi on >128 columns
+    (the 384-column E of r = 192 runs on a 16-CTA cluster)."""
     a = workloads.config1(seed=3, m=3000, n=400)
-    for k, r in ((30, 90), (40, 160)):
+    for k, r in ((30, 90), (40, 160), (64, 192)):  # 2r = 384: 16-CTA block-Jacobi cluster
         cfg = pod.IsmaConfig(k=k, r=r, c=150, tau=0.999, strategy="l2n", seed=2)
         f, tr = pod.isma_run(a, cfg)
         o = orc.run(a, k, r=r, c=150, tau=0.999, strategy="l2n", seed=2)
@@ -299,3 +300,28 @@ def test_config3_proxy_matches_oracle():
     assert principal_angles_sin(f.u, o["u"]).max() <= ANGLE_TOL_RAD
     assert principal_angles_sin(f.v, o["v"]).max() <= ANGLE_TOL_RAD
     f.validate(1e-10)
+
+
+@pytest.mark.parametrize("strategy,rows", [("l2n", False), ("ort", False), ("ls", True)])
+def test_float32_storage_matches_fp64_oracle_on_upcast(strategy, rows):
+    """BASELINE config 4 semantics: A stored float32 on the device (half the
+    HBM); every kernel upcasts exactly, so the run equals the reference's
+    float64 run on the upcast matrix (as_dense, matcore.py:49) at the fp64
+    tolerances -- index sets included."""
+    a32 = workloads.config4(seed=3, side=64, n=300)
+    assert a32.dtype == np.float32
+    a64 = a32.astype(np.float64)
+    kw = dict(k=12, r=36, c=40, tau=1 - 1e-8, strategy=strategy, seed=5)
+    cfg = pod.IsmaConfig(rows=rows, w=300 if rows else None, **kw)
+    f32, t32 = pod.isma_run(a32, cfg)
+    f64, t64 = pod.isma_run(a64, cfg)
+    o = orc.run(a64, 12, r=36, c=40, tau=1 - 1e-8, strategy=strategy, seed=5, rows=rows,
+                w=300 if rows else None)
+    assert [t.remaining for t in t32] == [t["remaining"] for t in o["trace"]]
+    assert [t.remaining for t in t32] == [t.remaining for t in t64]
+    assert sigma_relerr(f32.sigma, o["sigma"]) <= (1e-8 if rows else SIGMA_RTOL)
+    assert principal_angles_sin(f32.u, o["u"]).max() <= (1e-6 if rows else ANGLE_TOL_RAD)
+    assert sigma_relerr(f32.sigma, f64.sigma) <= 1e-12
+    rep = pod.wedin_measure(a32, f32, 10)
+    rep64 = pod.wedin_measure(a64, f64, 10)
+    assert abs(rep.measure - rep64.measure) <= 1e-8 * max(1.0, abs(rep64.measure))

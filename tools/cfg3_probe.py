@@ -1,7 +1,8 @@
-"""Full-size BASELINE config 3 (1M x 20k fp64, 160 GB) on one B200: device
-generation, one timed isma_run, per-kernel breakdown of one round.
+"""Full-size BASELINE config 3 (1M x 20k fp64, 160 GB) or config 4 (config-2
+generator at 1024^2 x 8192, stored fp32, 34 GB) on one B200: device
+generation, timed isma_run, per-kernel breakdown.
 
-    python tools/cfg3_probe.py [--m 1000000] [--n 20000] [--criterion modes]
+    python tools/cfg3_probe.py [--config 3|4] [--m 1000000] [--n 20000] [--criterion modes]
 """
 
 import argparse
@@ -22,8 +23,9 @@ from paper_1905_05107_b200.device import ColMat  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--m", type=int, default=1_000_000)
-    ap.add_argument("--n", type=int, default=20_000)
+    ap.add_argument("--config", type=int, default=3, choices=[3, 4])
+    ap.add_argument("--m", type=int, default=None)
+    ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--criterion", default="modes")
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--runs", type=int, default=2)
@@ -32,12 +34,20 @@ def main():
     free, total = torch.cuda.mem_get_info(dev)
     print(f"mem free {free / 2**30:.1f} GiB of {total / 2**30:.1f} GiB", flush=True)
     t = time.perf_counter()
-    at = workloads.config3_torch(0, args.m, args.n, device=dev)
+    if args.config == 3:
+        args.m = args.m or 1_000_000
+        args.n = args.n or 20_000
+        at = workloads.config3_torch(0, args.m, args.n, device=dev)
+        kw = dict(k=50, r=150, c=200)
+    else:
+        side = int(round((args.m or 1 << 20) ** 0.5))
+        args.m, args.n = side * side, args.n or 8192
+        at = workloads.config4_torch(7, side, args.n, device=dev)
+        kw = dict(k=64, r=192, c=256)
     torch.cuda.synchronize()
-    print(f"generated {args.m}x{args.n} in {time.perf_counter() - t:.1f} s", flush=True)
+    print(f"generated {args.m}x{args.n} {at.dtype} in {time.perf_counter() - t:.1f} s", flush=True)
     A = ColMat(at, args.m)
-    cfg = pod.IsmaConfig(k=50, r=150, c=200, tau=1 - args.tol, strategy="l2n",
-                         criterion=args.criterion, seed=7)
+    cfg = pod.IsmaConfig(tau=1 - args.tol, strategy="l2n", criterion=args.criterion, seed=7, **kw)
     out = {}
     for i in range(args.runs):
         torch.cuda.synchronize()
