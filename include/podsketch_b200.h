@@ -142,6 +142,11 @@ int pod_gemm_nn(int xtype, int64_t m, int64_t p, int64_t q, double alpha, const 
                 const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* gate,
                 void* stream);
 
+/* Cap (in CTAs; 0 = none) on the grids of the TN / NN GEMMs launched while
+ * set -- host-side state read at launch (and so baked into captured graphs):
+ * the pipelined next-round update runs capped beside the critical merge. */
+int pod_set_grid_cap(int ctas);
+
 /* Workspace (bytes) sufficient for any small solve of dimension <= n. */
 size_t pod_small_ws_bytes(int64_t n);
 

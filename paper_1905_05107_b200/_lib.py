@@ -53,6 +53,7 @@ SIGNATURES = {
                            _i64, _vp, _sz, _vp, _vp]),
     "pod_gemm_nn": (_i32, [_i32, _i64, _i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _f64, _vp,
                            _i64, _vp, _i64, _vp, _vp]),
+    "pod_set_grid_cap": (_i32, [_i32]),
     "pod_small_ws_bytes": (_sz, [_i64]),
     "pod_gram_eigh": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "pod_cholqr_factor": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp,

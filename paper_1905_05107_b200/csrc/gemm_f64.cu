@@ -98,6 +98,14 @@ __device__ __forceinline__ void nn_epilogue(const double (&acc)[4][FN][2], int64
   }
 }
 
+// Grid cap for the persistent / split-K GEMMs launched while it is set
+// (pod_set_grid_cap): lets a concurrent, off-critical-path stream (the
+// pipelined update of the next round) leave SMs to the critical path.  0 = all.
+static int g_grid_cap = 0;
+static inline int64_t capped(int64_t ctas) {
+  return g_grid_cap > 0 ? std::max<int64_t>(1, std::min<int64_t>(ctas, g_grid_cap)) : ctas;
+}
+
 // ---------------------------------------------------------------- TN ------
 namespace tn {
 constexpr int BP = 64, BQ = 64, BK = 32, LDS = BK + 4;  // LDS % 16 == 4: conflict-free frags
@@ -254,7 +262,7 @@ inline Plan plan(int64_t m, int64_t p, int64_t q, bool sym) {
   Plan pl;
   const int64_t tp = ceil_div(p, BP);
   pl.tiles = (int)(sym ? tp * (tp + 1) / 2 : tp * ceil_div(q, BQ));
-  const int target = 2 * 148;  // 2 CTAs/SM (110 KB smem each): ONE wave, never a partial second
+  const int target = (int)capped(2 * 148);  // 2 CTAs/SM: ONE wave, never a partial second
   int64_t want = std::max<int64_t>(1, target / pl.tiles);
   int64_t max_by_rows = std::max<int64_t>(1, ceil_div(m, 4 * BK));  // >= 4 k-blocks per CTA
   int64_t splits = std::min<int64_t>(want, max_by_rows);
@@ -464,11 +472,18 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
     cp_async_wait<1>();
     __syncthreads();
     const double* xs = buf ? xs1 : xs0;
+    const int64_t row0 = rb * BM + wm * 32;
     double acc[4][C::FN][2];
 #pragma unroll
     for (int f = 0; f < 4; ++f)
 #pragma unroll
       for (int g = 0; g < C::FN; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+    // beta Z of this block: loads in flight under the block's DMMAs (BN = 64:
+    // 16 doubles per thread; wider tiles load in the epilogue)
+    double zv[4][BN == 64 ? C::FN : 1][2];
+    if constexpr (BN == 64) {
+      if (beta != 0.0) nn_load_z<C::FN>(zv, row0, wn * (BN / C::WN), lane, m, q, Z, ldz);
+    }
 #pragma unroll 2
     for (int k0 = 0; k0 < KP; k0 += 4) {
       double a[4], b[C::FN];
@@ -484,8 +499,10 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
         for (int g = 0; g < C::FN; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
     }
     __syncthreads();  // xs fully consumed before the next prefetch overwrites it
-    const int64_t row0 = rb * BM + wm * 32;
-    nn_epilogue<C::FN>(acc, row0, wn * (BN / C::WN), lane, m, q, alpha, beta, Z, ldz, Y, ldy);
+    if constexpr (BN == 64)
+      nn_store<C::FN>(acc, zv, row0, wn * (BN / C::WN), lane, m, q, alpha, beta, Y, ldy);
+    else
+      nn_epilogue<C::FN>(acc, row0, wn * (BN / C::WN), lane, m, q, alpha, beta, Z, ldz, Y, ldy);
     buf ^= 1;
   }
   cp_async_wait<0>();
@@ -799,7 +816,7 @@ static int gemm_nn_x32(int64_t m, int64_t p, int64_t q, double alpha, const floa
   const int vt = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ldt % 2 == 0);
   const int64_t nblk = ceil_div(m, C::BM);
   const unsigned gy = (unsigned)ceil_div(q, 64);
-  const int64_t per = std::max<int64_t>(1, C::PER_SM * 148 / gy);
+  const int64_t per = std::max<int64_t>(1, capped(C::PER_SM * 148) / gy);
   const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
   nns::kernel<64, float><<<grid, nns::THREADS, C::SMEM, s>>>(m, (int)p, (int)q, alpha, X, ldx,
                                                              xcols, T, ldt, beta, Z, ldz, Y, ldy,
@@ -845,7 +862,7 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
       const int vec16 = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && (ldx % 2 == 0);
       const int per_sm = bytes <= 110 * 1024 ? 2 : 1;
       const int64_t nblk = ceil_div(m, nnp::BM);
-      const unsigned grid = (unsigned)std::min<int64_t>(nblk, (int64_t)per_sm * 148);
+      const unsigned grid = (unsigned)std::min<int64_t>(nblk, capped((int64_t)per_sm * 148));
       if (bn == 64)
         nnp::kernel<64><<<grid, nnp::THREADS, bytes, s>>>(m, (int)p, (int)q, alpha, X, ldx, xcols,
                                                           T, ldt, beta, Z, ldz, Y, ldy, gate, vec16);
@@ -876,18 +893,18 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
     if (q <= 64 || (!alias && nn_groups_enabled())) {
       const int64_t nblk = ceil_div(m, nns::Cfg<64>::BM);
       const unsigned gy = (unsigned)ceil_div(q, 64);
-      const int64_t per = std::max<int64_t>(1, nns::Cfg<64>::PER_SM * 148 / gy);
+      const int64_t per = std::max<int64_t>(1, capped(nns::Cfg<64>::PER_SM * 148) / gy);
       const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
       nns::kernel<64><<<grid, nns::THREADS, nns::Cfg<64>::SMEM, s>>>(
           m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
     } else if (q <= 128) {
       const int64_t nblk = ceil_div(m, nns::Cfg<128>::BM);
-      const unsigned grid = (unsigned)std::min<int64_t>(nblk, nns::Cfg<128>::PER_SM * 148);
+      const unsigned grid = (unsigned)std::min<int64_t>(nblk, capped(nns::Cfg<128>::PER_SM * 148));
       nns::kernel<128><<<grid, nns::THREADS, nns::Cfg<128>::SMEM, s>>>(
           m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
     } else {
       const int64_t nblk = ceil_div(m, nns::Cfg<192>::BM);
-      const unsigned grid = (unsigned)std::min<int64_t>(nblk, nns::Cfg<192>::PER_SM * 148);
+      const unsigned grid = (unsigned)std::min<int64_t>(nblk, capped(nns::Cfg<192>::PER_SM * 148));
       nns::kernel<192><<<grid, nns::THREADS, nns::Cfg<192>::SMEM, s>>>(
           m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
     }
@@ -909,5 +926,11 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
         m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate);
   }
   POD_CHECK_LAUNCH("nn");
+  return POD_OK;
+}
+
+extern "C" int pod_set_grid_cap(int ctas) {
+  POD_REQUIRE(ctas >= 0, "pod_set_grid_cap: negative cap");
+  pod::g_grid_cap = ctas;
   return POD_OK;
 }

@@ -37,10 +37,16 @@ import time
 import numpy as np
 import torch
 
+from . import _lib
 from .device import ColMat, dptr
 from .errors import DegenerateDistributionError, ParameterError
 
 REORTH_TOL = 1e-8  # merge.py:34
+# CTAs of the pipelined update's GEMMs (which run beside the merge chain on
+# the side stream); 0 = no cap.  POD_UPDATE_GRID_CAP overrides.
+# (measured: caps of 148-200 CTAs and forking the update at the round start
+# instead of after the merge's GEMM phase are within noise or slower)
+UPDATE_GRID_CAP = int(__import__("os").environ.get("POD_UPDATE_GRID_CAP", "0"))
 CHOLQR_PASSES = 4  # pass 0 always; passes 1..3 gated on the previous pass
 
 MODE_L2N, MODE_UNIFORM, MODE_WEIGHTS, MODE_ORT, MODE_ROWS = 0, 1, 2, 3, 4
@@ -156,9 +162,10 @@ class MergeWorkspace:
                            dptr(self.Rtmp), r, gate=gp)
             ctx.small_copy(l, l, dptr(self.Rtmp), r, dptr(Rout), r, gate=gp)
 
-    def merge_ops(self, cur, ub=0):
+    def merge_ops(self, cur, ub=0, before_core=None):
         """block_merge (merge.py:37-91) of stack `cur` (U1, sig[cur]) with
-        update slot `ub` (Uupd, sig_upd) into stack 1 - cur, at capacity r."""
+        update slot `ub` (Uupd, sig_upd) into stack 1 - cur, at capacity r.
+        `before_core` is issued after the GEMM phase, before the E-SVD."""
         ctx, r = self.ctx, self.r
         S, Snext = self.S[cur], self.S[1 - cur]
         U1 = S.cols(0, r)
@@ -183,6 +190,8 @@ class MergeWorkspace:
         ctx.small_gemm(r, r, r, 1.0, dptr(self.Rt2), r, 0, dptr(self.Rt), r, 0.0,
                        dptr(self.Rtmp), r, gate=gl)
         ctx.small_copy(r, r, dptr(self.Rtmp), r, dptr(self.Rt), r, gate=gl)
+        if before_core is not None:
+            before_core()
         ctx.merge_core(dptr(self.sig[cur]), r, dptr(self.M), r, dptr(self.Rt), r,
                        dptr(sig_upd), r, r, r, dptr(self.Tm), 2 * r, r,
                        dptr(self.sig[1 - cur]), info=self.rec[0, REC_KEEP:])  # merge.py:80-85
@@ -394,25 +403,33 @@ class IsmaEngine(MergeWorkspace):
         main = torch.cuda.current_stream(self.ctx.device)
         self.side.wait_stream(main)
         self.ctx.ws_suffix = "_upd"
+        lib = _lib.load()
+        lib.pod_set_grid_cap(UPDATE_GRID_CAP)  # leave SMs to the concurrent merge
         try:
             with torch.cuda.stream(self.side):
                 self.update_ops(mode, b, self.Uupd_b[b].cols(0, self.r))
         finally:
+            lib.pod_set_grid_cap(0)
             self.ctx.ws_suffix = ""
         if join:
             main.wait_stream(self.side)
 
     def round_ops(self, mode, cur, ub, pipelined, rowsrc=None):
         """Round t: merge(t) with update buffer ub (+ cosines, readback);
-        pipelined: update(t+1) into buffer 1 - ub concurrently."""
+        pipelined: update(t+1) into buffer 1 - ub on the side stream, forked
+        after merge(t)'s GEMM phase so that its GEMMs and eigensolver overlap
+        merge(t)'s latency-bound E-SVD (8-16 SMs) instead of competing with
+        merge(t)'s full-GPU GEMMs."""
         if pipelined:
-            self.update_side_ops(mode, 1 - ub, join=False)  # update(t+1) || merge(t)
-        else:
-            self.update_ops(mode, ub, self.Uupd_b[ub].cols(0, self.r), cur=cur, rowsrc=rowsrc)
+            self.merge_ops(cur, ub, before_core=lambda: self.update_side_ops(mode, 1 - ub,
+                                                                             join=False))
+            self.cosines_ops(cur, 1 - cur)
+            torch.cuda.current_stream(self.ctx.device).wait_stream(self.side)
+            self.readback()
+            return
+        self.update_ops(mode, ub, self.Uupd_b[ub].cols(0, self.r), cur=cur, rowsrc=rowsrc)
         self.merge_ops(cur, ub)
         self.cosines_ops(cur, 1 - cur)
-        if pipelined:
-            torch.cuda.current_stream(self.ctx.device).wait_stream(self.side)
         self.readback()
 
     def launch_round(self, mode, cur, ub, pipelined, rowsrc=None):
