@@ -1,6 +1,8 @@
 """GPU parity of the one-pass incremental driver (ooc.py:105-148) and the
 quality metrics (quality.py:38-118) against reference goldens and the oracle."""
 
+import os
+
 import numpy as np
 import pytest
 from conftest import load_golden, make_low_rank, make_noisy_low_rank
@@ -146,3 +148,19 @@ def test_duck_typed_reader_streams_like_block_reader(tmp_path):
     assert [t.remaining for t in t1] == [t.remaining for t in t2]
     np.testing.assert_array_equal(f1.sigma, f2.sigma)
     np.testing.assert_array_equal(f1.u, f2.u)
+
+
+def test_truncated_file_raises_at_its_block(tmp_path):
+    """A PODM payload cut inside block 3 of 4: the read-ahead stream surfaces
+    the reference's FormatError (byte offset in the message) when that block
+    is requested, after blocks 1-2 were read."""
+    a = make_noisy_low_rank(64, 40, 3, np.random.default_rng(12), noise=0.05)
+    path = _podm(tmp_path, a)
+    size = os.path.getsize(path)
+    with open(path, "r+b") as fh:
+        fh.truncate(size - 8 * 64 * 12)  # inside the third block (columns 20..29)
+    cfg = pod.IsmaConfig(k=3, c=10, tau=0.99, strategy="l2n", seed=1)
+    with pod.BlockReader(path, 4) as rd:
+        with pytest.raises(pod.FormatError, match="byte offset"):
+            pod.incremental_pod(rd, cfg)
+        assert rd.blocks_read == 2
