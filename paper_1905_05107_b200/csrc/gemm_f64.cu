@@ -274,6 +274,151 @@ inline Plan plan(int64_t m, int64_t p, int64_t q, bool sym) {
 }
 }  // namespace tn
 
+// ----------------------------------------------------------- TN (80) -----
+// 80 x 80 output tiles (10 x 10 fragments) for operand widths where 64-wide
+// tiles pad badly (r = 150 -> 160 instead of 192, n = 2000 exactly).  10 warps
+// (5 along p x 2 along q), warp tile 16 x 40 (2 x 5 fragments), BK = 16 so two
+// CTAs fit an SM; gathered column offsets live in shared memory instead of
+// per-thread pointer registers.
+namespace tn80 {
+constexpr int T = 80, NW = 10, THREADS = NW * 32;
+constexpr int BK = 16, LDS = BK + 4;  // % 16 == 4: conflict-free fragments
+constexpr int STAGES = 4;
+constexpr int TILE = T * LDS;
+template <typename TX, typename TY>
+constexpr size_t smem_bytes() {
+  return size_t(STAGES) * TILE * (sizeof(TX) + sizeof(TY)) + 2 * T * sizeof(int64_t);
+}
+
+template <typename TX, typename TY>
+__global__ void __launch_bounds__(THREADS, 2) partial_kernel(
+    int64_t m, int p, int q, const TX* __restrict__ X, int64_t ldx,
+    const int32_t* __restrict__ xcols, const TY* __restrict__ Y, int64_t ldy,
+    const int32_t* __restrict__ ycols, int64_t rows_per_split, double* __restrict__ ws,
+    const int32_t* __restrict__ gate, int sym) {
+  if (gate && *gate == 0) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tiles_p = (p + T - 1) / T;
+  int tp, tq;
+  if (sym) {
+    int t = blockIdx.x;
+    tq = 0;
+    while (t > tq) { t -= tq + 1; ++tq; }
+    tp = t;
+  } else {
+    tp = blockIdx.x % tiles_p;
+    tq = blockIdx.x / tiles_p;
+  }
+  const int split = blockIdx.y;
+  const int64_t r0 = (int64_t)split * rows_per_split;
+  const int64_t r1 = min(m, r0 + rows_per_split);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  TX* const xs0 = reinterpret_cast<TX*>(smem_raw);
+  TY* const ys0 = reinterpret_cast<TY*>(smem_raw + size_t(STAGES) * TILE * sizeof(TX));
+  int64_t* const xoff = reinterpret_cast<int64_t*>(smem_raw + size_t(STAGES) * TILE *
+                                                                  (sizeof(TX) + sizeof(TY)));
+  int64_t* const yoff = xoff + T;
+  for (int c = threadIdx.x; c < 2 * T; c += THREADS) {
+    const bool isx = c < T;
+    const int cc = isx ? c : c - T;
+    const int gc = (isx ? tp : tq) * T + cc;
+    const int32_t* cols = isx ? xcols : ycols;
+    int64_t off = -1;
+    if (gc < (isx ? p : q)) {
+      const int64_t col = cols ? (int64_t)cols[gc] : (int64_t)gc;
+      if (col >= 0) off = col * (isx ? ldx : ldy);  // index -1: zero column
+    }
+    (isx ? xoff : yoff)[cc] = off;
+  }
+  __syncthreads();
+  // loader: warp w moves rows rb + lane of columns w, w + 10, ... (8 each)
+  auto load_stage = [&](int st, int64_t rb) {
+    TX* xs = xs0 + (size_t)st * TILE;
+    TY* ys = ys0 + (size_t)st * TILE;
+    const int64_t row = rb + (lane & 15);
+    const bool rv = row < r1;
+    const int half = lane >> 4;  // lanes 0-15 / 16-31: two columns per instruction
+#pragma unroll
+    for (int i = 0; i < T / NW / 2; ++i) {
+      const int c = warp + NW * (2 * i + half);
+      const int64_t ox = xoff[c], oy = yoff[c];
+      cp_async_elem(xs + c * LDS + (lane & 15), ox >= 0 && rv ? X + ox + row : X, ox >= 0 && rv);
+      cp_async_elem(ys + c * LDS + (lane & 15), oy >= 0 && rv ? Y + oy + row : Y, oy >= 0 && rv);
+    }
+  };
+  const int wp = warp % 5, wq = warp / 5;  // warp tile: 16 (p) x 40 (q)
+  double acc[2][5][2];
+#pragma unroll
+  for (int f = 0; f < 2; ++f)
+#pragma unroll
+    for (int g = 0; g < 5; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+  const int64_t nkb = (r1 > r0) ? (r1 - r0 + BK - 1) / BK : 0;
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nkb) load_stage(st, r0 + (int64_t)st * BK);
+    cp_async_commit();
+  }
+  for (int64_t kb = 0; kb < nkb; ++kb) {
+    const int64_t nxt = kb + STAGES - 1;
+    if (nxt < nkb) load_stage((int)(nxt % STAGES), r0 + nxt * BK);
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    __syncthreads();
+    const TX* xs = xs0 + (size_t)(kb % STAGES) * TILE;
+    const TY* ys = ys0 + (size_t)(kb % STAGES) * TILE;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double a[2], b[5];
+#pragma unroll
+      for (int f = 0; f < 2; ++f)
+        a[f] = (double)xs[(wp * 16 + f * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+#pragma unroll
+      for (int g = 0; g < 5; ++g)
+        b[g] = (double)ys[(wq * 40 + g * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+#pragma unroll
+      for (int f = 0; f < 2; ++f)
+#pragma unroll
+        for (int g = 0; g < 5; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+  double* out = ws + (size_t)split * p * q;
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int i = tp * T + wp * 16 + f * 8 + (lane >> 2);
+#pragma unroll
+    for (int g = 0; g < 5; ++g)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = tq * T + wq * 40 + g * 8 + 2 * (lane & 3) + e;
+        if (i < p && j < q) out[(size_t)j * p + i] = acc[f][g][e];
+      }
+  }
+}
+
+inline tn::Plan plan(int64_t m, int64_t p, int64_t q, bool sym) {
+  tn::Plan pl;
+  const int64_t tp = ceil_div(p, T);
+  pl.tiles = (int)(sym ? tp * (tp + 1) / 2 : tp * ceil_div(q, T));
+  const int target = (int)capped(2 * 148);
+  int64_t want = std::max<int64_t>(1, target / pl.tiles);
+  int64_t max_by_rows = std::max<int64_t>(1, ceil_div(m, 4 * BK));
+  int64_t splits = std::min<int64_t>(want, max_by_rows);
+  splits = std::max<int64_t>(1, std::min<int64_t>(splits, 65535));
+  pl.rows_per_split = ceil_div(ceil_div(m, splits), BK) * BK;
+  if (pl.rows_per_split == 0) pl.rows_per_split = BK;
+  pl.splits = (int)std::max<int64_t>(1, ceil_div(m, pl.rows_per_split));
+  return pl;
+}
+// 80-wide tiles when they cover p x q with less padding than 64-wide ones
+inline bool better(int64_t p, int64_t q) {
+  const int64_t a64 = ceil_div(p, 64) * 64 * ceil_div(q, 64) * 64;
+  const int64_t a80 = ceil_div(p, 80) * 80 * ceil_div(q, 80) * 80;
+  return a80 * 10 < a64 * 9;  // at least 10 % less padded work
+}
+}  // namespace tn80
+
 // ---------------------------------------------------------------- NN ------
 // One CTA owns BM rows x ALL q (<= BN) output columns, so Y may alias X or Z
 // (each CTA reads its own rows completely before writing them).
@@ -677,6 +822,15 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
 }  // namespace nns
 
 static bool g_attr_done = false;
+// POD_TN80=0 disables the 80-wide TN tiles (A/B measurements)
+static bool tn80_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_TN80");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 // POD_NN_GROUPS=0 disables column groups in the streamed NN kernel (A/B)
 static bool nn_groups_enabled() {
   static int v = -1;
@@ -712,6 +866,16 @@ static int ensure_attrs() {
                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tn::smem_bytes<double, float>());
   if (e != cudaSuccess) return cuda_status(e, "tn attr");
+#define TN80_ATTR(A_, B_)                                                                   \
+  e = cudaFuncSetAttribute(tn80::partial_kernel<A_, B_>,                                   \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                           (int)tn80::smem_bytes<A_, B_>());                               \
+  if (e != cudaSuccess) return cuda_status(e, "tn80 attr");
+  TN80_ATTR(double, double)
+  TN80_ATTR(float, float)
+  TN80_ATTR(float, double)
+  TN80_ATTR(double, float)
+#undef TN80_ATTR
   e = cudaFuncSetAttribute(nn::kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)nn::Cfg<64>::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "nn attr");
@@ -750,7 +914,9 @@ using namespace pod;
 extern "C" size_t pod_gemm_tn_ws_bytes(int64_t m, int64_t p, int64_t q) {
   if (m <= 0 || p <= 0 || q <= 0) return 0;
   const tn::Plan a = tn::plan(m, p, q, false), b = tn::plan(m, p, q, p == q);
-  return (size_t)std::max(a.splits, b.splits) * p * q * sizeof(double);
+  const tn::Plan c = tn80::plan(m, p, q, false), d = tn80::plan(m, p, q, p == q);
+  const int sp = std::max(std::max(a.splits, b.splits), std::max(c.splits, d.splits));
+  return (size_t)sp * p * q * sizeof(double);
 }
 
 extern "C" int pod_gemm_tn(int xtype, int ytype, int64_t m, int64_t p, int64_t q, double alpha,
@@ -767,12 +933,23 @@ extern "C" int pod_gemm_tn(int xtype, int ytype, int64_t m, int64_t p, int64_t q
   int st = ensure_attrs();
   if (st) return st;
   const int sym = (X == Y && ldx == ldy && xcols == ycols && p == q && xtype == ytype) ? 1 : 0;
-  tn::Plan pl = tn::plan(m, p, q, sym != 0);
+  const bool w80 = tn80::better(p, q) && tn80_enabled();
+  tn::Plan pl = w80 ? tn80::plan(m, p, q, sym != 0) : tn::plan(m, p, q, sym != 0);
   POD_REQUIRE(ws_bytes >= (size_t)pl.splits * p * q * sizeof(double),
               "pod_gemm_tn: workspace too small (%zu < %zu)", ws_bytes,
               (size_t)pl.splits * p * q * sizeof(double));
   dim3 grid(pl.tiles, pl.splits);
-  if (xtype == POD_F64 && ytype == POD_F64)
+  if (w80) {
+#define TN80_LAUNCH(A_, B_)                                                                     \
+  tn80::partial_kernel<A_, B_><<<grid, tn80::THREADS, tn80::smem_bytes<A_, B_>(), s>>>(        \
+      m, (int)p, (int)q, (const A_*)X, ldx, xcols, (const B_*)Y, ldy, ycols, pl.rows_per_split, \
+      (double*)ws, gate, sym)
+    if (xtype == POD_F64 && ytype == POD_F64) TN80_LAUNCH(double, double);
+    else if (xtype == POD_F64) TN80_LAUNCH(double, float);
+    else if (ytype == POD_F32) TN80_LAUNCH(float, float);
+    else TN80_LAUNCH(float, double);
+#undef TN80_LAUNCH
+  } else if (xtype == POD_F64 && ytype == POD_F64)
     tn::partial_kernel<double, double><<<grid, tn::THREADS, tn::SMEM, s>>>(
         m, (int)p, (int)q, (const double*)X, ldx, xcols, (const double*)Y, ldy, ycols,
         pl.rows_per_split, (double*)ws, gate, sym);
