@@ -669,13 +669,16 @@ constexpr int LDT = BK + 4;  // T chunk stored [j][k]
 
 template <int BN, typename TX = double>
 struct Cfg {
+  // BN = 80 (column groups of 80: q = 150 -> 160 instead of 192) runs 10 warps
+  static constexpr int NWARP = (BN == 80) ? 10 : 8;
+  static constexpr int NTHREADS = NWARP * 32;
   static constexpr int STAGES = (BN == 128) ? 3 : 4;
   static constexpr int BM = (BN == 64) ? 128 : 64;  // rows per block (T reuse)
   // X chunk stored [k][row] in X's own type (fp32 storage converted exactly
   // at the fragment loads); padding keeps the fragment loads conflict-free
   static constexpr int LDX = BM + (sizeof(TX) == 8 ? 4 : 8);
   static constexpr int WM = BM / 32;  // warps along M
-  static constexpr int WN = 8 / WM;   // 4 warps along N
+  static constexpr int WN = NWARP / WM;  // warps along N
   static constexpr int FN = BN / WN / 8;
   static constexpr int XT = BK * LDX, TT = BN * LDT;
   static constexpr size_t XBYTES = size_t(XT) * sizeof(TX);  // multiple of 16
@@ -687,7 +690,8 @@ struct Cfg {
 // columns of a row block while another group may still be reading X there).
 
 template <int BN, typename TX = double>
-__global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, double alpha,
+__global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p, int q,
+                                                                 double alpha,
                                                   const TX* X, int64_t ldx,
                                                   const int32_t* __restrict__ xcols,
                                                   const double* __restrict__ T, int64_t ldT,
@@ -734,7 +738,7 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
       l_r0 += G * C::BM;
     }
     // X: C::BM rows x BK cols as row pairs (2 x 8 B)
-    for (int e = threadIdx.x; e < BK * (C::BM / 2); e += THREADS) {
+    for (int e = threadIdx.x; e < BK * (C::BM / 2); e += C::NTHREADS) {
       const int cl = e / (C::BM / 2), i2 = (e - cl * (C::BM / 2)) * 2;
       const int c = k0 + cl;
       const int64_t row = r0 + i2;
@@ -755,7 +759,7 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
       }
     }
     // T: rows k0..k0+BK, all BN cols, k pairs
-    for (int e = threadIdx.x; e < BN * (BK / 2); e += THREADS) {
+    for (int e = threadIdx.x; e < BN * (BK / 2); e += C::NTHREADS) {
       const int j = e / (BK / 2), k2 = (e - j * (BK / 2)) * 2;
       const int k = k0 + k2;
       const bool jv = j < q;
@@ -831,6 +835,16 @@ static bool tn80_enabled() {
   }
   return v == 1;
 }
+// column groups of 80 instead of 64 when they pad at least 10 % less
+// (POD_NN80=0 disables, for A/B measurements)
+static bool nn_groups80(int64_t q) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_NN80");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1 && q > 64 && ceil_div(q, 80) * 80 * 10 < ceil_div(q, 64) * 64 * 9;
+}
 // POD_NN_GROUPS=0 disables column groups in the streamed NN kernel (A/B)
 static bool nn_groups_enabled() {
   static int v = -1;
@@ -902,6 +916,12 @@ static int ensure_attrs() {
   if (e != cudaSuccess) return cuda_status(e, "nns attr");
   e = cudaFuncSetAttribute(nns::kernel<64, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)nns::Cfg<64, float>::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "nns attr");
+  e = cudaFuncSetAttribute(nns::kernel<80>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)nns::Cfg<80>::SMEM);
+  if (e != cudaSuccess) return cuda_status(e, "nns attr");
+  e = cudaFuncSetAttribute(nns::kernel<80, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)nns::Cfg<80, float>::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "nns attr");
   g_attr_done = true;
   return POD_OK;
@@ -988,16 +1008,27 @@ static int gemm_nn_x32(int64_t m, int64_t p, int64_t q, double alpha, const floa
                        const int32_t* xcols, const double* T, int64_t ldt, double beta,
                        const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* gate,
                        cudaStream_t s) {
-  using C = nns::Cfg<64, float>;
   const int vx = ((reinterpret_cast<uintptr_t>(X) & 7) == 0) && (ldx % 2 == 0);
   const int vt = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ldt % 2 == 0);
-  const int64_t nblk = ceil_div(m, C::BM);
-  const unsigned gy = (unsigned)ceil_div(q, 64);
-  const int64_t per = std::max<int64_t>(1, capped(C::PER_SM * 148) / gy);
-  const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
-  nns::kernel<64, float><<<grid, nns::THREADS, C::SMEM, s>>>(m, (int)p, (int)q, alpha, X, ldx,
-                                                             xcols, T, ldt, beta, Z, ldz, Y, ldy,
-                                                             gate, vx, vt);
+  if (nn_groups80(q)) {
+    using C = nns::Cfg<80, float>;
+    const int64_t nblk = ceil_div(m, C::BM);
+    const unsigned gy = (unsigned)ceil_div(q, 80);
+    const int64_t per = std::max<int64_t>(1, capped(C::PER_SM * 148) / gy);
+    const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
+    nns::kernel<80, float><<<grid, C::NTHREADS, C::SMEM, s>>>(m, (int)p, (int)q, alpha, X, ldx,
+                                                              xcols, T, ldt, beta, Z, ldz, Y,
+                                                              ldy, gate, vx, vt);
+  } else {
+    using C = nns::Cfg<64, float>;
+    const int64_t nblk = ceil_div(m, C::BM);
+    const unsigned gy = (unsigned)ceil_div(q, 64);
+    const int64_t per = std::max<int64_t>(1, capped(C::PER_SM * 148) / gy);
+    const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
+    nns::kernel<64, float><<<grid, C::NTHREADS, C::SMEM, s>>>(m, (int)p, (int)q, alpha, X, ldx,
+                                                              xcols, T, ldt, beta, Z, ldz, Y,
+                                                              ldy, gate, vx, vt);
+  }
   POD_CHECK_LAUNCH("nn streamed (fp32 X)");
   return POD_OK;
 }
@@ -1068,12 +1099,22 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
     };
     const bool alias = overlaps(X, ldx, p) || (beta != 0.0 && overlaps(Z, ldz, q));
     if (q <= 64 || (!alias && nn_groups_enabled())) {
-      const int64_t nblk = ceil_div(m, nns::Cfg<64>::BM);
-      const unsigned gy = (unsigned)ceil_div(q, 64);
-      const int64_t per = std::max<int64_t>(1, capped(nns::Cfg<64>::PER_SM * 148) / gy);
-      const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
-      nns::kernel<64><<<grid, nns::THREADS, nns::Cfg<64>::SMEM, s>>>(
-          m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+      if (nn_groups80(q)) {  // groups of 80 pad less (q = 150: 160 vs 192)
+        using C80 = nns::Cfg<80>;
+        const int64_t nblk = ceil_div(m, C80::BM);
+        const unsigned gy = (unsigned)ceil_div(q, 80);
+        const int64_t per = std::max<int64_t>(1, capped(C80::PER_SM * 148) / gy);
+        const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
+        nns::kernel<80><<<grid, C80::NTHREADS, C80::SMEM, s>>>(
+            m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+      } else {
+        const int64_t nblk = ceil_div(m, nns::Cfg<64>::BM);
+        const unsigned gy = (unsigned)ceil_div(q, 64);
+        const int64_t per = std::max<int64_t>(1, capped(nns::Cfg<64>::PER_SM * 148) / gy);
+        const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
+        nns::kernel<64><<<grid, nns::THREADS, nns::Cfg<64>::SMEM, s>>>(
+            m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+      }
     } else if (q <= 128) {
       const int64_t nblk = ceil_div(m, nns::Cfg<128>::BM);
       const unsigned grid = (unsigned)std::min<int64_t>(nblk, capped(nns::Cfg<128>::PER_SM * 148));
