@@ -110,6 +110,7 @@ class MergeWorkspace:
         self.h_rec = torch.zeros((1 + nupd, REC_LEN), dtype=torch.int64).pin_memory()
         self.h_xi = torch.zeros(kk, dtype=torch.float64).pin_memory()
         self.leak = torch.zeros(1, **f64)
+        self._qscratch = {}
         self.cur = 0
         self.l = 0
         self.stats = {"rounds": 0}
@@ -138,19 +139,33 @@ class MergeWorkspace:
     # ------------------------------------------------------- launch pieces --
     def cholqr_ops(self, Wsrc, Q, l, Rout, gate_base, first_gate=None, sharded=True):
         """Q = orthonormal factor of Wsrc (m x l) with Wsrc = Q Rout (the
-        Householder QR of merge.py:70/76, matcore.py:209 replaced by gated
-        CholeskyQR passes).  Pass 0 runs when first_gate is null or set;
-        pass p >= 1 runs when pass p-1 asked for it (slot gate_base + p)."""
+        Householder QR of merge.py:70/76, matcore.py:209 replaced by
+        CholeskyQR passes).  Passes 0 and 1 (CholeskyQR2) run when first_gate
+        is null or set -- pass 0 into a scratch block, pass 1 from it into Q,
+        so both GEMMs are out of place (column-group parallel); further
+        passes run in place when the previous pass asked for them (slot
+        gate_base + p)."""
         ctx, r = self.ctx, self.r
         g0 = first_gate
-        ctx.tn(l, l, 1.0, Wsrc, Wsrc, dptr(self.Gq), r, gate=g0, tag="tn_cholqr_gram")
-        if sharded:
-            self.comm.allreduce_sum_(self.Gq)
-        ctx.cholqr_factor(dptr(self.Gq), r, l, Wsrc.m, dptr(self.Rinv), r, dptr(self.Rk), r,
-                          gate_in=g0, gate_out=self.gate(gate_base + 1), first_pass=1)
-        ctx.nn(l, l, 1.0, Wsrc, dptr(self.Rinv), r, Q, gate=g0, tag="nn_cholqr_apply")
-        ctx.small_copy(l, l, dptr(self.Rk), r, dptr(Rout), r, gate=g0)
-        for p in range(1, CHOLQR_PASSES):
+        tmp = self._scratch_like(Q)
+        src = Wsrc
+        for p in range(2):  # CholeskyQR2: Wsrc -> tmp -> Q
+            dst = tmp if p == 0 else Q
+            ctx.tn(l, l, 1.0, src, src, dptr(self.Gq), r, gate=g0, tag="tn_cholqr_gram")
+            if sharded:
+                self.comm.allreduce_sum_(self.Gq)
+            ctx.cholqr_factor(dptr(self.Gq), r, l, src.m, dptr(self.Rinv), r, dptr(self.Rk), r,
+                              gate_in=g0, gate_out=self.gate(gate_base + p + 1),
+                              first_pass=1 if p == 0 else 0)
+            ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, dst, gate=g0, tag="nn_cholqr_apply")
+            if p == 0:
+                ctx.small_copy(l, l, dptr(self.Rk), r, dptr(Rout), r, gate=g0)
+            else:
+                ctx.small_gemm(l, l, l, 1.0, dptr(self.Rk), r, 0, dptr(Rout), r, 0.0,
+                               dptr(self.Rtmp), r, gate=g0)
+                ctx.small_copy(l, l, dptr(self.Rtmp), r, dptr(Rout), r, gate=g0)
+            src = dst
+        for p in range(2, CHOLQR_PASSES):
             gp = self.gate(gate_base + p)
             ctx.tn(l, l, 1.0, Q, Q, dptr(self.Gq), r, gate=gp, tag="tn_cholqr_gram")
             if sharded:
@@ -161,6 +176,15 @@ class MergeWorkspace:
             ctx.small_gemm(l, l, l, 1.0, dptr(self.Rk), r, 0, dptr(Rout), r, 0.0,
                            dptr(self.Rtmp), r, gate=gp)
             ctx.small_copy(l, l, dptr(self.Rtmp), r, dptr(Rout), r, gate=gp)
+
+    def _scratch_like(self, Q):
+        """m x r scratch block for the first CholeskyQR pass (one per row count)."""
+        key = Q.m
+        buf = self._qscratch.get(key)
+        if buf is None:
+            buf = ColMat.zeros(Q.m, self.r, self.ctx.device)
+            self._qscratch[key] = buf
+        return buf
 
     def merge_ops(self, cur, ub=0, before_core=None):
         """block_merge (merge.py:37-91) of stack `cur` (U1, sig[cur]) with
@@ -460,7 +484,9 @@ class IsmaEngine(MergeWorkspace):
                 self.graphs.clear()  # the warm-up grew a workspace other graphs captured
             gr = torch.cuda.CUDAGraph()
             l0 = self.ctx.launches
-            with torch.cuda.graph(gr, stream=st):
+            # thread_local: the OOC read-ahead thread may touch CUDA (pinned
+            # allocation, H2D copies) while a round is being captured
+            with torch.cuda.graph(gr, stream=st, capture_error_mode="thread_local"):
                 self.round_ops(mode, cur, ub, pipelined, rowsrc)
             self.graph_launches[key] = self.ctx.launches - l0
             self.graphs[key] = gr
