@@ -311,11 +311,22 @@ __device__ bool inter_step(const Slot& c0, const Slot& c1, const Geo& g, double 
   double* xw = c0.w + (size_t)xc * g.ld;
   double* xj = g.ldj ? c0.j + (size_t)xc * g.ldj : nullptr;
   double xa[RPL > 0 ? RPL : 1];
+  // the accumulated rotation's x column is register-cached too when its
+  // rows fit the same lanes (njrows <= nrows) -- small RPL only, so the
+  // wide-row instantiations keep their register budget
+  constexpr int JR = (RPL > 0 && RPL <= 8) ? RPL : 1;
+  const bool jreg = JR > 1 && xj && g.njrows <= g.nrows;
+  double xja[JR];
   if (RPL > 0) {
 #pragma unroll
     for (int k = 0; k < (RPL > 0 ? RPL : 1); ++k) {
       const int i = gl + k * tpp;
       xa[k] = (xlive && i < g.nrows) ? xw[i] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < JR; ++k) {
+      const int i = gl + k * tpp;
+      xja[k] = (jreg && xlive && i < g.njrows) ? xj[i] : 0.0;
     }
   }
   double al = xlive ? c0.nrm[xc] : 0.0;
@@ -367,7 +378,22 @@ __device__ bool inter_step(const Slot& c0, const Slot& c1, const Geo& g, double 
           yw[i] = fma(s_, x0, c_ * y0);
         }
       }
-      if (xj) {
+      if (jreg) {
+        double* yj = c1.j + (size_t)yc * g.ldj;
+        double yjb[JR];
+#pragma unroll
+        for (int k = 0; k < JR; ++k) {
+          const int i = gl + k * tpp;
+          yjb[k] = i < g.njrows ? yj[i] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < JR; ++k) {
+          const int i = gl + k * tpp;
+          const double x0 = xja[k], y0 = yjb[k];
+          xja[k] = fma(c_, x0, -s_ * y0);
+          if (i < g.njrows) yj[i] = fma(s_, x0, c_ * y0);
+        }
+      } else if (xj) {
         double* yj = c1.j + (size_t)yc * g.ldj;
         for (int i = gl; i < g.njrows; i += tpp) {
           const double x0 = xj[i], y0 = yj[i];
@@ -391,6 +417,11 @@ __device__ bool inter_step(const Slot& c0, const Slot& c1, const Geo& g, double 
       for (int k = 0; k < (RPL > 0 ? RPL : 1); ++k) {
         const int i = gl + k * tpp;
         if (i < g.nrows) xw[i] = xa[k];
+      }
+#pragma unroll
+      for (int k = 0; k < JR; ++k) {
+        const int i = gl + k * tpp;
+        if (jreg && i < g.njrows) xj[i] = xja[k];
       }
     }
     if (gl == 0) c0.nrm[xc] = al;
@@ -588,11 +619,14 @@ __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
                       int64_t ldm, const double* __restrict__ Rm, int64_t ldr,
                       const double* __restrict__ sig2, int l2, int r, int rcap,
                       double* __restrict__ T, int64_t ldt, int tcols, double* __restrict__ sig_new,
-                      int64_t* __restrict__ info, int max_sweeps) {
+                      int64_t* __restrict__ info, int max_sweeps, int trans) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double smem_bj[];
   const int n = l1 + l2;
-  const Geo g(n, n, 0, CL);
+  // trans: one-sided Jacobi on E^T (lower block-triangular, ~10 sweeps instead
+  // of ~14 on E) with the rotations accumulated in J: E^T J = W gives
+  // E = J (W^T), so U_E = J and sigma = ||W columns||
+  const Geo g(n, n, trans ? n : 0, CL);
   const Smem<CL> sm = carve<CL>(smem_bj, g);
   const int me = (int)cl.block_rank();
   // E = [[S1, M S2], [0, R S2]] columns of the two owned blocks
@@ -600,8 +634,9 @@ __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
     const Slot s = slot_at(sm.slots, g, 0, t2);
     const int blk = init_block(me, t2, CL);
     for (int t = threadIdx.x; t < g.bs * g.ld; t += blockDim.x) {
-      const int c = t / g.ld, i = t - c * g.ld;
-      const int j = blk * g.bs + c;
+      const int c = t / g.ld, ii0 = t - c * g.ld;
+      const int jj0 = blk * g.bs + c;
+      const int i = trans ? jj0 : ii0, j = trans ? ii0 : jj0;  // element E[i, j]
       double e = 0.0;
       if (j < n && i < n) {
         if (j < l1) e = (i == j) ? sig1[j] : 0.0;
@@ -616,6 +651,11 @@ __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
       }
       s.w[t] = e;
     }
+    if (trans)
+      for (int t = threadIdx.x; t < g.bs * g.ldj; t += blockDim.x) {
+        const int c = t / g.ldj, i = t - c * g.ldj;
+        s.j[t] = (i == blk * g.bs + c && i < n) ? 1.0 : 0.0;
+      }
     for (int c = threadIdx.x; c < g.bse; c += blockDim.x) {
       s.id[c] = (double)(c < g.bs ? blk * g.bs + c : 1 << 30);
       s.nrm[c] = 0.0;
@@ -649,9 +689,10 @@ __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
       const double sg = sqrt(sm.gnorm[id]);
       if (threadIdx.x == 0 && k < keep && k < rcap) sig_new[k] = sg;
       const double* w = s.w + (size_t)c * g.ld;
+      const double* jc = s.j + (size_t)c * g.ldj;
       for (int e = threadIdx.x; e < n; e += blockDim.x) {
         const int row = (e < l1) ? e : rcap + (e - l1);
-        T[row + (int64_t)k * ldt] = (k < keep) ? w[e] / sg : 0.0;
+        T[row + (int64_t)k * ldt] = (k < keep) ? (trans ? jc[e] : w[e] / sg) : 0.0;
       }
     }
   }
@@ -859,6 +900,16 @@ static int threads_for(const Geo& g, int tpp) { return ((g.bs * tpp + 31) / 32) 
 constexpr int BJ_CL = 8;
 static const int BJ_NOT_APPLICABLE = -1;
 
+// POD_BJ_TRANS=0: merge E-SVD on E itself instead of E^T (A/B measurements)
+static bool bj_trans_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_BJ_TRANS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool bj_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -874,50 +925,35 @@ int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, 
                   cudaStream_t stream) {
   if (!bj_enabled()) return BJ_NOT_APPLICABLE;
   const int n = (int)(l1 + l2);
-  {
-    // E too large for two blocks per CTA at 8 CTAs (2r > ~330): a 16-CTA
-    // cluster halves the block size
-    const bj::Geo g16(n, n, 0, 16);
-    const bj::Geo g8(n, n, 0, BJ_CL);
-    if (g8.smem_bytes(BJ_CL) > bj::SMEM_CAP && g16.smem_bytes(16) <= bj::SMEM_CAP) {
-      const size_t bytes = g16.smem_bytes(16);
-      const int tpp = bj::lanes_for(g16);
-      const int th = bj::threads_for(g16, tpp);
-      const int rpl = (g16.nrows + tpp - 1) / tpp;
-      if (th > 384) return BJ_NOT_APPLICABLE;
-#define BJ_L16(T_, R_) bj::launch(bj::merge_core_kernel<16, T_, R_>, 16, th, bytes, stream, sig1, (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new, info, 60)
-      if (tpp == 32) {
-        if (rpl <= 16) return BJ_L16(32, 16);
-        if (rpl <= 24) return BJ_L16(32, 24);
-        return BJ_L16(32, 0);
-      }
-      if (tpp == 16) {
-        if (rpl <= 24) return BJ_L16(16, 24);
-        return BJ_L16(16, 0);
-      }
-#undef BJ_L16
-      return BJ_NOT_APPLICABLE;
+  if (n < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
+  // preference: E^T with accumulated J (~10 instead of ~14 sweeps) at 8
+  // CTAs; then E itself at 8, then 16 CTAs -- the first geometry that fits
+  // (measured: E^T on a 16-CTA cluster is slower than E on 8 or 16)
+  for (int variant = 0; variant < 4; ++variant) {
+    const int trans = variant == 0 ? (bj_trans_enabled() ? 1 : 0) : 0;
+    if (variant < 2 && !trans) continue;
+    const int cl = (variant % 2 == 0) ? BJ_CL : 16;
+    const bj::Geo g(n, n, trans ? n : 0, cl);
+    const size_t bytes = g.smem_bytes(cl);
+    if (bytes > bj::SMEM_CAP) continue;
+    const int tpp = bj::lanes_for(g);
+    const int th = bj::threads_for(g, tpp);
+    const int rpl = (g.nrows + tpp - 1) / tpp;
+    if (th > 512 || (rpl > 8 && th > 384)) continue;
+#define BJ_L(C_, T_, R_) return bj::launch(bj::merge_core_kernel<C_, T_, R_>, C_, th, bytes, stream, sig1, (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new, info, 60, trans)
+    if (cl == BJ_CL) {
+      if (tpp == 8) { if (rpl <= 4) BJ_L(BJ_CL, 8, 4); if (rpl <= 8) BJ_L(BJ_CL, 8, 8); if (rpl <= 16) BJ_L(BJ_CL, 8, 16); if (rpl <= 24) BJ_L(BJ_CL, 8, 24); BJ_L(BJ_CL, 8, 0); }
+      if (tpp == 16) { if (rpl <= 4) BJ_L(BJ_CL, 16, 4); if (rpl <= 8) BJ_L(BJ_CL, 16, 8); if (rpl <= 16) BJ_L(BJ_CL, 16, 16); if (rpl <= 24) BJ_L(BJ_CL, 16, 24); BJ_L(BJ_CL, 16, 0); }
+      if (rpl <= 4) BJ_L(BJ_CL, 32, 4); if (rpl <= 8) BJ_L(BJ_CL, 32, 8); if (rpl <= 16) BJ_L(BJ_CL, 32, 16); if (rpl <= 24) BJ_L(BJ_CL, 32, 24); BJ_L(BJ_CL, 32, 0);
+    } else {
+      if (th > 384) continue;
+      if (tpp == 32) { if (rpl <= 16) BJ_L(16, 32, 16); if (rpl <= 24) BJ_L(16, 32, 24); BJ_L(16, 32, 0); }
+      if (tpp == 16) { if (rpl <= 24) BJ_L(16, 16, 24); BJ_L(16, 16, 0); }
+      continue;
     }
-  }
-  const bj::Geo g(n, n, 0, BJ_CL);
-  const size_t bytes = g.smem_bytes(BJ_CL);
-  if (bytes > bj::SMEM_CAP || n < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
-  const int tpp = bj::lanes_for(g);
-  const int th = bj::threads_for(g, tpp);
-  const int rpl = (g.nrows + tpp - 1) / tpp;
-  if (th > 512 || (rpl > 8 && th > 384)) return BJ_NOT_APPLICABLE;
-#define BJ_L(T_, R_) bj::launch(bj::merge_core_kernel<BJ_CL, T_, R_>, BJ_CL, th, bytes, stream, sig1, (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new, info, 60)
-#define BJ_R(T_)                         \
-  if (rpl <= 4) return BJ_L(T_, 4);      \
-  if (rpl <= 8) return BJ_L(T_, 8);      \
-  if (rpl <= 16) return BJ_L(T_, 16);    \
-  if (rpl <= 24) return BJ_L(T_, 24);    \
-  return BJ_L(T_, 0);
-  if (tpp == 8) { BJ_R(8) }
-  if (tpp == 16) { BJ_R(16) }
-  BJ_R(32)
-#undef BJ_R
 #undef BJ_L
+  }
+  return BJ_NOT_APPLICABLE;
 }
 
 int bj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t gd, int64_t r,
