@@ -419,111 +419,6 @@ inline bool better(int64_t p, int64_t q) {
 }
 }  // namespace tn80
 
-// ---------------------------------------------------------------- NN ------
-// One CTA owns BM rows x ALL q (<= BN) output columns, so Y may alias X or Z
-// (each CTA reads its own rows completely before writing them).
-namespace nn {
-constexpr int BK = 16;
-constexpr int LDT = BK + 4;  // % 16 == 4
-constexpr int THREADS = 256;
-constexpr int STAGES = 3;
-
-template <int BN>
-struct Cfg {
-  static constexpr int BM = (BN == 64) ? 128 : 64;
-  static constexpr int WM = BM / 32;         // warps along M (32 rows each)
-  static constexpr int WN = 8 / WM;          // warps along N
-  static constexpr int FN = BN / WN / 8;     // 8-col fragments per warp
-  static constexpr int LDX = BM + 4;         // % 16 == 4
-  static constexpr int XT = BK * LDX, TT = BN * LDT;
-  static constexpr size_t SMEM = size_t(STAGES) * (XT + TT) * sizeof(double);
-};
-
-template <int BN>
-__global__ void __launch_bounds__(THREADS) kernel(
-    int64_t m, int p, int q, double alpha, const double* X, int64_t ldx,
-    const int32_t* __restrict__ xcols, const double* __restrict__ T, int64_t ldt, double beta,
-    const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* __restrict__ gate) {
-  using C = Cfg<BN>;
-  if (gate && *gate == 0) return;
-  extern __shared__ __align__(16) double smem[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t row0 = (int64_t)blockIdx.x * C::BM;
-  // loader: 256 threads cover BM rows x BK cols of X
-  constexpr int RGROUPS = C::BM / 32;          // row groups of 32
-  constexpr int CPT = BK / (8 / RGROUPS);      // columns per thread
-  const int lrg = warp % RGROUPS, lcg = warp / RGROUPS;
-  const int64_t lrow = row0 + lrg * 32 + lane;
-  const bool lrv = lrow < m;
-
-  auto load_stage = [&](int st, int k0) {
-    double* xs = smem + (size_t)st * (C::XT + C::TT);
-    double* ts = xs + C::XT;
-#pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-      const int cl = lcg * CPT + i;
-      const int c = k0 + cl;
-      bool v = lrv && c < p;
-      int64_t col = c;
-      if (v && xcols) {
-        col = xcols[c];
-        v = col >= 0;  // index -1: zero column
-      }
-      const double* src = v ? X + col * ldx + lrow : X;
-      cp_async8(xs + cl * C::LDX + lrg * 32 + lane, src, v);
-    }
-    // T chunk: rows k0..k0+BK, cols 0..BN
-    for (int e = threadIdx.x; e < BN * BK; e += THREADS) {
-      const int j = e / BK, k = e % BK;
-      const bool v = j < q && (k0 + k) < p;
-      const double* src = v ? T + (k0 + k) + (int64_t)j * ldt : T;
-      cp_async8(ts + j * LDT + k, src, v);
-    }
-  };
-
-  const int wm = warp % C::WM, wn = warp / C::WM;
-  double acc[4][C::FN][2];
-#pragma unroll
-  for (int f = 0; f < 4; ++f)
-#pragma unroll
-    for (int g = 0; g < C::FN; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
-
-  const int nkb = (p + BK - 1) / BK;
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nkb) load_stage(s, s * BK);
-    cp_async_commit();
-  }
-  for (int kb = 0; kb < nkb; ++kb) {
-    const int nxt = kb + STAGES - 1;
-    if (nxt < nkb) load_stage(nxt % STAGES, nxt * BK);
-    cp_async_commit();
-    cp_async_wait<STAGES - 1>();
-    __syncthreads();
-    const double* xs = smem + (size_t)(kb % STAGES) * (C::XT + C::TT);
-    const double* ts = xs + C::XT;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      double a[4], b[C::FN];
-#pragma unroll
-      for (int f = 0; f < 4; ++f)
-        a[f] = xs[(kk * 4 + (lane & 3)) * C::LDX + wm * 32 + f * 8 + (lane >> 2)];
-#pragma unroll
-      for (int g = 0; g < C::FN; ++g)
-        b[g] = ts[(wn * (BN / C::WN) + g * 8 + (lane >> 2)) * LDT + kk * 4 + (lane & 3)];
-#pragma unroll
-      for (int f = 0; f < 4; ++f)
-#pragma unroll
-        for (int g = 0; g < C::FN; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
-    }
-    __syncthreads();
-  }
-  cp_async_wait<0>();
-
-  nn_epilogue<C::FN>(acc, row0 + wm * 32, wn * (BN / C::WN), lane, m, q, alpha, beta, Z, ldz, Y,
-                     ldy);
-}
-}  // namespace nn
 
 // -------------------------------------------------- NN persistent ------
 // T (p x q, p <= PMAX) resident in shared memory for the whole kernel; each
@@ -854,15 +749,6 @@ static bool nn_groups_enabled() {
   }
   return v == 1;
 }
-// POD_NN_LEGACY=1 selects the per-block streaming kernel (A/B measurements)
-static bool nn_streamed_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("POD_NN_LEGACY");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
 static int ensure_attrs() {
   if (g_attr_done) return POD_OK;
   cudaError_t e = cudaFuncSetAttribute(tn::partial_kernel<double, double>,
@@ -890,15 +776,6 @@ static int ensure_attrs() {
   TN80_ATTR(float, double)
   TN80_ATTR(double, float)
 #undef TN80_ATTR
-  e = cudaFuncSetAttribute(nn::kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)nn::Cfg<64>::SMEM);
-  if (e != cudaSuccess) return cuda_status(e, "nn attr");
-  e = cudaFuncSetAttribute(nn::kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)nn::Cfg<128>::SMEM);
-  if (e != cudaSuccess) return cuda_status(e, "nn attr");
-  e = cudaFuncSetAttribute(nn::kernel<192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)nn::Cfg<192>::SMEM);
-  if (e != cudaSuccess) return cuda_status(e, "nn attr");
   for (int bn : {64, 128, 192}) {
     const void* fn = bn == 64 ? (const void*)nnp::kernel<64>
                    : bn == 128 ? (const void*)nnp::kernel<128> : (const void*)nnp::kernel<192>;
@@ -1084,10 +961,9 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
       return POD_OK;
     }
   }
-  if (nn_streamed_enabled()) {
+  {
     const int vx = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && (ldx % 2 == 0);
     const int vt = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ldt % 2 == 0);
-    
     // Y aliasing X or Z (in-place Q <- Q R^-1): one column group only
     auto overlaps = [&](const double* a, int64_t lda, int64_t ncols) {
       if (!a) return false;
@@ -1129,22 +1005,6 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
     POD_CHECK_LAUNCH("nn streamed");
     return POD_OK;
   }
-  if (q <= 64) {
-    dim3 grid((unsigned)ceil_div(m, nn::Cfg<64>::BM));
-    nn::kernel<64><<<grid, nn::THREADS, nn::Cfg<64>::SMEM, s>>>(m, (int)p, (int)q, alpha, X, ldx,
-                                                               xcols, T, ldt, beta, Z, ldz, Y, ldy,
-                                                               gate);
-  } else if (q <= 128) {
-    dim3 grid((unsigned)ceil_div(m, nn::Cfg<128>::BM));
-    nn::kernel<128><<<grid, nn::THREADS, nn::Cfg<128>::SMEM, s>>>(
-        m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate);
-  } else {
-    dim3 grid((unsigned)ceil_div(m, nn::Cfg<192>::BM));
-    nn::kernel<192><<<grid, nn::THREADS, nn::Cfg<192>::SMEM, s>>>(
-        m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate);
-  }
-  POD_CHECK_LAUNCH("nn");
-  return POD_OK;
 }
 
 extern "C" int pod_set_grid_cap(int ctas) {
