@@ -567,9 +567,11 @@ class IsmaEngine(MergeWorkspace):
         mode = {"l2n": MODE_L2N, "ort": MODE_ORT}.get(strategy, MODE_UNIFORM)
         rows = self.w > 0
         # ort's distribution depends on the merged basis, and so does the
-        # leverage-driven row draw: no pipelining for either (nor for ICRS)
-        pipelined = (bitgen is not None and not self.comm.active and mode != MODE_ORT
-                     and not rows)
+        # leverage-driven row draw: no pipelining for either (nor for ICRS).
+        # Row-sharded runs pipeline too: every rank issues its collectives in
+        # the same program order (update Gram after the merge's GEMM-phase
+        # reductions), which the backend serialises on its own stream.
+        pipelined = bitgen is not None and mode != MODE_ORT and not rows
         state = bitgen.state if (rows and bitgen is not None) else None
         self._stage_uniforms(rng, 0, rows)
         self.update_ops(MODE_L2N, 0, self.S[cur].cols(0, r),                 # bootstrap
