@@ -1,4 +1,4 @@
-"""Device-resident ISMA engine (column-sampling path).
+"""Device-resident ISMA engine (column sampling and ICRS row sampling).
 
 Layout in HBM (one engine per run and GPU):
   A          m x n column-major, ld = m (the data matrix, read in place)
@@ -24,10 +24,12 @@ back one small record (g, |S|, ranks, keep) plus the k cosines.
 Per round (isma.py:276-293):
   draw -> Gram of A[:, idx] (TN, gathered) -> eigh (pivoted Cholesky +
   Jacobi) -> lift A[:, idx] T (NN, gathered)                 [get_update]
-  M = U1^T U2 -> W = U2 - U1 M -> CholeskyQR (<= 4 gated passes)
+  M = U1^T U2 -> W = U2 - U1 M -> CholeskyQR2 (+ <= 2 gated passes)
   -> leak gate -> gated second projection -> E-SVD (Jacobi)
   -> [U1 Q] T                                                [block_merge]
   -> cosines                                                 [convergence]
+With rows=True the update draws rows (row norms or leverage), builds the
+dedup-scaled row block Y and eigensolves Y^T Y (isma.py:168-176).
 """
 
 from __future__ import annotations
@@ -47,7 +49,7 @@ REORTH_TOL = 1e-8  # merge.py:34
 # (measured: caps of 148-200 CTAs and forking the update at the round start
 # instead of after the merge's GEMM phase are within noise or slower)
 UPDATE_GRID_CAP = int(__import__("os").environ.get("POD_UPDATE_GRID_CAP", "0"))
-CHOLQR_PASSES = 4  # pass 0 always; passes 1..3 gated on the previous pass
+CHOLQR_PASSES = 4  # passes 0-1 always (CholeskyQR2); passes 2..3 gated on the previous pass
 
 MODE_L2N, MODE_UNIFORM, MODE_WEIGHTS, MODE_ORT, MODE_ROWS = 0, 1, 2, 3, 4
 ORT_DEGENERATE_RTOL = 1e-14  # sampling.py:158 degenerate_rtol
