@@ -142,6 +142,19 @@ int pod_gemm_nn(int xtype, int64_t m, int64_t p, int64_t q, double alpha, const 
                 const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* gate,
                 void* stream);
 
+/* Page-lock and map a host buffer for direct kernel access (host-resident,
+ * streamed matrices; the device address is the host address under UVA,
+ * checked), and release it. */
+int pod_host_register(void* ptr, size_t bytes);
+int pod_host_unregister(void* ptr);
+
+/* D[:, j] = A[:, idx[j]] for j < g (idx -1: zero column; idx NULL: j).  A
+ * may be page-locked host memory mapped into the device address space (a
+ * host-resident, streamed matrix): one PCIe read of the sampled block per
+ * round (isma.py:163), the round's GEMMs then read D from HBM. */
+int pod_gather_cols(int atype, const void* A, int64_t m, int64_t lda, const int32_t* idx,
+                    int64_t g, void* D, int64_t ldd, void* stream);
+
 /* Cap (in CTAs; 0 = none) on the grids of the TN / NN GEMMs launched while
  * set -- host-side state read at launch (and so baked into captured graphs):
  * the pipelined next-round update runs capped beside the critical merge. */

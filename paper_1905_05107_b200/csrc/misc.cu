@@ -188,3 +188,65 @@ extern "C" int pod_scale_cols(double* U, int64_t m, int64_t l, int64_t ldu, cons
   POD_CHECK_LAUNCH("scale cols");
   return POD_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Sampled-column gather for host-resident (streamed) matrices: D[:, j] =
+// A[:, idx[j]] (idx -1: zero column) for j < g.  A may be page-locked host
+// memory mapped into the device address space, so this is the one PCIe read
+// of the sampled block per round (isma.py:163); the round's GEMMs then read
+// D from HBM.  Column-parallel, 16-byte vectorised when aligned.
+namespace pod {
+template <typename T>
+__global__ void __launch_bounds__(256) gather_cols_kernel(const T* __restrict__ A, int64_t m,
+                                                          int64_t lda, const int32_t* __restrict__ idx,
+                                                          int g, T* __restrict__ D, int64_t ldd,
+                                                          int vec) {
+  constexpr int V = 16 / sizeof(T);
+  for (int j = blockIdx.y; j < g; j += gridDim.y) {
+    const int64_t c = idx ? (int64_t)idx[j] : (int64_t)j;
+    T* dst = D + (int64_t)j * ldd;
+    if (c < 0) {
+      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+           i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = T(0);
+      continue;
+    }
+    const T* src = A + c * lda;
+    if (vec) {
+      const int64_t mv = m / V;
+      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < mv;
+           i += (int64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<int4*>(dst)[i] = __ldcs(reinterpret_cast<const int4*>(src) + i);
+      for (int64_t i = mv * V + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+           i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+    } else {
+      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+           i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+    }
+  }
+}
+}  // namespace pod
+
+extern "C" int pod_gather_cols(int atype, const void* A, int64_t m, int64_t lda,
+                               const int32_t* idx, int64_t g, void* D, int64_t ldd,
+                               void* stream) {
+  POD_REQUIRE(atype == POD_F64 || atype == POD_F32, "pod_gather_cols: bad operand type");
+  POD_REQUIRE(m >= 1 && g >= 0 && lda >= m && ldd >= m, "pod_gather_cols: bad shape");
+  if (g == 0) return POD_OK;
+  const size_t es = atype == POD_F64 ? 8 : 4;
+  const int vec = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(D)) % 16 == 0) &&
+                  ((lda * es) % 16 == 0) && ((ldd * es) % 16 == 0);
+  const int gx = (int)std::min<int64_t>(ceil_div(m, 256 * (16 / (int64_t)es)), 64);
+  dim3 grid((unsigned)std::max(1, gx), (unsigned)std::min<int64_t>(g, 1024));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (atype == POD_F64)
+    gather_cols_kernel<double><<<grid, 256, 0, s>>>((const double*)A, m, lda, idx, (int)g,
+                                                    (double*)D, ldd, vec);
+  else
+    gather_cols_kernel<float><<<grid, 256, 0, s>>>((const float*)A, m, lda, idx, (int)g,
+                                                   (float*)D, ldd, vec);
+  POD_CHECK_LAUNCH("gather cols");
+  return POD_OK;
+}

@@ -51,10 +51,9 @@ class ColMat:
         self.col0 = int(col0)
 
     @classmethod
-    def zeros(cls, m, ncols, device, ld=None):
+    def zeros(cls, m, ncols, device, ld=None, dtype=torch.float64):
         ld = int(m) if ld is None else int(ld)
-        return cls(torch.zeros((max(int(ncols), 1), ld), dtype=torch.float64, device=device), m,
-                   ncols)
+        return cls(torch.zeros((max(int(ncols), 1), ld), dtype=dtype, device=device), m, ncols)
 
     def cols(self, a, b=None):
         b = self.ncols if b is None else b
@@ -170,6 +169,10 @@ class Ctx:
         self._call("gather_scale_rows", 1, 0.0, (A.esize + 8.0) * hcap * g,
                    "pod_gather_scale_rows", A.code, A.ptr, A.ld, _ptr(cols), g, _ptr(rows),
                    _ptr(cnt), _ptr(p), float(w), hcap, _ptr(hdev), Y.ptr, Y.ld, self.stream)
+
+    def gather_cols(self, A, idx, g, D):
+        self._call("gather_cols", 1, 0.0, 2.0 * A.esize * A.m * g, "pod_gather_cols", A.code,
+                   A.ptr, A.m, A.ld, _ptr(idx), g, D.ptr, D.ld, self.stream)
 
     def resid_colnorms2(self, A, n, U, r, C, ldc, out, cols=None):
         ws = self.ws("resid", _lib.load().pod_resid_ws_bytes(A.m, n))
@@ -303,6 +306,48 @@ def get_ctx(device=None):
         ctx = Ctx(torch.device("cuda", key))
         _CTX[key] = ctx
     return ctx
+
+
+class HostResident:
+    """Context manager giving a ColMat over a HOST matrix that the kernels
+    read directly (page-locked, mapped; no device copy of A): numpy input is
+    made Fortran-ordered float64/float32 (as_dense semantics) and registered
+    for the duration; a page-locked torch tensor is used as is."""
+
+    def __init__(self, a):
+        self.registered = None
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda or a.ndim != 2:
+                from .errors import ParameterError
+
+                raise ParameterError("host residency needs a 2-D host matrix")
+            m, n = a.shape
+            t = a if a.dtype in (torch.float32, torch.float64) else a.to(torch.float64)
+            st = t.T if (t.stride(0) == 1 and t.stride(1) == max(m, 1)) else t.T.contiguous()
+        else:
+            arr = np.asarray(a)
+            m, n = arr.shape
+            arr = np.asarray(arr, dtype=np.float32 if arr.dtype == np.float32 else np.float64,
+                             order="F")
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", UserWarning)
+                st = torch.from_numpy(arr.T)
+            self._keep = arr
+        if not st.is_pinned():
+            _lib.call("pod_host_register", ctypes.c_void_p(st.data_ptr()),
+                      st.numel() * st.element_size())
+            self.registered = st.data_ptr()
+        self.col = ColMat(st, m, n)
+
+    def __enter__(self):
+        return self.col
+
+    def __exit__(self, *exc):
+        torch.cuda.synchronize()
+        if self.registered is not None:
+            _lib.call("pod_host_unregister", ctypes.c_void_p(self.registered))
+            self.registered = None
+        return False
 
 
 def to_device_colmajor(a, device):

@@ -329,6 +329,13 @@ class IsmaEngine(MergeWorkspace):
         self.side = torch.cuda.Stream(dev)
         self.ort = None  # (C = U^T A, residual norms) buffers of the "ort" strategy
         self.frob2 = 0.0
+        # host-resident A (page-locked, mapped): the norm pass, ort's U^T A and
+        # finalize's A^T U stream it over PCIe; each round copies its sampled
+        # columns into an HBM block D (multi-pass streamed ISMA)
+        self.host_A = not A.t.is_cuda
+        self._hbuf = None
+        self.D = [ColMat.zeros(A.m, g, dev, dtype=A.t.dtype) for _ in range(len(self.Uupd_b))] \
+            if self.host_A else None
         # row sampling (ICRS, isma.py:168-176): w row draws per round over the m rows
         self.w = int(w)
         if self.w:
@@ -379,11 +386,48 @@ class IsmaEngine(MergeWorkspace):
                         torch.zeros(n, dtype=torch.float64, device=dev))
         C, res2 = self.ort
         U = self.S[cur].cols(0, r)
+        if self.host_A:  # one PCIe pass: DMA column chunks, both products per chunk
+            def chunk(Ach, j0, j1):
+                ctx.tn(r, j1 - j0, 1.0, U, Ach, dptr(C, j0 * r), r, tag="tn_ort_UtA")
+                ctx.resid_colnorms2(Ach, j1 - j0, U, r, dptr(C, j0 * r), r, res2[j0:j1])
+            self._stream_columns(chunk)
+            return res2
         ctx.tn(r, n, 1.0, U, A, dptr(C), r, tag="tn_ort_UtA")
         self.comm.allreduce_sum_(C)
         ctx.resid_colnorms2(A, n, U, r, dptr(C), r, res2)
         self.comm.allreduce_sum_(res2)
         return res2
+
+    def _stream_columns(self, fn):
+        """Host-resident A: column chunks (~1 GB) DMA-copied into two HBM
+        buffers on a copy stream, each consumed by fn(chunk, j0, j1) on the
+        current stream while the next one is in flight -- one PCIe pass with
+        copy engines instead of kernel reads that a tiled product would
+        repeat per output tile."""
+        A, ctx = self.A, self.ctx
+        dev = ctx.device
+        m, n, es = A.m, self.n, A.esize
+        per = max(1, min(n, (1 << 30) // (m * es)))
+        if self._hbuf is None or self._hbuf[0].ncols < per:
+            self._hbuf = [ColMat.zeros(m, per, dev, dtype=A.t.dtype) for _ in range(2)]
+            self._copy_stream = torch.cuda.Stream(dev)
+            self._ev_ready = [torch.cuda.Event() for _ in range(2)]
+            self._ev_free = [torch.cuda.Event() for _ in range(2)]
+        main = torch.cuda.current_stream(dev)
+        cs = self._copy_stream
+        cs.wait_stream(main)
+        for i, j0 in enumerate(range(0, n, per)):
+            j1 = min(n, j0 + per)
+            b = i % 2
+            buf = self._hbuf[b]
+            if i >= 2:
+                cs.wait_event(self._ev_free[b])  # chunk i - 2 consumed this buffer
+            with torch.cuda.stream(cs):
+                buf.t[:j1 - j0, :m].copy_(A.t[j0:j1, :m], non_blocking=True)
+                self._ev_ready[b].record(cs)
+            main.wait_event(self._ev_ready[b])
+            fn(ColMat(buf.t, m, j1 - j0), j0, j1)
+            self._ev_free[b].record(main)
 
     def update_ops(self, mode, b, dest, cur=None, rowsrc=None):
         """get_update (isma.py:144-178) at capacity into update buffer b (its
@@ -401,8 +445,15 @@ class IsmaEngine(MergeWorkspace):
             thr = ORT_DEGENERATE_RTOL * self.frob2
         ctx.draw(mode, weights, self.live, self.n, self.uni[b], self.c, self.idx[b], self.cnt[b],
                  info=self.rec[1 + b, REC_G:], thr=thr)
+        # the sampled block D: gathered inside the GEMM loaders from A in HBM,
+        # or -- A host-resident -- copied once over PCIe into HBM (isma.py:163)
+        if self.host_A:
+            ctx.gather_cols(A, self.idx[b], g, self.D[b])
+            src, cols = self.D[b], None
+        else:
+            src, cols = A, self.idx[b]
         if rowsrc is None:
-            ctx.tn(g, g, 1.0, A, A, dptr(self.G[b]), g, xcols=self.idx[b], ycols=self.idx[b],
+            ctx.tn(g, g, 1.0, src, src, dptr(self.G[b]), g, xcols=cols, ycols=cols,
                    tag="tn_gram_gather")                                     # baselines.py:43
             self.comm.allreduce_sum_(self.G[b])
         else:
@@ -411,16 +462,16 @@ class IsmaEngine(MergeWorkspace):
                 self.levdiv.copy_(self.h_levdiv, non_blocking=True)
                 ctx.rownorms2(self.S[cur], self.k, self.rowq, div_dev=self.levdiv)
             else:                                                            # sampling.py:143-147
-                ctx.rownorms2(A, g, self.rowq, cols=self.idx[b])
+                ctx.rownorms2(src, g, self.rowq, cols=cols)
             hinfo = self.rec[1 + b, REC_H:]
             ctx.draw(MODE_ROWS, self.rowq, None, self.m, self.uniw[b], self.w, self.ridx[b],
                      self.rcnt[b], info=hinfo, p_out=self.rp[b])
-            ctx.gather_scale_rows(A, self.idx[b], g, self.ridx[b], self.rcnt[b], self.rp[b],
+            ctx.gather_scale_rows(src, cols, g, self.ridx[b], self.rcnt[b], self.rp[b],
                                   self.w, self.hcap, hinfo, self.Y[b])      # sampling.py:248-258
             ctx.tn(g, g, 1.0, self.Y[b], self.Y[b], dptr(self.G[b]), g, tag="tn_gram_rows")
         ctx.gram_eigh(dptr(self.G[b]), g, g, r, self.sig_upd_b[b], dptr(self.Tl[b]), g,
                       info=self.rec[1 + b, REC_RANK:])                       # baselines.py:44-48
-        ctx.nn(g, r, 1.0, A, dptr(self.Tl[b]), g, dest, xcols=self.idx[b],
+        ctx.nn(g, r, 1.0, src, dptr(self.Tl[b]), g, dest, xcols=cols,
                tag="nn_lift_gather")                                         # baselines.py:62-63
 
     def update_side_ops(self, mode, b, join=True):
@@ -503,7 +554,11 @@ class IsmaEngine(MergeWorkspace):
         dev = ctx.device
         U = self.S[self.cur].cols(0, r)
         Cm = ColMat.zeros(n, r, dev)
-        ctx.tn(n, r, 1.0, self.A, U, Cm.ptr, n, tag="tn_finalize_AtU")      # A^T U
+        if self.host_A:                                                      # A^T U, streamed
+            self._stream_columns(lambda Ach, j0, j1: ctx.tn(
+                j1 - j0, r, 1.0, Ach, U, dptr(Cm.t[0], j0), n, tag="tn_finalize_AtU"))
+        else:
+            ctx.tn(n, r, 1.0, self.A, U, Cm.ptr, n, tag="tn_finalize_AtU")  # A^T U
         self.comm.allreduce_sum_(Cm.t)
         Qc = ColMat.zeros(n, r, dev)
         Rc = torch.zeros(r * r, dtype=torch.float64, device=dev)
@@ -660,7 +715,8 @@ def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=
     A and the staged uniforms at replay time, so a reused engine is valid for
     new contents of a buffer it has seen."""
     world = 1 if comm is None else comm.world
-    key = (A.m, A.ncols, A.ld, A.code, int(k), int(r), int(c), criterion, bool(use_graphs),
+    key = (A.m, A.ncols, A.ld, A.code, A.t.is_cuda, int(k), int(r), int(c), criterion,
+           bool(use_graphs),
            ctx.device.index, world, int(row_offset), m_total, int(w))
     lru = _ENGINE_CACHE.setdefault(ctx.device.index, [])
     for i, eng in enumerate(lru):

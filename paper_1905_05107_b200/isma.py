@@ -124,22 +124,29 @@ def _validate_shape(a):
 
 
 def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False,
-             use_graphs=True, comm=None, m_total=None):
+             use_graphs=True, comm=None, m_total=None, residency="auto"):
     """Run the full iteration (isma.py:225-303) on the GPU.
 
     ``a`` may be a numpy array (copied host->device), a CUDA torch tensor
     or a ``device.ColMat`` (used in place).  Returns ``(TruncatedFactor,
     list[IterationTrace])`` exactly as the reference.
 
+    ``residency`` ("auto" | "device" | "host"): where a HOST matrix lives
+    during the run.  "host" keeps it in page-locked host memory read by the
+    kernels over PCIe -- the multi-pass streamed ISMA: one pass
+    for the norms, each round's sampled columns copied into HBM, one pass for
+    finalize (and one per round for "ort") -- for matrices larger than HBM.
+    Results are bit-identical to the device-resident run.  "auto" picks
+    "host" when the matrix would not leave headroom on the device.
+
     Row-sharded multi-GPU (parallel.py): pass ``comm=parallel.Comm()`` and
     this rank's row block ``a`` = A[r0:r1] with r0, r1 = shard_rows(m_total,
     world, rank); every rank must use an identically seeded generator.  The
     returned factor is the full (gathered) one on every rank.
     """
-    from .device import get_ctx, to_device_colmajor
-    from .engine import get_engine
-    from .matcore import TruncatedFactor
+    import torch
 
+    from .device import ColMat, HostResident, get_ctx, to_device_colmajor
     from .parallel import Comm, shard_rows
 
     a, m, n = _validate_shape(a)
@@ -161,7 +168,26 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
     if rng is None:
         rng = np.random.default_rng(config.seed)
     ctx = get_ctx(device)
+    if residency not in ("auto", "device", "host"):
+        raise ParameterError("residency must be 'auto', 'device' or 'host'")
+    on_host = not isinstance(a, ColMat) and not (isinstance(a, torch.Tensor) and a.is_cuda)
+    if on_host and residency == "auto":
+        nbytes = int(np.prod(getattr(a, "shape", (0,)))) * 8
+        free, _ = torch.cuda.mem_get_info(ctx.device)
+        residency = "host" if nbytes > 0.7 * free else "device"
+    if on_host and residency == "host" and not comm.active:
+        with HostResident(a) as A:
+            return _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m,
+                               return_device)
     A = to_device_colmajor(a, ctx.device)
+    return _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m,
+                       return_device)
+
+
+def _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m, return_device):
+    from .engine import get_engine
+    from .matcore import TruncatedFactor
+
     eng = get_engine(ctx, A, k=k, r=config.r, c=config.column_budget(),
                      criterion=config.criterion, use_graphs=use_graphs, comm=comm,
                      row_offset=row_offset, m_total=m if comm.active else None,

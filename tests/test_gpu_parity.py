@@ -325,3 +325,26 @@ def test_float32_storage_matches_fp64_oracle_on_upcast(strategy, rows):
     rep = pod.wedin_measure(a32, f32, 10)
     rep64 = pod.wedin_measure(a64, f64, 10)
     assert abs(rep.measure - rep64.measure) <= 1e-8 * max(1.0, abs(rep64.measure))
+
+
+@pytest.mark.parametrize("strategy,rows,criterion", [("l2n", False, "modes"),
+                                                     ("unf", False, "subspace"),
+                                                     ("ort", False, "modes"),
+                                                     ("ls", True, "modes")])
+def test_host_resident_streamed_run_is_bit_identical(strategy, rows, criterion):
+    """Multi-pass streamed ISMA: A stays in page-locked host
+    memory, read over PCIe (norm pass by the kernel, ort's U^T A and
+    finalize's A^T U on DMA-streamed column chunks) and each round copies its
+    sampled columns into HBM.  Index sets identical to the device-resident
+    run; the chunked products only change split-K summation order (float64
+    and float32 storage)."""
+    a = workloads.config1(seed=0)
+    cfg = pod.IsmaConfig(k=10, r=30, c=50, tau=0.999, strategy=strategy, rows=rows,
+                         w=400 if rows else None, criterion=criterion, seed=7)
+    for mat in (a, a.astype(np.float32)):
+        fd, td = pod.isma_run(mat, cfg, residency="device")
+        fh, th = pod.isma_run(mat, cfg, residency="host")
+        assert [t.remaining for t in th] == [t.remaining for t in td]
+        assert sigma_relerr(fh.sigma, fd.sigma) <= SIGMA_RTOL
+        assert principal_angles_sin(fh.u, fd.u).max() <= ANGLE_TOL_RAD
+        assert principal_angles_sin(fh.v, fd.v).max() <= ANGLE_TOL_RAD
