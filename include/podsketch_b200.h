@@ -155,13 +155,29 @@ int pod_host_unregister(void* ptr);
 int pod_gather_cols(int atype, const void* A, int64_t m, int64_t lda, const int32_t* idx,
                     int64_t g, void* D, int64_t ldd, void* stream);
 
+/* D[:, j] = A[:, idx[j]] * f[j] in fp64 (int64 indices; the materialised,
+ * scaled sample of scale_sampled_columns, sampling.py:234-245, used by the
+ * single-round baselines ltsvd / ctsvd, baselines.py:68-142). */
+int pod_gather_scale_cols(int atype, const void* A, int64_t m, int64_t lda, const int64_t* idx,
+                          const double* f, int64_t g, double* D, int64_t ldd, void* stream);
+
 /* Cap (in CTAs; 0 = none) on the grids of the TN / NN GEMMs launched while
  * set -- host-side state read at launch (and so baked into captured graphs):
  * the pipelined next-round update runs capped beside the critical merge. */
 int pod_set_grid_cap(int ctas);
 
-/* Workspace (bytes) sufficient for any small solve of dimension <= n. */
+/* Workspace (bytes) sufficient for a Gram eigensolve (g = n), a CholeskyQR
+ * factor (l = n) or a merge core (l1 + l2 = n) -- including the block sets
+ * of the grid-wide Jacobi solver that takes sizes beyond one cluster. */
 size_t pod_small_ws_bytes(int64_t n);
+
+/* Largest Gram order g pod_gram_eigh accepts. */
+int64_t pod_gram_eigh_max_g(void);
+
+/* Workspace (bytes) for pod_svd_small of an nr x nc block (V wanted iff
+ * withv): the grid-wide solver's block sets, used only when the cluster
+ * solvers do not fit; 0 when the grid solver does not fit either. */
+size_t pod_svd_small_ws_bytes(int64_t nr, int64_t nc, int withv);
 
 /* gram_spectrum + lift setup (baselines.py:35-65): eigen-decomposition of
  * the PSD Gram G (g x g), descending, eigenvalue dust <= 1e-12 lambda_1

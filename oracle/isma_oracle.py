@@ -217,6 +217,81 @@ def lift(d, sigma, v, r):
     return u, sigma[:keep].copy()
 
 
+def scaled_cols(a, uniq, counts, p, c, dedup=True):
+    """sampling.py:225-245 (_scale_factors + scale_sampled_columns) -- dedup:
+    D = a[:, uniq] * sqrt(t_i / (c p_i)); else one column per draw times
+    1 / sqrt(c p_i).  ``p`` holds the weights of ``uniq``."""
+    if dedup:
+        f, idx = np.sqrt(counts / (c * p)), uniq
+    else:
+        f = 1.0 / np.sqrt(c * np.repeat(p, counts))
+        idx = np.repeat(uniq, counts)
+    return np.asfortranarray(a[:, idx] * f)
+
+
+def scaled_rows_any(d, uniq, counts, p, w, dedup=True):
+    """sampling.py:248-258 for both dedup settings (``p``: weights of uniq)."""
+    if dedup:
+        f, idx = np.sqrt(counts / (w * p)), uniq
+    else:
+        f = 1.0 / np.sqrt(w * np.repeat(p, counts))
+        idx = np.repeat(uniq, counts)
+    return np.asfortranarray(d[idx, :] * f[:, None])
+
+
+def ltsvd(a, cand, weights, k, c, rng, dedup=True):
+    """baselines.py:68-109 -- one column draw, scaled sample, Gram eigh,
+    lift of min(k, rank) modes.  Returns (u, sigma, draw)."""
+    uniq, cnt = cdf_draw(cand, weights, rng.random(int(c)))
+    p = weights[np.searchsorted(cand, uniq)]
+    d = scaled_cols(a, uniq, cnt, p, c, dedup)
+    sig, v = gram_eig(d)
+    u, s = lift(d, sig, v, k)
+    return u, s, (uniq, cnt)
+
+
+def ctsvd(a, cand, weights, k, c, w, epsilon, rng, dedup=True):
+    """baselines.py:112-142 -- column draw, row draw from the sample's row
+    norms, Gram eigh of the row sample, energy filter gamma = eps/(100k),
+    lift through the column sample.  Returns (u, sigma)."""
+    uniq, cnt = cdf_draw(cand, weights, rng.random(int(c)))
+    p = weights[np.searchsorted(cand, uniq)]
+    dc = scaled_cols(a, uniq, cnt, p, c, dedup)
+    q = row_weights(dc)
+    ridx, rcnt = cdf_draw(np.arange(dc.shape[0]), q, rng.random(int(w)))
+    dw = scaled_rows_any(dc, ridx, rcnt, q[ridx], w, dedup)
+    sig, v = gram_eig(dw)
+    gamma = epsilon / (100.0 * k)
+    frob2 = float(np.sum(sig * sig))
+    passing = int(np.count_nonzero(sig * sig >= gamma * frob2))
+    return lift(dc, sig, v, min(k, passing))
+
+
+def dense_svd(a):
+    """matcore.py:178-197 -- thin SVD (gesdd, gesvd fallback), canonical
+    signs.  Returns (u, sigma, v)."""
+    u, s, vt = lapack_svd(dense_f64(a))
+    u, v = canon_signs(u, vt.T)
+    return u, s, v
+
+
+def pod_via_gram(a, k):
+    """matcore.py:213-241 -- top-k eigenpairs of A^T A (dsyevr subset),
+    descending, clipped, dust dropped, u = A v / sigma, canonical signs.
+    Returns (u, sigma, v)."""
+    a = dense_f64(a)
+    n = a.shape[1]
+    lam, v = sla.eigh(a.T @ a, subset_by_index=(n - k, n - 1))
+    lam = np.clip(lam[::-1], 0.0, None)
+    v = v[:, ::-1]
+    sigma = np.sqrt(lam)
+    keep = lam > GRAM_DUST_RTOL * max(lam[0], np.finfo(float).tiny)
+    sigma, v = sigma[keep], v[:, keep]
+    u = (a @ v) / sigma
+    u, v = canon_signs(u, v)
+    return u, sigma, v
+
+
 def merge(u1, s1, u2, s2, r):
     """merge.py:37-91 -- BLOCK MERGE at rank r (no right vectors)."""
     u1, s1 = u1[:, :r], s1[:r]

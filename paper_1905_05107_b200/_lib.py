@@ -55,9 +55,12 @@ SIGNATURES = {
                            _i64, _vp, _i64, _vp, _vp]),
     "pod_set_grid_cap": (_i32, [_i32]),
     "pod_gather_cols": (_i32, [_i32, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "pod_gather_scale_cols": (_i32, [_i32, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp]),
     "pod_host_register": (_i32, [_vp, _sz]),
     "pod_host_unregister": (_i32, [_vp]),
     "pod_small_ws_bytes": (_sz, [_i64]),
+    "pod_svd_small_ws_bytes": (_sz, [_i64, _i64, _i32]),
+    "pod_gram_eigh_max_g": (_i64, []),
     "pod_gram_eigh": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "pod_cholqr_factor": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp,
                                  _vp, _i32, _vp]),

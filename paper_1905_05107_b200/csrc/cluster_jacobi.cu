@@ -687,6 +687,22 @@ int cj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int6
   }
 }
 
+// Whether the cluster solver's shared-memory layout fits (same byte counts
+// as the launches above); callers route larger problems to grid_jacobi.cu.
+template <int CL>
+static bool cj_fits_t(int64_t nc, int64_t nr, int64_t njr) {
+  const int64_t nrl = (nr + CL - 1) / CL, njl = (njr + CL - 1) / CL;
+  return cj_scratch_bytes<CL>((int)nc) + (size_t)(nrl + njl) * nc * sizeof(double) <= CJ_SMEM_CAP;
+}
+bool cj_fits(int64_t nc, int64_t nr, int64_t njr) {
+  if (nc > CJ_MAX_N || nr > 4096) return false;
+  switch (cj_cluster()) {
+    case 2: return cj_fits_t<2>(nc, nr, njr);
+    case 4: return cj_fits_t<4>(nc, nr, njr);
+    default: return cj_fits_t<8>(nc, nr, njr);
+  }
+}
+
 }  // namespace pod
 
 #ifdef POD_CJ_TIMING

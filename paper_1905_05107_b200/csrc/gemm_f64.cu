@@ -935,12 +935,11 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
   POD_REQUIRE(m >= 0 && p >= 0 && q >= 0, "pod_gemm_nn_f64: negative size");
   if (m == 0 || q == 0) return POD_OK;
   POD_REQUIRE(ldy >= m, "pod_gemm_nn_f64: ldy < m");
-  POD_REQUIRE(q <= 192, "pod_gemm_nn_f64: q=%lld > 192 output columns", (long long)q);
   POD_REQUIRE(beta == 0.0 || Z != nullptr, "pod_gemm_nn_f64: beta != 0 needs Z");
   int st = ensure_attrs();
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
-  {
+  if (q <= 192) {
     const int bn = q <= 64 ? 64 : (q <= 128 ? 128 : 192);
     const size_t bytes = nnp::smem_bytes((int)p, bn);
     if (p >= 1 && bytes <= 110 * 1024) {  // T resident, 2 CTAs/SM: persistent kernel
@@ -974,7 +973,10 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
       return a0 < y1 && y0 < a1;
     };
     const bool alias = overlaps(X, ldx, p) || (beta != 0.0 && overlaps(Z, ldz, q));
-    if (q <= 64 || (!alias && nn_groups_enabled())) {
+    // > 192 output columns: column groups only (each group reads all of X)
+    POD_REQUIRE(q <= 192 || !alias, "pod_gemm_nn_f64: in-place update with q=%lld > 192",
+                (long long)q);
+    if (q <= 64 || q > 192 || (!alias && nn_groups_enabled())) {
       if (nn_groups80(q)) {  // groups of 80 pad less (q = 150: 160 vs 192)
         using C80 = nns::Cfg<80>;
         const int64_t nblk = ceil_div(m, C80::BM);

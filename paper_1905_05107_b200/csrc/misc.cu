@@ -250,3 +250,42 @@ extern "C" int pod_gather_cols(int atype, const void* A, int64_t m, int64_t lda,
   POD_CHECK_LAUNCH("gather cols");
   return POD_OK;
 }
+
+// D[:, j] = A[:, idx[j]] * f[j] in fp64 (scale_sampled_columns, sampling.py:
+// 234-245: one column per index, already repeated/deduplicated by the caller)
+namespace pod {
+template <typename T>
+__global__ void __launch_bounds__(256) gather_scale_cols_kernel(const T* __restrict__ A, int64_t m,
+                                                                int64_t lda,
+                                                                const int64_t* __restrict__ idx,
+                                                                const double* __restrict__ f, int g,
+                                                                double* __restrict__ D, int64_t ldd) {
+  for (int j = blockIdx.y; j < g; j += gridDim.y) {
+    const T* src = A + idx[j] * lda;
+    double* dst = D + (int64_t)j * ldd;
+    const double s = f[j];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+      dst[i] = (double)src[i] * s;
+  }
+}
+}  // namespace pod
+
+extern "C" int pod_gather_scale_cols(int atype, const void* A, int64_t m, int64_t lda,
+                                     const int64_t* idx, const double* f, int64_t g, double* D,
+                                     int64_t ldd, void* stream) {
+  POD_REQUIRE(atype == POD_F64 || atype == POD_F32, "pod_gather_scale_cols: bad operand type");
+  POD_REQUIRE(m >= 1 && g >= 0 && lda >= m && ldd >= m, "pod_gather_scale_cols: bad shape");
+  if (g == 0) return POD_OK;
+  const int gx = (int)std::min<int64_t>(ceil_div(m, 256 * 4), 64);
+  dim3 grid((unsigned)std::max(1, gx), (unsigned)std::min<int64_t>(g, 1024));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (atype == POD_F64)
+    gather_scale_cols_kernel<double><<<grid, 256, 0, s>>>((const double*)A, m, lda, idx, f, (int)g,
+                                                          D, ldd);
+  else
+    gather_scale_cols_kernel<float><<<grid, 256, 0, s>>>((const float*)A, m, lda, idx, f, (int)g,
+                                                         D, ldd);
+  POD_CHECK_LAUNCH("gather scale cols");
+  return POD_OK;
+}

@@ -409,6 +409,22 @@ int cj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t g
                  double* sigma, double* T, int64_t ldt, int64_t* info, cudaStream_t stream);
 int cj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int64_t ldu,
            double* sigma, double* V, int64_t ldv, int64_t* info, cudaStream_t stream);
+bool cj_fits(int64_t nc, int64_t nr, int64_t njr);
+size_t gj_ws_bytes(int64_t n, int64_t nrows, int64_t njrows);
+size_t gj_gram_large_ws_bytes(int64_t g);
+int gj_gram_eigh_large(const double* G, int64_t ldg, int64_t g, int64_t r, double* sigma,
+                       double* T, int64_t ldt, int64_t* info, void* ws, size_t ws_bytes,
+                       cudaStream_t s);
+int gj_gram_eigh(const double* X, int64_t ldx, const int* piv, const int64_t* rank, int64_t g,
+                 int64_t r, double* sigma, double* T, int64_t ldt, int64_t* info, void* ws,
+                 size_t ws_bytes, cudaStream_t s);
+int gj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int64_t ldu,
+           double* sigma, double* V, int64_t ldv, int64_t* info, void* ws, size_t ws_bytes,
+           cudaStream_t s);
+int gj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
+                  int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
+                  int64_t ldt, int64_t tcols, double* sig_new, int64_t* info, void* ws,
+                  size_t ws_bytes, cudaStream_t s);
 
 }  // namespace pod
 
@@ -420,17 +436,49 @@ static size_t gram_ws_bytes(int64_t g) {
   return (size_t)g * g * 8 + (size_t)g * 4 + 64 + 2 * (size_t)g * g * 8;
 }
 
+// Solver routing by size: block Jacobi on one cluster (block_jacobi.cu),
+// then the row-distributed cluster solver (cluster_jacobi.cu), then the
+// grid-wide solver with L2-resident blocks (grid_jacobi.cu), whose block
+// sets live in the caller's workspace.  Gram eigensolves beyond g = 512 skip
+// the pivoted Cholesky and run one-sided Jacobi on G itself.
+constexpr int64_t PIVCHOL_MAX_G = 512;
+
+static size_t gram_total_ws(int64_t g) {
+  if (g > PIVCHOL_MAX_G) return gj_gram_large_ws_bytes(g);
+  return gram_ws_bytes(g) + gj_ws_bytes(g, g, 0);
+}
+
 extern "C" size_t pod_small_ws_bytes(int64_t n) {
-  return std::max(gram_ws_bytes(n), cholqr_bytes(n));
+  return std::max(std::max(gram_total_ws(n), cholqr_bytes(n)),
+                  std::max(gj_ws_bytes(n, n, n), gj_ws_bytes(n, n, 0)));
+}
+
+extern "C" int64_t pod_gram_eigh_max_g(void) {
+  static int64_t v = 0;
+  if (!v) {  // feasibility is monotone in g: bisect on the grid solver's fit
+    int64_t lo = PIVCHOL_MAX_G, hi = 1 << 16;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) / 2;
+      (gj_gram_large_ws_bytes(mid) ? lo : hi) = mid;
+    }
+    v = lo;
+  }
+  return v;
+}
+
+extern "C" size_t pod_svd_small_ws_bytes(int64_t nr, int64_t nc, int withv) {
+  if (nr < 1 || nc < 1) return 0;
+  return gj_ws_bytes(nc, nr, withv ? nc : 0);
 }
 
 extern "C" int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r, double* sigma,
                              double* T, int64_t ldt, int64_t* info, void* ws, size_t ws_bytes,
                              void* stream) {
   POD_REQUIRE(g >= 1 && r >= 1 && ldg >= g && ldt >= g, "pod_gram_eigh: bad shape");
-  POD_REQUIRE(g <= 512, "pod_gram_eigh: g=%lld exceeds 512", (long long)g);
-  POD_REQUIRE(ws_bytes >= gram_ws_bytes(g), "pod_gram_eigh: workspace too small");
+  POD_REQUIRE(ws_bytes >= gram_total_ws(g), "pod_gram_eigh: workspace too small");
   cudaStream_t s = (cudaStream_t)stream;
+  if (g > PIVCHOL_MAX_G)
+    return gj_gram_eigh_large(G, ldg, g, r, sigma, T, ldt, info, ws, ws_bytes, s);
   double* X = (double*)ws;
   int* piv = (int*)(X + (size_t)g * g);
   int64_t* rank = (int64_t*)(((uintptr_t)(piv + g) + 15) & ~(uintptr_t)15);
@@ -458,7 +506,10 @@ extern "C" int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r,
     const int bst = bj_gram_eigh(X, piv, rank, g, r, sigma, T, ldt, info, s);
     if (bst != -1) return bst;  // -1: size not handled by the block solver
   }
-  return cj_gram_eigh(X, piv, rank, g, r, sigma, T, ldt, info, s);
+  if (cj_fits(g, g, 0)) return cj_gram_eigh(X, piv, rank, g, r, sigma, T, ldt, info, s);
+  const size_t head = gram_ws_bytes(g);
+  return gj_gram_eigh(X, g, piv, rank, g, r, sigma, T, ldt, info, (char*)ws + head,
+                      ws_bytes - head, s);
 }
 
 extern "C" int pod_cholqr_factor(const double* G, int64_t ldg, int64_t l, int64_t nrows,
@@ -489,24 +540,25 @@ extern "C" int pod_merge_core(const double* sig1, int64_t l1, const double* M, i
                               void* stream) {
   POD_REQUIRE(l1 >= 1 && l2 >= 1 && r >= 1 && rcap >= l1 && ldt >= rcap + l2 && tcols >= 1,
               "pod_merge_core: bad shape");
-  (void)ws;
-  (void)ws_bytes;
   const int bst = bj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols,
                                 sig_new, info, (cudaStream_t)stream);
   if (bst != -1) return bst;  // -1: size not handled by the block solver
-  return cj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info,
-                       (cudaStream_t)stream);
+  if (cj_fits(l1 + l2, l1 + l2, 0))
+    return cj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new,
+                         info, (cudaStream_t)stream);
+  return gj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info,
+                       ws, ws_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int pod_svd_small(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U,
                              int64_t ldu, double* sigma, double* V, int64_t ldv, int64_t* info,
                              void* ws, size_t ws_bytes, void* stream) {
   POD_REQUIRE(nr >= 1 && nc >= 1 && lda >= nr && nr >= nc, "pod_svd_small: bad shape");
-  (void)ws;
-  (void)ws_bytes;
   const int bst = bj_svd(A, lda, nr, nc, U, ldu, sigma, V, ldv, info, (cudaStream_t)stream);
   if (bst != -1) return bst;  // -1: size not handled by the block solver
-  return cj_svd(A, lda, nr, nc, U, ldu, sigma, V, ldv, info, (cudaStream_t)stream);
+  if (cj_fits(nc, nr, V ? nc : 0))
+    return cj_svd(A, lda, nr, nc, U, ldu, sigma, V, ldv, info, (cudaStream_t)stream);
+  return gj_svd(A, lda, nr, nc, U, ldu, sigma, V, ldv, info, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 extern "C" int pod_small_gemm(int64_t p, int64_t q, int64_t k, double alpha, const double* A,

@@ -174,6 +174,11 @@ class Ctx:
         self._call("gather_cols", 1, 0.0, 2.0 * A.esize * A.m * g, "pod_gather_cols", A.code,
                    A.ptr, A.m, A.ld, _ptr(idx), g, D.ptr, D.ld, self.stream)
 
+    def gather_scale_cols(self, A, idx64, f, g, D):
+        self._call("gather_scale_cols", 1, 0.0, (A.esize + 8.0) * A.m * g,
+                   "pod_gather_scale_cols", A.code, A.ptr, A.m, A.ld, _ptr(idx64), _ptr(f), g,
+                   D.ptr, D.ld, self.stream)
+
     def resid_colnorms2(self, A, n, U, r, C, ldc, out, cols=None):
         ws = self.ws("resid", _lib.load().pod_resid_ws_bytes(A.m, n))
         self._call("resid_colnorms2", 2, 2.0 * A.m * n * r, A.m * (A.esize * n + 8.0 * r),
@@ -229,7 +234,8 @@ class Ctx:
                   self.stream)
 
     def svd_small(self, A, lda, nr, nc, U, ldu, sigma, V, ldv):
-        ws = self.small_ws(max(nr, nc))
+        ws = self.ws("small", max(_lib.load().pod_svd_small_ws_bytes(nr, nc, int(V is not None)),
+                                  _lib.load().pod_small_ws_bytes(min(nr, nc))))
         self._call("svd_small", 1, 0.0, 8.0 * nr * nc, "pod_svd_small", A, lda, nr, nc, U, ldu, _ptr(sigma), V, ldv, _ptr(self.info),
                   _ptr(ws), ws.numel(), self.stream)
 

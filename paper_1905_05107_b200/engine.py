@@ -70,6 +70,10 @@ G_FQR = 11          # finalize CholeskyQR passes: 11..15
 N_GATES = 16
 
 
+#: widest in-place Q <- Q R^-1 the NN kernel takes (pod_gemm_nn_f64)
+NN_INPLACE_MAX_Q = 192
+
+
 class MergeWorkspace:
     """Buffers and launch sequences of BLOCK MERGE at rank r for m-row
     factors (used by the ISMA engine, block_merge and the one-pass
@@ -174,7 +178,11 @@ class MergeWorkspace:
                 self.comm.allreduce_sum_(self.Gq)
             ctx.cholqr_factor(dptr(self.Gq), r, l, Q.m, dptr(self.Rinv), r, dptr(self.Rk), r,
                               gate_in=gp, gate_out=self.gate(gate_base + p + 1), first_pass=0)
-            ctx.nn(l, l, 1.0, Q, dptr(self.Rinv), r, Q, gate=gp, tag="nn_cholqr_apply")
+            if l <= NN_INPLACE_MAX_Q:
+                ctx.nn(l, l, 1.0, Q, dptr(self.Rinv), r, Q, gate=gp, tag="nn_cholqr_apply")
+            else:  # wider than the in-place NN kernel: through the scratch block
+                ctx.nn(l, l, 1.0, Q, dptr(self.Rinv), r, tmp, gate=gp, tag="nn_cholqr_apply")
+                ctx.small_copy(Q.m, l, tmp.ptr, tmp.ld, Q.ptr, Q.ld, gate=gp)
             ctx.small_gemm(l, l, l, 1.0, dptr(self.Rk), r, 0, dptr(Rout), r, 0.0,
                            dptr(self.Rtmp), r, gate=gp)
             ctx.small_copy(l, l, dptr(self.Rtmp), r, dptr(Rout), r, gate=gp)
@@ -305,6 +313,10 @@ class IsmaEngine(MergeWorkspace):
         self.n = A.ncols
         self.c = int(c)
         gcap = min(self.c, A.ncols)
+        gmax = int(_lib.load().pod_gram_eigh_max_g())
+        if gcap > gmax:
+            raise ParameterError(f"column budget c={self.c} can draw {gcap} distinct columns; "
+                                 f"the sampled-Gram eigensolver takes at most {gmax}")
         super().__init__(ctx, A.m, r, k=k, criterion=criterion, upd_cap=gcap, comm=comm,
                          row_offset=row_offset, nupd=2)
         self.m_total = A.m if m_total is None else int(m_total)

@@ -168,3 +168,147 @@ def ctsvd_sample_count(k, epsilon, delta):
     _check_count_params(k, epsilon, delta)
     return int(math.ceil(float(k * k) * (1.0 + math.sqrt(math.log(2.0 / delta))) ** 2
                          / epsilon ** 4))
+
+
+# ---------------------------------------------------------------------------
+# Row / residual / leverage distributions and sample scaling (sampling.py:
+# 143-258), computed with the library's kernels; the results are host values
+# as in the reference.
+
+def _dev(a):
+    from .device import ColMat, get_ctx, to_device_colmajor
+
+    ctx = get_ctx()
+    return ctx, (a if isinstance(a, ColMat) else to_device_colmajor(a, ctx.device))
+
+
+def row_norm_distribution(d):
+    """Distribution over all rows of ``d`` proportional to squared norms
+    (sampling.py:143-147)."""
+    import torch
+
+    ctx, D = _dev(d)
+    out = torch.empty(D.m, dtype=torch.float64, device=ctx.device)
+    ctx.rownorms2(D, D.ncols, out)
+    return Distribution.from_weights(np.arange(D.m), out.cpu().numpy(), what="row")
+
+
+def leverage_distribution(u):
+    """Row distribution from the leverage scores ||u_i||^2 / k of an
+    orthonormal basis (sampling.py:190-201)."""
+    import torch
+
+    if np.ndim(u) != 2 or np.shape(u)[1] == 0:
+        raise ParameterError("u must be 2-D with at least one column")
+    ctx, U = _dev(u)
+    out = torch.empty(U.m, dtype=torch.float64, device=ctx.device)
+    ctx.rownorms2(U, U.ncols, out, div=float(U.ncols))
+    return Distribution.from_weights(np.arange(U.m), out.cpu().numpy(), what="leverage")
+
+
+def residual_distribution(a, u, candidates=None, *, degenerate_rtol=1e-14):
+    """Weights proportional to the squared residual of each candidate column
+    after projection on the orthonormal ``u`` (sampling.py:158-187): C =
+    U^T A[:, S] and ||a_j - U c_j||^2 in one fused pass, never materialised.
+    Raises DegenerateDistributionError when the residual total is at most
+    ``degenerate_rtol * ||A||_F^2``."""
+    import torch
+
+    from .device import dptr
+
+    a_shape = np.shape(a)
+    if candidates is None:
+        candidates = np.arange(a_shape[1])
+    candidates = np.asarray(candidates, dtype=np.int64)
+    if candidates.size == 0:
+        raise ParameterError("candidate set is empty")
+    if np.ndim(u) != 2 or np.shape(u)[0] != a_shape[0]:
+        raise ParameterError("u must be 2-D with the same row count as a")
+    if np.shape(u)[1] == 0:
+        return column_norm_distribution(a, candidates)
+    ctx, A = _dev(a)
+    _, U = _dev(u if not isinstance(u, np.ndarray) else np.asarray(u, dtype=np.float64))
+    dev = ctx.device
+    g, r = candidates.size, U.ncols
+    cols = torch.as_tensor(candidates.astype(np.int32), device=dev)
+    C = torch.empty(r * g, dtype=torch.float64, device=dev)
+    ctx.tn(r, g, 1.0, U, A, dptr(C), r, ycols=cols, tag="tn_resid_proj")
+    res2 = torch.empty(g, dtype=torch.float64, device=dev)
+    ctx.resid_colnorms2(A, g, U, r, dptr(C), r, res2, cols=cols)
+    norms = torch.empty(A.ncols, dtype=torch.float64, device=dev)
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    ctx.colnorms2(A, norms, flag)
+    res2 = res2.cpu().numpy()
+    total = res2.sum()
+    if total <= degenerate_rtol * float(norms.sum().item()):
+        raise DegenerateDistributionError(
+            "candidate columns are fully captured by the current basis")
+    return Distribution(candidates, res2 / total)
+
+
+def _scale_factors(dist, draw, total, dedup):
+    """sampling.py:225-231 (host scalars, same formulas)."""
+    from .errors import PodsketchError
+
+    p = dist.weight_of(draw.unique_indices)
+    if np.any(p <= 0.0):
+        raise PodsketchError("drawn index has zero weight; sampler invariant broken")
+    if dedup:
+        return np.sqrt(draw.counts / (total * p))
+    return 1.0 / np.sqrt(total * np.repeat(p, draw.counts))
+
+
+def _scale_columns_dev(a, draw, dist, c, dedup):
+    import torch
+
+    from .device import ColMat
+
+    f = _scale_factors(dist, draw, c, dedup)
+    idx = draw.unique_indices if dedup else np.repeat(draw.unique_indices, draw.counts)
+    ctx, A = _dev(a)
+    dev = ctx.device
+    D = ColMat.zeros(A.m, idx.size, dev)
+    ctx.gather_scale_cols(A, torch.as_tensor(idx.astype(np.int64), device=dev),
+                          torch.as_tensor(f, dtype=torch.float64, device=dev), idx.size, D)
+    return D
+
+
+def scale_sampled_columns(a, draw, dist, c, dedup=True):
+    """The scaled sample (sampling.py:234-245): dedup -> one column per
+    distinct index scaled by sqrt(t_i / (c p_i)), so D D^T = C C^T; else one
+    column per draw scaled by 1/sqrt(c p_i).  Gathered and scaled on the
+    device with the host-computed factors (bit-identical products)."""
+    return _scale_columns_dev(a, draw, dist, c, dedup).to_numpy()
+
+
+def _scale_rows_dev(c, draw, dist, w, dedup):
+    import torch
+
+    from .device import ColMat
+    from .errors import PodsketchError
+
+    if dedup:
+        rows, cnt = draw.unique_indices, draw.counts
+    else:
+        rows = np.repeat(draw.unique_indices, draw.counts)
+        cnt = np.ones(rows.size, dtype=np.int64)
+    p = dist.weight_of(rows)
+    if np.any(p <= 0.0):
+        raise PodsketchError("drawn index has zero weight; sampler invariant broken")
+    ctx, Cm = _dev(c)
+    dev = ctx.device
+    h = rows.size
+    Y = ColMat.zeros(h, Cm.ncols, dev)
+    hdev = torch.tensor([h], dtype=torch.int64, device=dev)
+    ctx.gather_scale_rows(Cm, None, Cm.ncols, torch.as_tensor(rows.astype(np.int32), device=dev),
+                          torch.as_tensor(cnt.astype(np.int64), device=dev),
+                          torch.as_tensor(p, dtype=torch.float64, device=dev), float(w), h, hdev,
+                          Y)
+    return Y
+
+
+def scale_sampled_rows(c, draw, dist, w, dedup=True):
+    """Row counterpart (sampling.py:248-258): dedup -> one row per distinct
+    index scaled by sqrt(t_i / (w q_i)), so Y^T Y = W^T W; else one row per
+    draw scaled by 1/sqrt(w q_i).  Gathered and scaled on the device."""
+    return _scale_rows_dev(c, draw, dist, w, dedup).to_numpy()

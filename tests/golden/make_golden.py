@@ -157,6 +157,43 @@ def main():
                         remaining=np.array([t.remaining for t in tr], dtype=np.int64),
                         seed=np.int64(2))
 
+    # single-round baselines (baselines.py:68-142) and exact factorizations
+    # (matcore.py:187-254); draws recorded through the baselines module's name
+    import podsketch.baselines as ref_base
+
+    ref_base.sample_with_replacement = _recording_sample
+    base = {}
+    dist = podsketch.column_norm_distribution(a1)
+    for tag, fn in (
+            ("lt", lambda dd: podsketch.ltsvd(a1, dist, 10, 50, np.random.default_rng(3),
+                                              dedup=dd)),
+            ("ct", lambda dd: podsketch.ctsvd(a1, dist, 10, 60, 300, 0.7,
+                                              np.random.default_rng(4), dedup=dd)),
+            ("ctf", lambda dd: podsketch.ctsvd(a1, dist, 10, 60, 300, 30.0,
+                                               np.random.default_rng(4), dedup=dd))):
+        for dd in (True, False):
+            DRAWS.clear()
+            f = fn(dd)
+            key = f"{tag}{int(dd)}"
+            base[f"{key}_u"], base[f"{key}_s"] = f.u, f.sigma
+            base[f"{key}_idx"] = DRAWS[0][0]
+            base[f"{key}_cnt"] = DRAWS[0][1]
+    gen = np.random.default_rng(21)
+    mats = {"tall": gen.standard_normal((300, 40)), "wide": gen.standard_normal((40, 300)),
+            "skinny": gen.standard_normal((5000, 30)) * np.logspace(0, -6, 30)}
+    for name, x in mats.items():
+        f = podsketch.dense_svd(x)
+        base[f"svd_{name}_a"], base[f"svd_{name}_u"] = x, f.u
+        base[f"svd_{name}_s"], base[f"svd_{name}_v"] = f.sigma, f.v
+    f = podsketch.pod_via_gram(a1, 10)
+    base["gram_u"], base["gram_s"], base["gram_v"] = f.u, f.sigma, f.v
+    q, rr = podsketch.matcore.thin_qr(mats["tall"])
+    base["qr_q"], base["qr_r"] = q, rr
+    near = np.linalg.qr(gen.standard_normal((300, 20)))[0] + 1e-7 * gen.standard_normal((300, 20))
+    q, sv = podsketch.matcore.orthonormalize(near)
+    base["orth_in"], base["orth_q"], base["orth_s"] = near, q, sv
+    np.savez_compressed(os.path.join(HERE, "baselines.npz"), **base)
+
     # Wedin report (quality.py:82-118) for the config-1 finalized factor, keep=k+1
     cfg = podsketch.IsmaConfig(k=10, r=30, c=50, tau=0.99, strategy="l2n", seed=7)
     f, _ = podsketch.isma_run(a1, cfg, keep=11)

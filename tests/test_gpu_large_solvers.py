@@ -1,0 +1,120 @@
+"""Problem sizes beyond one thread-block cluster's shared memory: the
+grid-wide Jacobi solver (csrc/grid_jacobi.cu, with a grid-wide pivoted Cholesky beyond g = 512) behind
+pod_gram_eigh,
+pod_svd_small and pod_merge_core, the NN kernel's column groups beyond 192
+output columns, and ISMA runs that need them -- the reference's default
+column budget (c = ltsvd_sample_count(k, 0.7, 0.6) = 746 at k = 10) and a
+rank r = 3k = 300 run."""
+
+import numpy as np
+import pytest
+from parity_util import ANGLE_TOL_RAD, SIGMA_RTOL, principal_angles_sin, sigma_relerr
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_1905_05107_b200 as pod  # noqa: E402
+from oracle import isma_oracle as orc  # noqa: E402
+from paper_1905_05107_b200 import workloads  # noqa: E402
+from paper_1905_05107_b200.device import dptr, get_ctx  # noqa: E402
+
+
+def _spectrum(n, rng, decay=40.0):
+    q = np.linalg.qr(rng.standard_normal((n, n)))[0]
+    lam = np.exp(-np.arange(n) / decay)
+    return (q * lam) @ q.T, lam, q
+
+
+@pytest.mark.parametrize("g", [400, 450, 700, 1300, 2000])
+def test_gram_eigh_beyond_one_cluster(g):
+    rng = np.random.default_rng(g)
+    G, lam, q = _spectrum(g, rng)
+    G = (G + G.T) / 2
+    ctx = get_ctx()
+    dev = ctx.device
+    Gd = torch.as_tensor(np.asfortranarray(G).T.copy().reshape(-1), device=dev)
+    r = 12
+    sig = torch.empty(g, dtype=torch.float64, device=dev)
+    T = torch.empty(g * r, dtype=torch.float64, device=dev)
+    info = torch.zeros(4, dtype=torch.int64, device=dev)
+    ctx.gram_eigh(dptr(Gd), g, g, r, sig, dptr(T), g, info=info)
+    s = sig.cpu().numpy()
+    want = np.sqrt(np.where(lam > 1e-12 * lam[0], lam, 0.0))
+    # the eigenvalues of the rounded G carry eps * lambda_1 absolute error
+    assert np.abs(s ** 2 - want ** 2).max() <= 1e-13 * lam[0] * np.sqrt(g)
+    inf = info.cpu().numpy()
+    assert inf[1] == r and 0 < inf[2] < 60
+    v = T.view(r, g).cpu().numpy().T * s[:r]
+    assert principal_angles_sin(v, q[:, :r]).max() <= 1e-9
+
+
+@pytest.mark.parametrize("shape", [(1000, 700), (700, 1000), (6000, 800)])
+def test_dense_svd_grid_solver_matches_oracle(shape):
+    rng = np.random.default_rng(sum(shape))
+    a = rng.standard_normal(shape) * np.logspace(0, -4, shape[1])
+    f = pod.dense_svd(a)
+    u, s, v = orc.dense_svd(a)
+    assert sigma_relerr(f.sigma, s) <= SIGMA_RTOL
+    k = 20
+    assert principal_angles_sin(f.u[:, :k], u[:, :k]).max() <= ANGLE_TOL_RAD
+    np.testing.assert_allclose(f.u[:, :k], u[:, :k], atol=1e-8)
+    np.testing.assert_allclose(f.v[:, :k], v[:, :k], atol=1e-8)
+
+
+@pytest.mark.parametrize("n", [700, 1500])
+def test_pod_via_gram_wide(n):
+    rng = np.random.default_rng(n)
+    a = (np.linalg.qr(rng.standard_normal((3000, 10)))[0] * np.linspace(10, 1, 10)) @ \
+        np.linalg.qr(rng.standard_normal((n, 10)))[0].T + 1e-3 * rng.standard_normal((3000, n))
+    f = pod.pod_via_gram(a, 8)
+    u, s, v = orc.pod_via_gram(a, 8)
+    assert sigma_relerr(f.sigma, s) <= 1e-10
+    np.testing.assert_allclose(f.u, u, atol=1e-8)
+    np.testing.assert_allclose(f.v, v, atol=1e-8)
+
+
+def test_block_merge_wide_core_matches_oracle():
+    """l1 + l2 = 640: the E-SVD runs on the grid solver; the merge GEMMs
+    have 320 output columns (column groups)."""
+    rng = np.random.default_rng(5)
+    m, k1 = 2000, 320
+    f1 = pod.TruncatedFactor(np.linalg.qr(rng.standard_normal((m, k1)))[0],
+                             np.sort(rng.random(k1) + 0.5)[::-1].copy())
+    f2 = pod.TruncatedFactor(np.linalg.qr(rng.standard_normal((m, k1)))[0],
+                             np.sort(rng.random(k1) + 0.5)[::-1].copy())
+    out = pod.block_merge(f1, f2, 300)
+    u, s = orc.merge(f1.u, f1.sigma, f2.u, f2.sigma, 300)
+    assert sigma_relerr(out.sigma, s) <= SIGMA_RTOL
+    assert principal_angles_sin(out.u[:, :50], u[:, :50]).max() <= 1e-7
+    out.validate(1e-10)
+
+
+def test_isma_reference_default_column_budget_cfg1():
+    """IsmaConfig(k=10) with the reference default c = 746 on config 1: the
+    rounds run at capacity g = min(c, n) = 500 sampled columns, beyond one
+    cluster's shared memory."""
+    a = workloads.config1(seed=0)
+    cfg = pod.IsmaConfig(k=10, seed=0)
+    c = cfg.column_budget()
+    assert c == orc.ltsvd_count(10, 0.7, 0.6) == 746
+    f, tr = pod.isma_run(a, cfg, rng=np.random.default_rng(3))
+    o = orc.run(a, 10, c=c, tau=cfg.tau, strategy=cfg.strategy, rng=np.random.default_rng(3))
+    assert [t.remaining for t in tr] == [t["remaining"] for t in o["trace"]]
+    assert min(c, a.shape[1]) == 500
+    assert sigma_relerr(f.sigma, o["sigma"]) <= SIGMA_RTOL
+    assert principal_angles_sin(f.u, o["u"]).max() <= ANGLE_TOL_RAD
+
+
+def test_isma_rank_300():
+    """k = 100, r = 300: merge cores of 600 columns, NN updates with 300
+    output columns, CholeskyQR passes through the scratch block."""
+    a = workloads.config1(seed=1, m=3000, n=1200)
+    cfg = pod.IsmaConfig(k=100, c=400, tau=0.999, strategy="l2n", seed=2)
+    f, tr = pod.isma_run(a, cfg, rng=np.random.default_rng(4))
+    o = orc.run(a, 100, c=400, tau=0.999, strategy="l2n", rng=np.random.default_rng(4))
+    assert [t.remaining for t in tr] == [t["remaining"] for t in o["trace"]]
+    f.validate(1e-9)
+    assert sigma_relerr(f.sigma[:50], o["sigma"][:50]) <= 1e-9
+    assert principal_angles_sin(f.u[:, :30], o["u"][:, :30]).max() <= 1e-7

@@ -114,3 +114,41 @@ def test_budget_formula():
     # reference tests/test_sampling.py:363-373 (acceptance 8): k=1, eps=1, delta=0.5
     assert orc.ltsvd_count(10, 0.7, 0.6) == 746
     assert orc.ltsvd_count(20, 0.7, 0.6) == 1491
+
+
+def _cfg1_weights():
+    a1 = workloads.config1(seed=0)
+    return a1, np.arange(a1.shape[1]), orc.normalized_weights(orc.column_norms2(a1))
+
+
+@pytest.mark.parametrize("dedup", [True, False])
+def test_single_round_baselines_match_reference(dedup):
+    """oracle ltsvd / ctsvd (baselines.py:68-142) == the reference run in
+    make_golden.py: identical draws, factors to rounding."""
+    g = load_golden("baselines")
+    a1, cand, wts = _cfg1_weights()
+    key = f"lt{int(dedup)}"
+    u, s, (idx, cnt) = orc.ltsvd(a1, cand, wts, 10, 50, np.random.default_rng(3), dedup)
+    assert np.array_equal(idx, g[f"{key}_idx"]) and np.array_equal(cnt, g[f"{key}_cnt"])
+    np.testing.assert_allclose(s, g[f"{key}_s"], rtol=1e-12)
+    np.testing.assert_allclose(u, g[f"{key}_u"], atol=1e-10)
+    for tag, eps in (("ct", 0.7), ("ctf", 30.0)):
+        key = f"{tag}{int(dedup)}"
+        u, s = orc.ctsvd(a1, cand, wts, 10, 60, 300, eps, np.random.default_rng(4), dedup)
+        assert s.size == g[f"{key}_s"].size
+        np.testing.assert_allclose(s, g[f"{key}_s"], rtol=1e-12)
+        np.testing.assert_allclose(u, g[f"{key}_u"], atol=1e-9)
+    assert g["ctf1_s"].size < 10  # the energy filter case really filters
+
+
+def test_exact_factorizations_match_reference():
+    g = load_golden("baselines")
+    for name in ("tall", "wide", "skinny"):
+        u, s, v = orc.dense_svd(g[f"svd_{name}_a"])
+        np.testing.assert_allclose(s, g[f"svd_{name}_s"], rtol=1e-12, atol=1e-15)
+        np.testing.assert_allclose(u, g[f"svd_{name}_u"], atol=1e-9)
+        np.testing.assert_allclose(v, g[f"svd_{name}_v"], atol=1e-9)
+    u, s, v = orc.pod_via_gram(workloads.config1(seed=0), 10)
+    np.testing.assert_allclose(s, g["gram_s"], rtol=1e-12)
+    np.testing.assert_allclose(u, g["gram_u"], atol=1e-9)
+    np.testing.assert_allclose(v, g["gram_v"], atol=1e-9)
