@@ -123,6 +123,13 @@ def fix_signs(u, v=None):
     return du.to_numpy(), (None if dv is None else dv.to_numpy())
 
 
+def mean_center_rows(a):
+    """Subtract each row's mean (matcore.py:168-175); a host preprocessing
+    step of the CLI's ``convert --center``, outside the GPU path."""
+    a = as_dense(a)
+    return as_dense(a - a.mean(axis=1, keepdims=True))
+
+
 # ---------------------------------------------------------------------------
 # Exact dense factorizations on the device (matcore.py:187-254).  The data
 # matrix may be numpy or a torch tensor (host or CUDA, fp64 or fp32 storage);
