@@ -319,6 +319,183 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
   }
 }
 
+// Register-resident CholeskyQR factor for l <= 64 (the merge rank of
+// BASELINE configs 1-2): same contract as cholqr_kernel.  256 threads: thread
+// (i = t % 64, q = t / 64) holds row i of the scaled Gram H at columns
+// q, q + 4, ..., so a right-looking Cholesky step is one broadcast row (from
+// the four threads owning row j, double-buffered in shared memory) and a
+// register update -- ONE barrier per step.  Every thread of row i tracks the
+// diagonal entry H[i][i] itself, so the next pivot needs no extra exchange.
+// Rh^-1 is formed the same way by right-looking back substitution.
+constexpr int CQS_L = 64, CQS_T = 256, CQS_G = CQS_T / CQS_L, CQS_U = CQS_L / CQS_G;
+
+// 1/sqrt(x) for normal positive x: fp32 seed (exactly rescaled by a power
+// of four) and three fp64 Newton steps -- no division or sqrt slow path
+__device__ __forceinline__ double rsqrt_pos(double x) {
+  int e;
+  double m = frexp(x, &e);  // x = m 2^e, m in [0.5, 1)
+  if (e & 1) {
+    m *= 2.0;
+    e -= 1;
+  }
+  double y = (double)rsqrtf((float)m);
+  y = y * fma(-0.5 * m, y * y, 1.5);
+  y = y * fma(-0.5 * m, y * y, 1.5);
+  y = y * fma(-0.5 * m, y * y, 1.5);
+  return ldexp(y, -e / 2);
+}
+
+__global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
+    const double* __restrict__ G, int64_t ldg, int l, double nrows, double* __restrict__ Rinv,
+    int64_t ldri, double* __restrict__ R, int64_t ldr, double* __restrict__ dinfo,
+    const int32_t* __restrict__ gate_in, int32_t* __restrict__ gate_out, int first_pass) {
+  if (gate_in && *gate_in == 0) {
+    if (gate_out && threadIdx.x == 0) *gate_out = 0;
+    return;
+  }
+  __shared__ double d[CQS_L];               // column scales sqrt(G_ii)
+  __shared__ double Rs[CQS_L * CQS_L];      // Rh, row-major Rs[j * 64 + k]
+  __shared__ double rowbuf[2][CQS_L];
+  __shared__ double dinv[CQS_L];           // 1 / Rh[j][j]
+  __shared__ double red[CQS_T / 32];
+  __shared__ int s_fail;
+  const int t = threadIdx.x, i = t % CQS_L, q = t / CQS_L;
+  const bool live_i = i < l;
+  if (t < CQS_L) {
+    const double gii = live_i ? G[i + (int64_t)i * ldg] : 0.0;
+    d[t] = (gii > 0.0) ? sqrt(gii) : 0.0;
+  }
+  __syncthreads();
+  // H = D^-1 G D^-1 (dead columns -> identity); recomputed for a shifted retry
+  auto scaled = [&](int j) {
+    if (!(live_i && j < l)) return 0.0;
+    if (d[i] == 0.0 || d[j] == 0.0) return (i == j) ? 1.0 : 0.0;
+    return (G[i + (int64_t)j * ldg] / d[i]) / d[j];
+  };
+  double loc_def = 0.0;
+#pragma unroll
+  for (int u = 0; u < CQS_U; ++u) {
+    const int j = q + CQS_G * u;
+    if (live_i && j < l && d[i] != 0.0 && d[j] != 0.0)
+      loc_def = fmax(loc_def, fabs(scaled(j) - (i == j ? 1.0 : 0.0)));
+  }
+  {
+    const double v = warp_max(loc_def);
+    if ((t & 31) == 0) red[t >> 5] = v;
+  }
+  __syncthreads();
+  double defect = 0.0;
+  for (int w = 0; w < CQS_T / 32; ++w) defect = fmax(defect, red[w]);
+  double shift = 0.0;
+  int attempt = 0;
+  double h[CQS_U];
+  for (;;) {
+    double dg = 0.0;  // this row's diagonal entry, tracked by all CQS_G threads of the row
+#pragma unroll
+    for (int u = 0; u < CQS_U; ++u) {
+      const int j = q + CQS_G * u;
+      h[u] = scaled(j) + ((i == j && live_i) ? shift : 0.0);
+    }
+    if (live_i) dg = scaled(i) + shift;
+    if (t == 0) s_fail = 0;
+    __syncthreads();
+    bool fail = false;
+    for (int j = 0; j < l; ++j) {
+      double* rb = rowbuf[j & 1];
+      // all threads read the pivot of row j from the row's owners' copy: the
+      // owners publish 1 / r_jj with the row
+      if (i == j) {
+        if (!(dg > 0.0)) {
+          if (q == 0) s_fail = 1;
+        } else {
+          const double inv = rsqrt_pos(dg);  // 1 / r_jj
+          const double rjj = dg * inv;
+          if (q == 0) dinv[j] = inv;
+#pragma unroll
+          for (int u = 0; u < CQS_U; ++u) {
+            const int c = q + CQS_G * u;
+            if (c < l && c >= j) {
+              const double v = (c == j) ? rjj : h[u] * inv;
+              rb[c] = v;
+              Rs[j * CQS_L + c] = v;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      if (s_fail) {
+        fail = true;
+        break;
+      }
+      if (live_i && i > j) {
+        const double mi = rb[i];
+        dg = fma(-mi, mi, dg);
+#pragma unroll
+        for (int u = 0; u < CQS_U; ++u) {
+          const int c = q + CQS_G * u;
+          if (c < l && c >= i) h[u] = fma(-mi, rb[c], h[u]);
+        }
+      }
+    }
+    if (!fail) break;
+    __syncthreads();
+    ++attempt;
+    // shifted CholeskyQR (Fukaya et al.): s = 11 (m l + l (l + 1)) u ||H||, ||H|| <= l
+    const double base = 11.0 * (nrows * l + (double)l * (l + 1)) * 1.1102230246251565e-16 * l;
+    shift = (attempt == 1) ? base : shift * 100.0;
+    if (attempt > 8) break;
+  }
+  __syncthreads();  // Rs complete; rowbuf free
+  // X = Rh^-1 by right-looking back substitution: thread (k, q) keeps row k
+  // of the accumulated right-hand side at its columns
+  double x[CQS_U];
+#pragma unroll
+  for (int u = 0; u < CQS_U; ++u) x[u] = (q + CQS_G * u == i) ? 1.0 : 0.0;
+  for (int r = l - 1; r >= 0; --r) {
+    double* rb = rowbuf[r & 1];
+    if (i == r) {
+      const double inv = dinv[r];
+#pragma unroll
+      for (int u = 0; u < CQS_U; ++u) {
+        const int c = q + CQS_G * u;
+        if (c < l && c >= r) {
+          x[u] *= inv;
+          rb[c] = x[u];
+        }
+      }
+    }
+    __syncthreads();
+    if (i < r) {
+      const double rk = Rs[i * CQS_L + r];
+#pragma unroll
+      for (int u = 0; u < CQS_U; ++u) {
+        const int c = q + CQS_G * u;
+        if (c < l && c >= r) x[u] = fma(-rk, rb[c], x[u]);
+      }
+    }
+  }
+  // R = Rh D, Rinv = D^-1 Rh^-1; dead columns -> zero rows / columns
+  if (live_i) {
+#pragma unroll
+    for (int u = 0; u < CQS_U; ++u) {
+      const int j = q + CQS_G * u;
+      if (j >= l) continue;
+      const bool dead = d[i] == 0.0 || d[j] == 0.0;
+      R[i + (int64_t)j * ldr] = (dead || j < i) ? 0.0 : Rs[i * CQS_L + j] * d[j];
+      Rinv[i + (int64_t)j * ldri] = (dead || j < i) ? 0.0 : x[u] / d[i];
+    }
+  }
+  if (t == 0) {
+    int ndead = 0;
+    for (int k = 0; k < l; ++k) ndead += d[k] == 0.0;
+    dinfo[0] = defect;
+    dinfo[1] = (double)attempt;
+    dinfo[2] = (double)ndead;
+    dinfo[3] = shift;
+    if (gate_out) *gate_out = first_pass ? 1 : ((defect > 1e-4 || attempt > 0) ? 1 : 0);
+  }
+}
+
 // ----------------------------------------------------- small GEMM / max --
 // C (p x q) = alpha * op(A) B + beta * C, op(A) = A (p x k) or A^T (A is k x p)
 __global__ void small_gemm_kernel(int p, int q, int k, double alpha, const double* __restrict__ A,
@@ -391,6 +568,16 @@ static int set_smem(const void* fn, size_t bytes) {
   if (i == nf && nf < 16) { fns[nf] = fn; ++nf; }
   if (i < 16) done[i] = SMALL_SMEM_CAP;
   return POD_OK;
+}
+
+// POD_CHOLQR_SMALL=0: the general CholeskyQR kernel for l <= 64 too (A/B)
+static bool cqs_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_CHOLQR_SMALL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 static size_t cholqr_bytes(int64_t l) { return (size_t)3 * l * l * 8 + (size_t)l * 8 + 64; }
@@ -517,6 +704,13 @@ extern "C" int pod_cholqr_factor(const double* G, int64_t ldg, int64_t l, int64_
                                  void* ws, size_t ws_bytes, const int32_t* gate_in,
                                  int32_t* gate_out, int first_pass, void* stream) {
   POD_REQUIRE(l >= 1 && ldg >= l && ldri >= l && ldr >= l, "pod_cholqr_factor: bad shape");
+  if (l <= CQS_L && cqs_enabled()) {
+    cholqr_small_kernel<<<1, CQS_T, 0, (cudaStream_t)stream>>>(G, ldg, (int)l, (double)nrows,
+                                                              Rinv, ldri, R, ldr, dinfo, gate_in,
+                                                              gate_out, first_pass);
+    POD_CHECK_LAUNCH("cholqr small");
+    return POD_OK;
+  }
   const size_t bytes = cholqr_bytes(l);
   const int use_smem = bytes <= SMALL_SMEM_CAP;
   POD_REQUIRE(use_smem || ws_bytes >= bytes, "pod_cholqr_factor: workspace too small");

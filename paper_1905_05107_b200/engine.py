@@ -70,6 +70,11 @@ G_FQR = 11          # finalize CholeskyQR passes: 11..15
 N_GATES = 16
 
 
+#: update slots of the ISMA engine: round t merges slot t % 3 while its side
+#: stream finishes update(t+1) (eigensolve + lift, slot (t+1) % 3) and starts
+#: update(t+2) (draw + Gram, slot (t+2) % 3)
+NSLOT = 3
+
 #: widest in-place Q <- Q R^-1 the NN kernel takes (pod_gemm_nn_f64)
 NN_INPLACE_MAX_Q = 192
 
@@ -92,7 +97,7 @@ class MergeWorkspace:
         f64 = dict(dtype=torch.float64, device=dev)
         r = self.r
         self.S = [ColMat.zeros(self.m, 2 * r, dev), ColMat.zeros(self.m, 2 * r, dev)]
-        # update slots (two for the cross-round pipeline of the ISMA engine)
+        # update slots (three for the cross-round pipeline of the ISMA engine)
         self.Uupd_b = [ColMat.zeros(self.m, r, dev) for _ in range(nupd)]
         self.sig_upd_b = [torch.zeros(max(r, upd_cap or 0), **f64) for _ in range(nupd)]
         self.Uupd, self.sig_upd = self.Uupd_b[0], self.sig_upd_b[0]
@@ -298,14 +303,16 @@ class MergeWorkspace:
 class IsmaEngine(MergeWorkspace):
     """The ISMA loop on one GPU (or one row shard).
 
-    Cross-round pipeline: the update of round t+1 (draw, Gram, eigensolve,
-    lift) only depends on the candidate set, not on the merge of round t, so
-    each captured round graph runs merge(t) + cosines(t) on the main stream
-    and update(t+1) on a side stream into the other update buffer.  The
-    uniforms of round t+1 are staged speculatively before round t's loop test;
-    if the loop stops, the generator is rolled back to its state before that
-    batch, so it is consumed exactly as by the reference (numpy Generators;
-    other generator objects run without the pipeline)."""
+    Cross-round pipeline: an update (draw, Gram, eigensolve, lift) only
+    depends on the candidate set, not on the merges, so each captured round
+    graph runs merge(t) + cosines(t) on the main stream and, on a side stream
+    forked at the start of the round, the eigensolve and lift of update(t+1)
+    and the draw and Gram of update(t+2) -- three update slots in rotation.
+    The uniforms of round t+2 are staged speculatively before round t runs;
+    when the loop stops, the generator is rolled back to its state before the
+    first batch of a round that never ran, so it is consumed exactly as by
+    the reference (numpy Generators; other generator objects run without the
+    pipeline)."""
 
     def __init__(self, ctx, A, *, k, r, c, criterion="modes", use_graphs=True, comm=None,
                  row_offset=0, m_total=None, w=0):
@@ -318,7 +325,7 @@ class IsmaEngine(MergeWorkspace):
             raise ParameterError(f"column budget c={self.c} can draw {gcap} distinct columns; "
                                  f"the sampled-Gram eigensolver takes at most {gmax}")
         super().__init__(ctx, A.m, r, k=k, criterion=criterion, upd_cap=gcap, comm=comm,
-                         row_offset=row_offset, nupd=2)
+                         row_offset=row_offset, nupd=NSLOT)
         self.m_total = A.m if m_total is None else int(m_total)
         dev = ctx.device
         f64 = dict(dtype=torch.float64, device=dev)
@@ -327,12 +334,12 @@ class IsmaEngine(MergeWorkspace):
         self.norms2 = torch.empty(n, **f64)
         self.nonfinite = torch.zeros(1, dtype=torch.int32, device=dev)
         self.live = torch.ones(n, dtype=torch.uint8, device=dev)
-        self.uni = [torch.empty(self.c, **f64) for _ in range(2)]
-        self.h_uni = [torch.empty(self.c, dtype=torch.float64).pin_memory() for _ in range(2)]
-        self.idx = [torch.empty(g, dtype=torch.int32, device=dev) for _ in range(2)]
-        self.cnt = [torch.empty(g, dtype=torch.int64, device=dev) for _ in range(2)]
-        self.G = [torch.empty(g * g, **f64) for _ in range(2)]
-        self.Tl = [torch.empty(g * r, **f64) for _ in range(2)]
+        self.uni = [torch.empty(self.c, **f64) for _ in range(NSLOT)]
+        self.h_uni = [torch.empty(self.c, dtype=torch.float64).pin_memory() for _ in range(NSLOT)]
+        self.idx = [torch.empty(g, dtype=torch.int32, device=dev) for _ in range(NSLOT)]
+        self.cnt = [torch.empty(g, dtype=torch.int64, device=dev) for _ in range(NSLOT)]
+        self.G = [torch.empty(g * g, **f64) for _ in range(NSLOT)]
+        self.Tl = [torch.empty(g * r, **f64) for _ in range(NSLOT)]
         self.npos = 0
         self.use_graphs = use_graphs
         self.graphs = {}
@@ -442,12 +449,18 @@ class IsmaEngine(MergeWorkspace):
             self._ev_free[b].record(main)
 
     def update_ops(self, mode, b, dest, cur=None, rowsrc=None):
-        """get_update (isma.py:144-178) at capacity into update buffer b (its
+        """get_update (isma.py:144-178) at capacity into update slot b (its
         own draw/Gram/eigensolver scratch).  rowsrc None: column path (Gram
         of the gathered columns D).  rowsrc "norms"/"lev": ICRS -- w rows
         drawn from D's squared row norms or from the leverage of the current
         top-k basis (stack `cur`), the dedup-scaled row block Y and Y^T Y."""
-        ctx, A, g, r = self.ctx, self.A, self.gcap, self.r
+        self.draw_gram_ops(mode, b, cur=cur, rowsrc=rowsrc)
+        self.eigh_lift_ops(b, dest)
+
+    def draw_gram_ops(self, mode, b, cur=None, rowsrc=None):
+        """First half of get_update: the draw (isma.py:158-164) and the
+        sampled Gram (baselines.py:43) or, for ICRS, the row draw and Y^T Y."""
+        ctx, A, g = self.ctx, self.A, self.gcap
         self.uni[b].copy_(self.h_uni[b], non_blocking=True)
         weights, thr = None, 0.0
         if mode == MODE_L2N:
@@ -468,27 +481,33 @@ class IsmaEngine(MergeWorkspace):
             ctx.tn(g, g, 1.0, src, src, dptr(self.G[b]), g, xcols=cols, ycols=cols,
                    tag="tn_gram_gather")                                     # baselines.py:43
             self.comm.allreduce_sum_(self.G[b])
-        else:
-            self.uniw[b].copy_(self.h_uniw[b], non_blocking=True)
-            if rowsrc == "lev":                                              # sampling.py:190-201
-                self.levdiv.copy_(self.h_levdiv, non_blocking=True)
-                ctx.rownorms2(self.S[cur], self.k, self.rowq, div_dev=self.levdiv)
-            else:                                                            # sampling.py:143-147
-                ctx.rownorms2(src, g, self.rowq, cols=cols)
-            hinfo = self.rec[1 + b, REC_H:]
-            ctx.draw(MODE_ROWS, self.rowq, None, self.m, self.uniw[b], self.w, self.ridx[b],
-                     self.rcnt[b], info=hinfo, p_out=self.rp[b])
-            ctx.gather_scale_rows(src, cols, g, self.ridx[b], self.rcnt[b], self.rp[b],
-                                  self.w, self.hcap, hinfo, self.Y[b])      # sampling.py:248-258
-            ctx.tn(g, g, 1.0, self.Y[b], self.Y[b], dptr(self.G[b]), g, tag="tn_gram_rows")
+            return
+        self.uniw[b].copy_(self.h_uniw[b], non_blocking=True)
+        if rowsrc == "lev":                                                  # sampling.py:190-201
+            self.levdiv.copy_(self.h_levdiv, non_blocking=True)
+            ctx.rownorms2(self.S[cur], self.k, self.rowq, div_dev=self.levdiv)
+        else:                                                                # sampling.py:143-147
+            ctx.rownorms2(src, g, self.rowq, cols=cols)
+        hinfo = self.rec[1 + b, REC_H:]
+        ctx.draw(MODE_ROWS, self.rowq, None, self.m, self.uniw[b], self.w, self.ridx[b],
+                 self.rcnt[b], info=hinfo, p_out=self.rp[b])
+        ctx.gather_scale_rows(src, cols, g, self.ridx[b], self.rcnt[b], self.rp[b],
+                              self.w, self.hcap, hinfo, self.Y[b])          # sampling.py:248-258
+        ctx.tn(g, g, 1.0, self.Y[b], self.Y[b], dptr(self.G[b]), g, tag="tn_gram_rows")
+
+    def eigh_lift_ops(self, b, dest):
+        """Second half of get_update: eigensolve of slot b's Gram
+        (baselines.py:44-48) and the lift through D (baselines.py:62-63)."""
+        ctx, A, g, r = self.ctx, self.A, self.gcap, self.r
+        src, cols = (self.D[b], None) if self.host_A else (A, self.idx[b])
         ctx.gram_eigh(dptr(self.G[b]), g, g, r, self.sig_upd_b[b], dptr(self.Tl[b]), g,
                       info=self.rec[1 + b, REC_RANK:])                       # baselines.py:44-48
         ctx.nn(g, r, 1.0, src, dptr(self.Tl[b]), g, dest, xcols=cols,
                tag="nn_lift_gather")                                         # baselines.py:62-63
 
-    def update_side_ops(self, mode, b, join=True):
-        """update_ops on the side stream with its own workspaces (forked from
-        the current stream; joined back when `join`)."""
+    def side_ops(self, fn, join=True):
+        """fn() on the side stream with its own workspaces (forked from the
+        current stream; joined back when `join`)."""
         main = torch.cuda.current_stream(self.ctx.device)
         self.side.wait_stream(main)
         self.ctx.ws_suffix = "_upd"
@@ -496,7 +515,7 @@ class IsmaEngine(MergeWorkspace):
         lib.pod_set_grid_cap(UPDATE_GRID_CAP)  # leave SMs to the concurrent merge
         try:
             with torch.cuda.stream(self.side):
-                self.update_ops(mode, b, self.Uupd_b[b].cols(0, self.r))
+                fn()
         finally:
             lib.pod_set_grid_cap(0)
             self.ctx.ws_suffix = ""
@@ -504,14 +523,22 @@ class IsmaEngine(MergeWorkspace):
             main.wait_stream(self.side)
 
     def round_ops(self, mode, cur, ub, pipelined, rowsrc=None):
-        """Round t: merge(t) with update buffer ub (+ cosines, readback);
-        pipelined: update(t+1) into buffer 1 - ub on the side stream, forked
-        after merge(t)'s GEMM phase so that its GEMMs and eigensolver overlap
-        merge(t)'s latency-bound E-SVD (8-16 SMs) instead of competing with
-        merge(t)'s full-GPU GEMMs."""
+        """Round t: merge(t) with update slot ub (+ cosines, readback).
+        pipelined: the side stream, forked at the start of the round, first
+        finishes update(t+1) -- eigensolve (a few SMs, beside the merge's
+        GEMM phase) and lift -- then draws and forms the Gram of update(t+2);
+        those GEMMs fall into the merge's latency-bound E-SVD.  The update
+        chain thus has a whole round to run in, and only the merge chain is
+        on the critical path."""
         if pipelined:
-            self.merge_ops(cur, ub, before_core=lambda: self.update_side_ops(mode, 1 - ub,
-                                                                             join=False))
+            u1, u2 = (ub + 1) % NSLOT, (ub + 2) % NSLOT
+
+            def side():
+                self.eigh_lift_ops(u1, self.Uupd_b[u1].cols(0, self.r))
+                self.draw_gram_ops(mode, u2)
+
+            self.side_ops(side, join=False)
+            self.merge_ops(cur, ub)
             self.cosines_ops(cur, 1 - cur)
             torch.cuda.current_stream(self.ctx.device).wait_stream(self.side)
             self.readback()
@@ -533,8 +560,9 @@ class IsmaEngine(MergeWorkspace):
         if gr is None:
             dev = self.ctx.device
             # eager warm-up (grows every workspace) on a side stream, state restored
-            keep = (self.live, self.rec, self.Uupd_b[0].t, self.Uupd_b[1].t, self.S[0].t,
-                    self.S[1].t, self.sig[0], self.sig[1], self.sig_upd_b[0], self.sig_upd_b[1])
+            keep = (self.live, self.rec, self.S[0].t, self.S[1].t, self.sig[0], self.sig[1],
+                    *(u.t for u in self.Uupd_b), *self.sig_upd_b, *self.G, *self.Tl, *self.idx,
+                    *self.cnt)
             saved = [t.clone() for t in keep]
             st = torch.cuda.Stream(dev)
             st.wait_stream(torch.cuda.current_stream(dev))
@@ -630,7 +658,7 @@ class IsmaEngine(MergeWorkspace):
         t0 = time.perf_counter()
         cur = self.cur
         r = self.r
-        # the pipeline stages uniforms one round ahead; only generators whose
+        # the pipeline stages uniforms two rounds ahead; only generators whose
         # state can be rolled back support that
         bitgen = getattr(rng, "bit_generator", None)
         mode = {"l2n": MODE_L2N, "ort": MODE_ORT}.get(strategy, MODE_UNIFORM)
@@ -661,11 +689,16 @@ class IsmaEngine(MergeWorkspace):
         xi = np.zeros(self.k)
         it = 0
         ub = 1
-        saved_state = None
+        # generator state before each speculatively staged batch (round -> state)
+        spec = {}
+        ran = 0  # rounds launched
         if pipelined and rem and not (mode == MODE_L2N and self.npos <= 0):
-            saved_state = bitgen.state
-            self._stage_uniforms(rng, ub)                                    # round 1
-            self.update_side_ops(mode, ub)
+            spec[1] = bitgen.state
+            self._stage_uniforms(rng, 1)                                     # round 1
+            spec[2] = bitgen.state
+            self._stage_uniforms(rng, 2)                                     # round 2
+            self.side_ops(lambda: (self.update_ops(mode, 1, self.Uupd_b[1].cols(0, r)),
+                                   self.draw_gram_ops(mode, 2)))
         while rem and (it == 0 or bool(np.any(xi < tau))):
             it += 1
             t0 = time.perf_counter()
@@ -673,8 +706,9 @@ class IsmaEngine(MergeWorkspace):
                 break  # l2n over only zero-norm columns (isma.py:211-215, 280-281)
             rowsrc = None
             if pipelined:
-                saved_state = bitgen.state
-                self._stage_uniforms(rng, 1 - ub)                            # round it + 1
+                ub = it % NSLOT
+                spec[it + 2] = bitgen.state
+                self._stage_uniforms(rng, (it + 2) % NSLOT)                  # round it + 2
             else:
                 if rows:
                     state = bitgen.state if bitgen is not None else None
@@ -682,6 +716,7 @@ class IsmaEngine(MergeWorkspace):
                     self.h_levdiv[0] = float(min(self.k, self.l))
                 self._stage_uniforms(rng, ub, rows)
             self.launch_round(mode, cur, ub, pipelined, rowsrc)
+            ran = it
             rec, xi = self.read_record(ub)
             if rows:
                 self._check_rows(rec, rng, state)
@@ -695,10 +730,11 @@ class IsmaEngine(MergeWorkspace):
             self.stats.setdefault("merge_sweeps", []).append(rec[REC_MERGE_SWEEPS])
             traces.append(trace_cls(it, g, rec[REC_H] if rows else 0, rem, xi.copy(),
                                     time.perf_counter() - t0))
-            if pipelined:
-                ub = 1 - ub
-        if pipelined and saved_state is not None:
-            bitgen.state = saved_state  # undo the speculative batch of the round never run
+        if pipelined and spec:
+            # undo the speculative batches of the rounds never run
+            first = min((u for u in spec if u > ran), default=None)
+            if first is not None:
+                bitgen.state = spec[first]
         self.cur = cur
         v = None
         if finalize and self.l:
