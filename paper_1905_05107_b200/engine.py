@@ -671,11 +671,29 @@ class IsmaEngine(MergeWorkspace):
         pipelined = bitgen is not None and mode != MODE_ORT and not rows
         state = bitgen.state if (rows and bitgen is not None) else None
         self._stage_uniforms(rng, 0, rows)
-        self.update_ops(MODE_L2N, 0, self.S[cur].cols(0, r),                 # bootstrap
-                        rowsrc="norms" if rows else None)
+        # generator state before each speculatively staged batch (round -> state)
+        spec = {}
+        ran = 0  # rounds launched
+        if pipelined:
+            # rounds 1 and 2 are staged speculatively so that update(1) and the
+            # draw + Gram of update(2) run on the side stream beside the
+            # bootstrap's eigensolve (they only need draw(0)'s candidate set)
+            spec[1] = bitgen.state
+            self._stage_uniforms(rng, 1)                                     # round 1
+            spec[2] = bitgen.state
+            self._stage_uniforms(rng, 2)                                     # round 2
+            self.draw_gram_ops(MODE_L2N, 0)                                  # bootstrap draw + Gram
+            self.side_ops(lambda: (self.update_ops(mode, 1, self.Uupd_b[1].cols(0, r)),
+                                   self.draw_gram_ops(mode, 2)), join=False)
+            self.eigh_lift_ops(0, self.S[cur].cols(0, r))                    # bootstrap eigh + lift
+        else:
+            self.update_ops(MODE_L2N, 0, self.S[cur].cols(0, r),             # bootstrap
+                            rowsrc="norms" if rows else None)
         self.sig[cur].copy_(self.sig_upd_b[0][:r])
         self.readback()
         rec, _ = self.read_record(0)
+        if pipelined:
+            torch.cuda.current_stream(self.ctx.device).wait_stream(self.side)
         if rows:
             self._check_rows(rec, rng, state)
         g, rem, keep0, h = rec[REC_G], rec[REC_REM], rec[REC_KEEP_UPD], rec[REC_H]
@@ -689,16 +707,6 @@ class IsmaEngine(MergeWorkspace):
         xi = np.zeros(self.k)
         it = 0
         ub = 1
-        # generator state before each speculatively staged batch (round -> state)
-        spec = {}
-        ran = 0  # rounds launched
-        if pipelined and rem and not (mode == MODE_L2N and self.npos <= 0):
-            spec[1] = bitgen.state
-            self._stage_uniforms(rng, 1)                                     # round 1
-            spec[2] = bitgen.state
-            self._stage_uniforms(rng, 2)                                     # round 2
-            self.side_ops(lambda: (self.update_ops(mode, 1, self.Uupd_b[1].cols(0, r)),
-                                   self.draw_gram_ops(mode, 2)))
         while rem and (it == 0 or bool(np.any(xi < tau))):
             it += 1
             t0 = time.perf_counter()
