@@ -202,6 +202,14 @@ int pod_cholqr_factor(const double* G, int64_t ldg, int64_t l, int64_t nrows, do
                       size_t ws_bytes, const int32_t* gate_in, int32_t* gate_out, int first_pass,
                       void* stream);
 
+/* pod_cholqr_factor with an optional accumulated factor: when Racc is not
+ * null, Racc <- R Racc in place (the CholeskyQR passes' running R,
+ * merge.py:70 / matcore.py:209); R itself may then be null for l <= 64. */
+int pod_cholqr_factor2(const double* G, int64_t ldg, int64_t l, int64_t nrows, double* Rinv,
+                       int64_t ldri, double* R, int64_t ldr, double* Racc, int64_t ldacc,
+                       double* dinfo, void* ws, size_t ws_bytes, const int32_t* gate_in,
+                       int32_t* gate_out, int first_pass, void* stream);
+
 /* Merge core (merge.py:80-88): E = [[diag sig1, M diag sig2],[0, R diag sig2]],
  * its SVD, keep = min(r, #sigma_E > 1e-14 max(sigma_E0, 1e-300)), and the
  * rotation T ((rcap + l2) x tcols, ld ldt) mapping the stacked basis

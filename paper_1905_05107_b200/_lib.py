@@ -64,6 +64,8 @@ SIGNATURES = {
     "pod_gram_eigh": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "pod_cholqr_factor": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp, _sz, _vp,
                                  _vp, _i32, _vp]),
+    "pod_cholqr_factor2": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp,
+                                  _vp, _sz, _vp, _vp, _i32, _vp]),
     "pod_merge_core": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64,
                               _i64, _vp, _vp, _vp, _sz, _vp]),
     "pod_svd_small": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),

@@ -347,8 +347,9 @@ __device__ __forceinline__ double rsqrt_pos(double x) {
 
 __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
     const double* __restrict__ G, int64_t ldg, int l, double nrows, double* __restrict__ Rinv,
-    int64_t ldri, double* __restrict__ R, int64_t ldr, double* __restrict__ dinfo,
-    const int32_t* __restrict__ gate_in, int32_t* __restrict__ gate_out, int first_pass) {
+    int64_t ldri, double* __restrict__ R, int64_t ldr, double* Racc, int64_t ldacc,
+    double* __restrict__ dinfo, const int32_t* __restrict__ gate_in,
+    int32_t* __restrict__ gate_out, int first_pass) {
   if (gate_in && *gate_in == 0) {
     if (gate_out && threadIdx.x == 0) *gate_out = 0;
     return;
@@ -475,14 +476,40 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
     }
   }
   // R = Rh D, Rinv = D^-1 Rh^-1; dead columns -> zero rows / columns
+  auto rk = [&](int a, int b) {  // R[a][b]
+    return (d[a] == 0.0 || d[b] == 0.0 || b < a) ? 0.0 : Rs[a * CQS_L + b] * d[b];
+  };
   if (live_i) {
 #pragma unroll
     for (int u = 0; u < CQS_U; ++u) {
       const int j = q + CQS_G * u;
       if (j >= l) continue;
       const bool dead = d[i] == 0.0 || d[j] == 0.0;
-      R[i + (int64_t)j * ldr] = (dead || j < i) ? 0.0 : Rs[i * CQS_L + j] * d[j];
+      if (R) R[i + (int64_t)j * ldr] = rk(i, j);
       Rinv[i + (int64_t)j * ldri] = (dead || j < i) ? 0.0 : x[u] / d[i];
+    }
+  }
+  if (Racc) {  // Racc <- R Racc (both upper triangular), in place
+    double acc[CQS_U];
+#pragma unroll
+    for (int u = 0; u < CQS_U; ++u) acc[u] = 0.0;
+    if (live_i) {
+      for (int k = i; k < l; ++k) {
+        const double a = rk(i, k);
+#pragma unroll
+        for (int u = 0; u < CQS_U; ++u) {
+          const int j = q + CQS_G * u;
+          if (j < l && k <= j) acc[u] = fma(a, Racc[k + (int64_t)j * ldacc], acc[u]);
+        }
+      }
+    }
+    __syncthreads();  // every read of the old Racc precedes the writes
+    if (live_i) {
+#pragma unroll
+      for (int u = 0; u < CQS_U; ++u) {
+        const int j = q + CQS_G * u;
+        if (j < l) Racc[i + (int64_t)j * ldacc] = acc[u];
+      }
     }
   }
   if (t == 0) {
@@ -636,7 +663,7 @@ static size_t gram_total_ws(int64_t g) {
 }
 
 extern "C" size_t pod_small_ws_bytes(int64_t n) {
-  return std::max(std::max(gram_total_ws(n), cholqr_bytes(n)),
+  return std::max(std::max(gram_total_ws(n), cholqr_bytes(n) + (size_t)n * n * 8),
                   std::max(gj_ws_bytes(n, n, n), gj_ws_bytes(n, n, 0)));
 }
 
@@ -703,14 +730,26 @@ extern "C" int pod_cholqr_factor(const double* G, int64_t ldg, int64_t l, int64_
                                  double* Rinv, int64_t ldri, double* R, int64_t ldr, double* dinfo,
                                  void* ws, size_t ws_bytes, const int32_t* gate_in,
                                  int32_t* gate_out, int first_pass, void* stream) {
-  POD_REQUIRE(l >= 1 && ldg >= l && ldri >= l && ldr >= l, "pod_cholqr_factor: bad shape");
+  return pod_cholqr_factor2(G, ldg, l, nrows, Rinv, ldri, R, ldr, nullptr, 1, dinfo, ws, ws_bytes,
+                            gate_in, gate_out, first_pass, stream);
+}
+
+extern "C" int pod_cholqr_factor2(const double* G, int64_t ldg, int64_t l, int64_t nrows,
+                                  double* Rinv, int64_t ldri, double* R, int64_t ldr,
+                                  double* Racc, int64_t ldacc, double* dinfo, void* ws,
+                                  size_t ws_bytes, const int32_t* gate_in, int32_t* gate_out,
+                                  int first_pass, void* stream) {
+  POD_REQUIRE(l >= 1 && ldg >= l && ldri >= l && ldr >= l && (!Racc || ldacc >= l),
+              "pod_cholqr_factor: bad shape");
+  POD_REQUIRE(R || Racc, "pod_cholqr_factor: no R output");
+  cudaStream_t st = (cudaStream_t)stream;
   if (l <= CQS_L && cqs_enabled()) {
-    cholqr_small_kernel<<<1, CQS_T, 0, (cudaStream_t)stream>>>(G, ldg, (int)l, (double)nrows,
-                                                              Rinv, ldri, R, ldr, dinfo, gate_in,
-                                                              gate_out, first_pass);
+    cholqr_small_kernel<<<1, CQS_T, 0, st>>>(G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr,
+                                             Racc, ldacc, dinfo, gate_in, gate_out, first_pass);
     POD_CHECK_LAUNCH("cholqr small");
     return POD_OK;
   }
+  POD_REQUIRE(R, "pod_cholqr_factor: l = %lld > 64 needs the R output", (long long)l);
   const size_t bytes = cholqr_bytes(l);
   const int use_smem = bytes <= SMALL_SMEM_CAP;
   POD_REQUIRE(use_smem || ws_bytes >= bytes, "pod_cholqr_factor: workspace too small");
@@ -724,8 +763,18 @@ extern "C" int pod_cholqr_factor(const double* G, int64_t ldg, int64_t l, int64_
       G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr, dinfo, (double*)ws, use_smem, gate_in,
       gate_out, first_pass);
   POD_CHECK_LAUNCH("cholqr");
+  if (Racc) {  // Racc <- R Racc through the workspace's tail (general path)
+    POD_REQUIRE(ws_bytes >= cholqr_bytes(l) + (size_t)l * l * 8, "pod_cholqr_factor: workspace");
+    double* tmp = (double*)((char*)ws + cholqr_bytes(l));
+    int blocks = (int)std::min<int64_t>(ceil_div(l * l, 256), 1024);
+    small_gemm_kernel<<<blocks, 256, 0, st>>>((int)l, (int)l, (int)l, 1.0, R, ldr, 0, Racc, ldacc,
+                                              0.0, tmp, l, gate_in);
+    small_copy_kernel<<<blocks, 256, 0, st>>>((int)l, (int)l, tmp, l, Racc, ldacc, gate_in);
+    POD_CHECK_LAUNCH("cholqr accumulate");
+  }
   return POD_OK;
 }
+
 
 extern "C" int pod_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm,
                               const double* R, int64_t ldr, const double* sig2, int64_t l2,

@@ -226,6 +226,15 @@ class Ctx:
         self._call("cholqr_factor", 1, 0.0, 8.0 * l * l, "pod_cholqr_factor", G, ldg, l, nrows, Rinv, ldri, R, ldr, _ptr(self.dinfo),
                   _ptr(ws), ws.numel(), _gp(gate_in), _gp(gate_out), int(first_pass), self.stream)
 
+    def cholqr_factor_acc(self, G, ldg, l, nrows, Rinv, ldri, R, ldr, Racc, ldacc, gate_in=None,
+                          gate_out=None, first_pass=0):
+        """pod_cholqr_factor2: as cholqr_factor, and Racc <- R Racc when Racc
+        is given (R may then be None for l <= 64)."""
+        ws = self.small_ws(l)
+        self._call("cholqr_factor", 1, 0.0, 8.0 * l * l, "pod_cholqr_factor2", G, ldg, l, nrows,
+                   Rinv, ldri, R, ldr, Racc, ldacc, _ptr(self.dinfo), _ptr(ws), ws.numel(),
+                   _gp(gate_in), _gp(gate_out), int(first_pass), self.stream)
+
     def merge_core(self, sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new,
                    info=None):
         ws = self.small_ws(l1 + l2)

@@ -160,37 +160,34 @@ class MergeWorkspace:
         g0 = first_gate
         tmp = self._scratch_like(Q)
         src = Wsrc
+        # the running R: pass 0 writes it, later passes fold R_p R into it
+        # inside the factor kernel (pod_cholqr_factor2)
+        rk = None if l <= 64 else dptr(self.Rk)
         for p in range(2):  # CholeskyQR2: Wsrc -> tmp -> Q
             dst = tmp if p == 0 else Q
             ctx.tn(l, l, 1.0, src, src, dptr(self.Gq), r, gate=g0, tag="tn_cholqr_gram")
             if sharded:
                 self.comm.allreduce_sum_(self.Gq)
-            ctx.cholqr_factor(dptr(self.Gq), r, l, src.m, dptr(self.Rinv), r, dptr(self.Rk), r,
-                              gate_in=g0, gate_out=self.gate(gate_base + p + 1),
-                              first_pass=1 if p == 0 else 0)
+            ctx.cholqr_factor_acc(dptr(self.Gq), r, l, src.m, dptr(self.Rinv), r,
+                                  dptr(Rout) if p == 0 else rk, r,
+                                  None if p == 0 else dptr(Rout), r,
+                                  gate_in=g0, gate_out=self.gate(gate_base + p + 1),
+                                  first_pass=1 if p == 0 else 0)
             ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, dst, gate=g0, tag="nn_cholqr_apply")
-            if p == 0:
-                ctx.small_copy(l, l, dptr(self.Rk), r, dptr(Rout), r, gate=g0)
-            else:
-                ctx.small_gemm(l, l, l, 1.0, dptr(self.Rk), r, 0, dptr(Rout), r, 0.0,
-                               dptr(self.Rtmp), r, gate=g0)
-                ctx.small_copy(l, l, dptr(self.Rtmp), r, dptr(Rout), r, gate=g0)
             src = dst
         for p in range(2, CHOLQR_PASSES):
             gp = self.gate(gate_base + p)
             ctx.tn(l, l, 1.0, Q, Q, dptr(self.Gq), r, gate=gp, tag="tn_cholqr_gram")
             if sharded:
                 self.comm.allreduce_sum_(self.Gq)
-            ctx.cholqr_factor(dptr(self.Gq), r, l, Q.m, dptr(self.Rinv), r, dptr(self.Rk), r,
-                              gate_in=gp, gate_out=self.gate(gate_base + p + 1), first_pass=0)
+            ctx.cholqr_factor_acc(dptr(self.Gq), r, l, Q.m, dptr(self.Rinv), r, rk, r,
+                                  dptr(Rout), r, gate_in=gp,
+                                  gate_out=self.gate(gate_base + p + 1), first_pass=0)
             if l <= NN_INPLACE_MAX_Q:
                 ctx.nn(l, l, 1.0, Q, dptr(self.Rinv), r, Q, gate=gp, tag="nn_cholqr_apply")
             else:  # wider than the in-place NN kernel: through the scratch block
                 ctx.nn(l, l, 1.0, Q, dptr(self.Rinv), r, tmp, gate=gp, tag="nn_cholqr_apply")
                 ctx.small_copy(Q.m, l, tmp.ptr, tmp.ld, Q.ptr, Q.ld, gate=gp)
-            ctx.small_gemm(l, l, l, 1.0, dptr(self.Rk), r, 0, dptr(Rout), r, 0.0,
-                           dptr(self.Rtmp), r, gate=gp)
-            ctx.small_copy(l, l, dptr(self.Rtmp), r, dptr(Rout), r, gate=gp)
 
     def _scratch_like(self, Q):
         """m x r scratch block for the first CholeskyQR pass (one per row count)."""
