@@ -495,12 +495,19 @@ class IsmaEngine(MergeWorkspace):
     def eigh_lift_ops(self, b, dest):
         """Second half of get_update: eigensolve of slot b's Gram
         (baselines.py:44-48) and the lift through D (baselines.py:62-63)."""
-        ctx, A, g, r = self.ctx, self.A, self.gcap, self.r
-        src, cols = (self.D[b], None) if self.host_A else (A, self.idx[b])
-        ctx.gram_eigh(dptr(self.G[b]), g, g, r, self.sig_upd_b[b], dptr(self.Tl[b]), g,
-                      info=self.rec[1 + b, REC_RANK:])                       # baselines.py:44-48
-        ctx.nn(g, r, 1.0, src, dptr(self.Tl[b]), g, dest, xcols=cols,
-               tag="nn_lift_gather")                                         # baselines.py:62-63
+        self.eigh_ops(b)
+        self.lift_ops(b, dest)
+
+    def eigh_ops(self, b):
+        g, r = self.gcap, self.r
+        self.ctx.gram_eigh(dptr(self.G[b]), g, g, r, self.sig_upd_b[b], dptr(self.Tl[b]), g,
+                           info=self.rec[1 + b, REC_RANK:])                  # baselines.py:44-48
+
+    def lift_ops(self, b, dest):
+        g, r = self.gcap, self.r
+        src, cols = (self.D[b], None) if self.host_A else (self.A, self.idx[b])
+        self.ctx.nn(g, r, 1.0, src, dptr(self.Tl[b]), g, dest, xcols=cols,
+                    tag="nn_lift_gather")                                    # baselines.py:62-63
 
     def side_ops(self, fn, join=True):
         """fn() on the side stream with its own workspaces (forked from the
@@ -521,21 +528,19 @@ class IsmaEngine(MergeWorkspace):
 
     def round_ops(self, mode, cur, ub, pipelined, rowsrc=None):
         """Round t: merge(t) with update slot ub (+ cosines, readback).
-        pipelined: the side stream, forked at the start of the round, first
-        finishes update(t+1) -- eigensolve (a few SMs, beside the merge's
-        GEMM phase) and lift -- then draws and forms the Gram of update(t+2);
-        those GEMMs fall into the merge's latency-bound E-SVD.  The update
+        pipelined: the side stream, forked at the start of the round, runs
+        the eigensolve of update(t+1) (a few SMs, beside the merge's GEMM
+        phase); once that GEMM phase is done it lifts update(t+1) and draws
+        and forms the Gram of update(t+2) -- GEMMs that then share the GPU
+        with the merge's latency-bound E-SVD instead of its GEMMs.  The update
         chain thus has a whole round to run in, and only the merge chain is
         on the critical path."""
         if pipelined:
             u1, u2 = (ub + 1) % NSLOT, (ub + 2) % NSLOT
-
-            def side():
-                self.eigh_lift_ops(u1, self.Uupd_b[u1].cols(0, self.r))
-                self.draw_gram_ops(mode, u2)
-
-            self.side_ops(side, join=False)
-            self.merge_ops(cur, ub)
+            self.side_ops(lambda: self.eigh_ops(u1), join=False)
+            self.merge_ops(cur, ub, before_core=lambda: self.side_ops(
+                lambda: (self.lift_ops(u1, self.Uupd_b[u1].cols(0, self.r)),
+                         self.draw_gram_ops(mode, u2)), join=False))
             self.cosines_ops(cur, 1 - cur)
             torch.cuda.current_stream(self.ctx.device).wait_stream(self.side)
             self.readback()
