@@ -118,7 +118,7 @@ PROFILE_TAGS = ["colnorms2", "colnorms2", "tn_gram_gather", "tn_gram_gather", "t
                 "tn_merge_proj", "tn_cholqr_gram", "tn_cholqr_gram", "nn_lift_gather",
                 "nn_lift_gather", "nn_merge_resid", "nn_merge_resid", "nn_merge_rotate",
                 "nn_merge_rotate", "gram_eigh", "gram_eigh", "gram_eigh", "gram_eigh",
-                "merge_core", "merge_core"]
+                "merge_core", "merge_core", "cholqr_factor", "cholqr_factor"]
 
 
 def _profiled_traffic():

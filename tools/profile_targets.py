@@ -29,6 +29,10 @@ M = torch.randn(r * r, dtype=torch.float64, device=dev) * 0.1
 R = torch.triu(torch.randn((r, r), dtype=torch.float64, device=dev)).T.contiguous().reshape(-1)
 Tm = torch.empty(2 * r * r, dtype=torch.float64, device=dev)
 sn = torch.empty(r, dtype=torch.float64, device=dev)
+Wt = W.t[:r, :m]
+Gq = (Wt @ Wt.T).T.contiguous().reshape(-1)
+Rinv = torch.empty(r * r, dtype=torch.float64, device=dev)
+Rk = torch.empty(r * r, dtype=torch.float64, device=dev)
 ops = [
     ("colnorms", lambda: ctx.colnorms2(A, norms, flag)),
     ("tn_gram_gather", lambda: ctx.tn(g, g, 1.0, A, A, dptr(C), g, xcols=idx, ycols=idx)),
@@ -40,6 +44,7 @@ ops = [
     ("gram_eigh", lambda: ctx.gram_eigh(dptr(G), g, g, r, sig, dptr(Tl), g)),
     ("merge_core", lambda: ctx.merge_core(dptr(sig1), r, dptr(M), r, dptr(R), r, dptr(sig1), r, r, r,
                                           dptr(Tm), 2 * r, r, dptr(sn))),
+    ("cholqr_factor", lambda: ctx.cholqr_factor(dptr(Gq), r, r, m, dptr(Rinv), r, dptr(Rk), r)),
 ]
 for name, fn in ops:
     fn(); fn()
