@@ -152,9 +152,10 @@ struct Geo {
     bse = (bs + 1) & ~1;
     slot = bs * ld + bs * ldj + 2 * bse;
   }
-  __host__ __device__ size_t smem_bytes(int cl) const {
-    // 2 mbarriers + flags [2][CL] (as doubles) + gathered norms [2 cl bs] + 4 slots
-    return (size_t)(2 + 2 * cl + 2 * cl * bs + 4 * (size_t)slot) * sizeof(double);
+  // up to 4 mbarriers + flags [2][CL] (as doubles) + gathered norms [2 cl bs]
+  // + nset block sets of 2 slots
+  __host__ __device__ size_t smem_bytes(int cl, int nset = 2) const {
+    return (size_t)(4 + 2 * cl + 2 * cl * bs + 2 * (size_t)nset * slot) * sizeof(double);
   }
 };
 

@@ -30,16 +30,21 @@ namespace bj {
 // Runs the sweeps.  On return the CURRENT set holds the converged blocks
 // (exact squared norms in nrm) and every CTA's gnorm[id] holds all n squared
 // norms.  Returns the sweep count.
+// nset = 3 block sets: the blocks of step st+1 land in a third set, so a CTA
+// may run ahead of a neighbour without overwriting data the neighbour still
+// reads -- the cluster barrier is then needed once per sweep (the
+// convergence vote) instead of once per tournament step.  nset = 2 keeps the
+// per-step barrier (sizes whose three sets do not fit shared memory).
 template <int CL, int TPP, int RPL>
 __device__ int run_sweeps(cg::cluster_group& cl, const Geo& g, double* slots, uint64_t* mbar,
                           double* flags, double* gnorm, int& cur_set, double tol,
-                          int max_sweeps) {
+                          int max_sweeps, int nset) {
   const int me = (int)cl.block_rank();
   const int bs = g.bs;
   const double tol2 = tol * tol;
   const int NB = 2 * CL;
   int set = cur_set;
-  uint32_t use[2] = {0u, 0u};
+  uint32_t use[3] = {0u, 0u, 0u};
   // destinations of this CTA's slot 0 (top) and slot 1 (bottom) after a step
   int d0c, d0s, d1c, d1s;
   if (me == 0) { d0c = 0; d0s = 0; d1c = (CL > 1) ? 1 : 0; d1s = 0; }
@@ -111,7 +116,9 @@ __device__ int run_sweeps(cg::cluster_group& cl, const Geo& g, double* slots, ui
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncthreads();
       BJ_T(4);
-      cluster_barrier();  // every CTA done with this step (and its incoming copies consumed)
+      // two sets: every CTA done with this step (its incoming copies consumed)
+      // before new blocks may overwrite them; three sets: only for the vote
+      if (last || nset == 2) cluster_barrier();
       BJ_T(5);
       if (last) {
         double tot = 0.0;
@@ -120,8 +127,8 @@ __device__ int run_sweeps(cg::cluster_group& cl, const Geo& g, double* slots, ui
         rot = false;
       }
       if (last && (converged || sweep + 1 >= max_sweeps)) break;
-      // move both blocks to their next owners (set -> 1 - set)
-      const int nxt = 1 - set;
+      // move both blocks to their next owners (set -> next set)
+      const int nxt = (set + 1 == nset) ? 0 : set + 1;
       if (threadIdx.x == 0) {
         mbar_arrive_expect(&mbar[nxt], 2u * slot_bytes);
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -175,7 +182,7 @@ template <int CL>
 __device__ __forceinline__ Smem<CL> carve(double* base, const Geo& g) {
   Smem<CL> s;
   s.mbar = reinterpret_cast<uint64_t*>(base);
-  s.flags = base + 2;
+  s.flags = base + 4;
   s.gnorm = s.flags + 2 * CL;
   s.slots = s.gnorm + 2 * CL * g.bs;
   return s;
@@ -186,6 +193,7 @@ __device__ void setup(cg::cluster_group& cl, const Smem<CL>& sm) {
   if (threadIdx.x == 0) {
     mbar_init(&sm.mbar[0], 1);
     mbar_init(&sm.mbar[1], 1);
+    mbar_init(&sm.mbar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   for (int t = threadIdx.x; t < 2 * CL; t += blockDim.x) sm.flags[t] = 0.0;
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
                       int64_t ldm, const double* __restrict__ Rm, int64_t ldr,
                       const double* __restrict__ sig2, int l2, int r, int rcap,
                       double* __restrict__ T, int64_t ldt, int tcols, double* __restrict__ sig_new,
-                      int64_t* __restrict__ info, int max_sweeps, int trans) {
+                      int64_t* __restrict__ info, int max_sweeps, int trans, int nset) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double smem_bj[];
   const int n = l1 + l2;
@@ -256,7 +264,7 @@ __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
   setup<CL>(cl, sm);
   int set = 0;
   const int sweeps = run_sweeps<CL, TPP, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
-                                         2.220446049250313e-16 * (double)max(n, 16), max_sweeps);
+                                         2.220446049250313e-16 * (double)max(n, 16), max_sweeps, nset);
   // sigma, keep (identical in every CTA)
   double s0 = 0.0;
   for (int i = 0; i < n; ++i) s0 = fmax(s0, sm.gnorm[i]);
@@ -307,7 +315,7 @@ __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
     gram_eigh_kernel(const double* __restrict__ X, const int* __restrict__ piv,
                      const int64_t* __restrict__ rank_in, int gdim, int r,
                      double* __restrict__ sigma_out, double* __restrict__ T, int64_t ldt,
-                     int64_t* __restrict__ info, int max_sweeps) {
+                     int64_t* __restrict__ info, int max_sweeps, int nset) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double smem_bj[];
   const Geo g(gdim, gdim, 0, CL);
@@ -331,7 +339,7 @@ __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
   int set = 0;
   const int sweeps = run_sweeps<CL, TPP, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
                                          2.220446049250313e-16 * (double)max(gdim, 16),
-                                         max_sweeps);
+                                         max_sweeps, nset);
   // lambda = squared norms (ids >= rank are zero columns)
   double lam0 = 0.0;
   for (int i = 0; i < gdim; ++i) lam0 = fmax(lam0, sm.gnorm[i]);
@@ -380,7 +388,7 @@ template <int CL, int TPP, int RPL>
 __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
     svd_kernel(const double* __restrict__ A, int64_t lda, int nr, int nc, double* __restrict__ U,
                int64_t ldu, double* __restrict__ sigma, double* __restrict__ V, int64_t ldv,
-               int64_t* __restrict__ info, int max_sweeps) {
+               int64_t* __restrict__ info, int max_sweeps, int nset) {
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double smem_bj[];
   const Geo g(nc, nr, V ? nc : 0, CL);
@@ -408,7 +416,7 @@ __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
   setup<CL>(cl, sm);
   int set = 0;
   const int sweeps = run_sweeps<CL, TPP, RPL>(cl, g, sm.slots, sm.mbar, sm.flags, sm.gnorm, set,
-                                         2.220446049250313e-16 * (double)max(nr, 16), max_sweeps);
+                                         2.220446049250313e-16 * (double)max(nr, 16), max_sweeps, nset);
   if (me == 0 && threadIdx.x == 0) info[0] = sweeps;
   for (int t2 = 0; t2 < 2; ++t2) {
     const Slot s = slot_at(sm.slots, g, set, t2);
@@ -526,13 +534,14 @@ int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, 
     if (variant < 2 && !trans) continue;
     const int cl = (variant % 2 == 0) ? BJ_CL : 16;
     const bj::Geo g(n, n, trans ? n : 0, cl);
-    const size_t bytes = g.smem_bytes(cl);
+    const int nset = g.smem_bytes(cl, 3) <= bj::SMEM_CAP ? 3 : 2;
+    const size_t bytes = g.smem_bytes(cl, nset);
     if (bytes > bj::SMEM_CAP) continue;
     const int tpp = bj::lanes_for(g);
     const int th = bj::threads_for(g, tpp);
     const int rpl = (g.nrows + tpp - 1) / tpp;
     if (th > 512 || (rpl > 8 && th > 384)) continue;
-#define BJ_L(C_, T_, R_) return bj::launch(bj::merge_core_kernel<C_, T_, R_>, C_, th, bytes, stream, sig1, (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new, info, 60, trans)
+#define BJ_L(C_, T_, R_) return bj::launch(bj::merge_core_kernel<C_, T_, R_>, C_, th, bytes, stream, sig1, (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new, info, 60, trans, nset)
     if (cl == BJ_CL) {
       if (tpp == 8) { if (rpl <= 4) BJ_L(BJ_CL, 8, 4); if (rpl <= 8) BJ_L(BJ_CL, 8, 8); if (rpl <= 16) BJ_L(BJ_CL, 8, 16); if (rpl <= 24) BJ_L(BJ_CL, 8, 24); BJ_L(BJ_CL, 8, 0); }
       if (tpp == 16) { if (rpl <= 4) BJ_L(BJ_CL, 16, 4); if (rpl <= 8) BJ_L(BJ_CL, 16, 8); if (rpl <= 16) BJ_L(BJ_CL, 16, 16); if (rpl <= 24) BJ_L(BJ_CL, 16, 24); BJ_L(BJ_CL, 16, 0); }
@@ -552,13 +561,14 @@ int bj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t g
                  double* sigma, double* T, int64_t ldt, int64_t* info, cudaStream_t stream) {
   if (!bj_enabled()) return BJ_NOT_APPLICABLE;
   const bj::Geo g((int)gd, (int)gd, 0, BJ_CL);
-  const size_t bytes = g.smem_bytes(BJ_CL);
+  const int nset = g.smem_bytes(BJ_CL, 3) <= bj::SMEM_CAP ? 3 : 2;
+  const size_t bytes = g.smem_bytes(BJ_CL, nset);
   if (bytes > bj::SMEM_CAP || gd < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
   const int tpp = bj::lanes_for(g);
   const int th = bj::threads_for(g, tpp);
   const int rpl = (g.nrows + tpp - 1) / tpp;
   if (th > 512 || (rpl > 8 && th > 384)) return BJ_NOT_APPLICABLE;
-#define BJ_L(T_, R_) bj::launch(bj::gram_eigh_kernel<BJ_CL, T_, R_>, BJ_CL, th, bytes, stream, X, piv, rank, (int)gd, (int)r, sigma, T, ldt, info, 60)
+#define BJ_L(T_, R_) bj::launch(bj::gram_eigh_kernel<BJ_CL, T_, R_>, BJ_CL, th, bytes, stream, X, piv, rank, (int)gd, (int)r, sigma, T, ldt, info, 60, nset)
 #define BJ_R(T_)                         \
   if (rpl <= 4) return BJ_L(T_, 4);      \
   if (rpl <= 8) return BJ_L(T_, 8);      \
@@ -576,13 +586,14 @@ int bj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int6
            double* sigma, double* V, int64_t ldv, int64_t* info, cudaStream_t stream) {
   if (!bj_enabled()) return BJ_NOT_APPLICABLE;
   const bj::Geo g((int)nc, (int)nr, V ? (int)nc : 0, BJ_CL);
-  const size_t bytes = g.smem_bytes(BJ_CL);
+  const int nset = g.smem_bytes(BJ_CL, 3) <= bj::SMEM_CAP ? 3 : 2;
+  const size_t bytes = g.smem_bytes(BJ_CL, nset);
   if (bytes > bj::SMEM_CAP || nc < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
   const int tpp = bj::lanes_for(g);
   const int th = bj::threads_for(g, tpp);
   const int rpl = (g.nrows + tpp - 1) / tpp;
   if (th > 512 || (rpl > 8 && th > 384)) return BJ_NOT_APPLICABLE;
-#define BJ_L(T_, R_) bj::launch(bj::svd_kernel<BJ_CL, T_, R_>, BJ_CL, th, bytes, stream, A, lda, (int)nr, (int)nc, U, ldu, sigma, V, ldv, info, 60)
+#define BJ_L(T_, R_) bj::launch(bj::svd_kernel<BJ_CL, T_, R_>, BJ_CL, th, bytes, stream, A, lda, (int)nr, (int)nc, U, ldu, sigma, V, ldv, info, 60, nset)
 #define BJ_R(T_)                         \
   if (rpl <= 4) return BJ_L(T_, 4);      \
   if (rpl <= 8) return BJ_L(T_, 8);      \
