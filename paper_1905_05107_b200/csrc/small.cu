@@ -124,10 +124,11 @@ __global__ void __launch_bounds__(PIVCHOL_THREADS) pivchol_kernel(
     }
     const int p = s_p;
     const double rjj = sqrt(d);
+    const double rinv = 1.0 / rjj;
     // (A) r_j by original index
     for (int q = threadIdx.x; q < g; q += blockDim.x) {
       double v = 0.0;
-      if (!s_done[q]) v = (q == p) ? rjj : at(p, q) / rjj;
+      if (!s_done[q]) v = (q == p) ? rjj : at(p, q) * rinv;
       s_rv[q] = (q == p) ? 0.0 : v;  // p leaves the Schur complement
       Rq[j + (int64_t)q * g] = v;
     }
@@ -192,7 +193,9 @@ __global__ void __launch_bounds__(PIVCHOL_THREADS) pivchol_kernel(
 
 // --------------------------------------------------------- CholeskyQR ----
 // Upper-triangular inverse of Rh (l x l, ld l) into X (ld l): warp per column.
-__device__ __forceinline__ void upper_inverse(const double* Rh, int l, double* X) {
+// rdiag[i] = 1 / Rh[i][i] (precomputed: no division in the dependent chain)
+__device__ __forceinline__ void upper_inverse(const double* Rh, int l, double* X,
+                                              const double* rdiag) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int j = warp; j < l; j += nw) {
     double* xj = X + (int64_t)j * l;
@@ -204,7 +207,7 @@ __device__ __forceinline__ void upper_inverse(const double* Rh, int l, double* X
       double s = 0.0;
       for (int k = i + 1 + lane; k <= j; k += 32) s = fma(Rh[i + (int64_t)k * l], xj[k], s);
       s = warp_sum(s);
-      if (lane == 0) xj[i] = -s / Rh[i + (int64_t)i * l];
+      if (lane == 0) xj[i] = -s * rdiag[i];
       __syncwarp();
     }
   }
@@ -226,11 +229,14 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
   double* C = H + (size_t)l * l;       // Cholesky factor workspace
   double* X = C + (size_t)l * l;       // inverse
   double* d = X + (size_t)l * l;       // column scales
+  double* dr = d + l;                  // their reciprocals (0 for dead columns)
+  double* dr2 = dr + l;                // 1 / Rh[j][j]
   __shared__ int s_fail;
   __shared__ double s_defect;
   for (int i = threadIdx.x; i < l; i += blockDim.x) {
     const double gii = G[i + (int64_t)i * ldg];
     d[i] = (gii > 0.0) ? sqrt(gii) : 0.0;
+    dr[i] = d[i] > 0.0 ? 1.0 / d[i] : 0.0;
   }
   if (threadIdx.x == 0) s_defect = 0.0;
   __syncthreads();
@@ -241,7 +247,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
     if (d[i] == 0.0 || d[j] == 0.0) {
       h = (i == j) ? 1.0 : 0.0;
     } else {
-      h = (G[i + (int64_t)j * ldg] / d[i]) / d[j];
+      h = G[i + (int64_t)j * ldg] * dr[i] * dr[j];
       loc_def = fmax(loc_def, fabs(h - (i == j ? 1.0 : 0.0)));
     }
     H[t] = h;
@@ -276,8 +282,10 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
         break;
       }
       const double rjj = sqrt(piv);
+      const double rinv = 1.0 / rjj;
       __syncthreads();
-      for (int k = j + threadIdx.x; k < l; k += blockDim.x) C[j + (int64_t)k * l] = (k == j) ? rjj : C[j + (int64_t)k * l] / rjj;
+      if (threadIdx.x == 0) dr2[j] = rinv;
+      for (int k = j + threadIdx.x; k < l; k += blockDim.x) C[j + (int64_t)k * l] = (k == j) ? rjj : C[j + (int64_t)k * l] * rinv;
       __syncthreads();
       const int rem = l - j - 1;
       for (int64_t t = threadIdx.x; t < (int64_t)rem * rem; t += blockDim.x) {
@@ -300,14 +308,14 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
     if (i > j) C[t] = 0.0;
   }
   __syncthreads();
-  upper_inverse(C, l, X);
+  upper_inverse(C, l, X, dr2);
   // R = Rh D, Rinv = D^-1 Rh^-1; dead columns -> zero rows / columns
   int ndead = 0;
   for (int64_t t = threadIdx.x; t < (int64_t)l * l; t += blockDim.x) {
     const int j = (int)(t / l), i = (int)(t - (int64_t)j * l);
     const bool dead = d[i] == 0.0 || d[j] == 0.0;
     R[i + (int64_t)j * ldr] = dead ? 0.0 : C[t] * d[j];
-    Rinv[i + (int64_t)j * ldri] = dead ? 0.0 : X[t] / d[i];
+    Rinv[i + (int64_t)j * ldri] = dead ? 0.0 : X[t] * dr[i];
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < l; ++i) ndead += d[i] == 0.0;
@@ -362,23 +370,29 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
   __shared__ int s_fail;
   const int t = threadIdx.x, i = t % CQS_L, q = t / CQS_L;
   const bool live_i = i < l;
+  __shared__ double dr[CQS_L];  // 1 / d (0 for dead columns)
   if (t < CQS_L) {
     const double gii = live_i ? G[i + (int64_t)i * ldg] : 0.0;
-    d[t] = (gii > 0.0) ? sqrt(gii) : 0.0;
+    const double di = (gii > 0.0) ? sqrt(gii) : 0.0;
+    d[t] = di;
+    dr[t] = di > 0.0 ? 1.0 / di : 0.0;
+    rowbuf[0][t] = rowbuf[1][t] = 0.0;
   }
   __syncthreads();
   // H = D^-1 G D^-1 (dead columns -> identity); recomputed for a shifted retry
   auto scaled = [&](int j) {
     if (!(live_i && j < l)) return 0.0;
     if (d[i] == 0.0 || d[j] == 0.0) return (i == j) ? 1.0 : 0.0;
-    return (G[i + (int64_t)j * ldg] / d[i]) / d[j];
+    return G[i + (int64_t)j * ldg] * dr[i] * dr[j];
   };
   double loc_def = 0.0;
+  double h[CQS_U];
 #pragma unroll
   for (int u = 0; u < CQS_U; ++u) {
     const int j = q + CQS_G * u;
+    h[u] = scaled(j);
     if (live_i && j < l && d[i] != 0.0 && d[j] != 0.0)
-      loc_def = fmax(loc_def, fabs(scaled(j) - (i == j ? 1.0 : 0.0)));
+      loc_def = fmax(loc_def, fabs(h[u] - (i == j ? 1.0 : 0.0)));
   }
   {
     const double v = warp_max(loc_def);
@@ -389,13 +403,14 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
   for (int w = 0; w < CQS_T / 32; ++w) defect = fmax(defect, red[w]);
   double shift = 0.0;
   int attempt = 0;
-  double h[CQS_U];
   for (;;) {
     double dg = 0.0;  // this row's diagonal entry, tracked by all CQS_G threads of the row
+    if (attempt) {  // shifted retry: rebuild the scaled rows
 #pragma unroll
-    for (int u = 0; u < CQS_U; ++u) {
-      const int j = q + CQS_G * u;
-      h[u] = scaled(j) + ((i == j && live_i) ? shift : 0.0);
+      for (int u = 0; u < CQS_U; ++u) {
+        const int j = q + CQS_G * u;
+        h[u] = scaled(j) + ((i == j && live_i) ? shift : 0.0);
+      }
     }
     if (live_i) dg = scaled(i) + shift;
     if (t == 0) s_fail = 0;
@@ -405,6 +420,10 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
       double* rb = rowbuf[j & 1];
       // all threads read the pivot of row j from the row's owners' copy: the
       // owners publish 1 / r_jj with the row
+      // branch-free row work: entries left of the diagonal (c < j for the
+      // owner, c < i in the update) are computed too but never read as
+      // results (R below the diagonal is masked at the output), and every
+      // value involved stays finite
       if (i == j) {
         if (!(dg > 0.0)) {
           if (q == 0) s_fail = 1;
@@ -415,11 +434,9 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
 #pragma unroll
           for (int u = 0; u < CQS_U; ++u) {
             const int c = q + CQS_G * u;
-            if (c < l && c >= j) {
-              const double v = (c == j) ? rjj : h[u] * inv;
-              rb[c] = v;
-              Rs[j * CQS_L + c] = v;
-            }
+            const double v = (c == j) ? rjj : h[u] * inv;
+            rb[c] = v;
+            Rs[j * CQS_L + c] = v;
           }
         }
       }
@@ -428,14 +445,11 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
         fail = true;
         break;
       }
-      if (live_i && i > j) {
+      if (i > j) {
         const double mi = rb[i];
         dg = fma(-mi, mi, dg);
 #pragma unroll
-        for (int u = 0; u < CQS_U; ++u) {
-          const int c = q + CQS_G * u;
-          if (c < l && c >= i) h[u] = fma(-mi, rb[c], h[u]);
-        }
+        for (int u = 0; u < CQS_U; ++u) h[u] = fma(-mi, rb[q + CQS_G * u], h[u]);
       }
     }
     if (!fail) break;
@@ -454,25 +468,20 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
   for (int u = 0; u < CQS_U; ++u) x[u] = (q + CQS_G * u == i) ? 1.0 : 0.0;
   for (int r = l - 1; r >= 0; --r) {
     double* rb = rowbuf[r & 1];
+    // row r of X is zero left of the diagonal, so the updates need no masks
     if (i == r) {
       const double inv = dinv[r];
 #pragma unroll
       for (int u = 0; u < CQS_U; ++u) {
-        const int c = q + CQS_G * u;
-        if (c < l && c >= r) {
-          x[u] *= inv;
-          rb[c] = x[u];
-        }
+        x[u] *= inv;
+        rb[q + CQS_G * u] = x[u];
       }
     }
     __syncthreads();
     if (i < r) {
       const double rk = Rs[i * CQS_L + r];
 #pragma unroll
-      for (int u = 0; u < CQS_U; ++u) {
-        const int c = q + CQS_G * u;
-        if (c < l && c >= r) x[u] = fma(-rk, rb[c], x[u]);
-      }
+      for (int u = 0; u < CQS_U; ++u) x[u] = fma(-rk, rb[q + CQS_G * u], x[u]);
     }
   }
   // R = Rh D, Rinv = D^-1 Rh^-1; dead columns -> zero rows / columns
@@ -486,7 +495,7 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
       if (j >= l) continue;
       const bool dead = d[i] == 0.0 || d[j] == 0.0;
       if (R) R[i + (int64_t)j * ldr] = rk(i, j);
-      Rinv[i + (int64_t)j * ldri] = (dead || j < i) ? 0.0 : x[u] / d[i];
+      Rinv[i + (int64_t)j * ldri] = (dead || j < i) ? 0.0 : x[u] * dr[i];
     }
   }
   if (Racc) {  // Racc <- R Racc (both upper triangular), in place
@@ -607,7 +616,7 @@ static bool cqs_enabled() {
   return v == 1;
 }
 
-static size_t cholqr_bytes(int64_t l) { return (size_t)3 * l * l * 8 + (size_t)l * 8 + 64; }
+static size_t cholqr_bytes(int64_t l) { return (size_t)3 * l * l * 8 + (size_t)3 * l * 8 + 64; }
 
 int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
                   int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,

@@ -85,7 +85,8 @@ def test_reference_adds_angles_and_wedin(capsys, mat, tmp_path):
     assert len(rep["angles"]["mode_degrees"]) == 3 and max(rep["angles"]["principal_degrees"]) < 1
     assert set(rep["wedin"]) >= {"r_norm", "s_norm", "omega_hat", "measure", "ceiling"}
     g = _run(capsys, "run", "gram", path, "--k", "3", "--reference", path)
-    assert max(g["angles"]["principal_degrees"]) < 1e-6 and "wedin" in g
+    # the Gram path squares the conditioning: agreement to ~1e-7 rad
+    assert max(g["angles"]["principal_degrees"]) < 1e-5 and "wedin" in g
 
 
 def test_save_factor_and_compare(capsys, mat, tmp_path):
