@@ -651,9 +651,10 @@ int gj_gram_eigh(const double* X, int64_t ldx, const int* piv, const int64_t* ra
                  int64_t r, double* sigma, double* T, int64_t ldt, int64_t* info, void* ws,
                  size_t ws_bytes, cudaStream_t s);
 
-int gj_gram_eigh_large(const double* G, int64_t ldg, int64_t g, int64_t r, double* sigma,
-                       double* T, int64_t ldt, int64_t* info, void* ws, size_t ws_bytes,
-                       cudaStream_t s) {
+// Grid pivoted Cholesky of G into the workspace: X = R^T (written over W),
+// piv, rank; *rest / *rest_bytes = the workspace left for the Jacobi stage.
+int gj_pivchol(const double* G, int64_t ldg, int64_t g, void* ws, size_t ws_bytes, double** Xo,
+               int** pivo, int64_t** ranko, void** rest, size_t* rest_bytes, cudaStream_t s) {
   const size_t need = gj_gram_large_ws_bytes(g);
   POD_REQUIRE(need > 0, "gram eigh: g = %lld exceeds the grid Jacobi solver", (long long)g);
   POD_REQUIRE(ws_bytes >= need, "gram eigh: workspace too small (%zu < %zu)", ws_bytes, need);
@@ -688,8 +689,29 @@ int gj_gram_eigh_large(const double* G, int64_t ldg, int64_t g, int64_t r, doubl
   cudaError_t e = cudaLaunchKernelEx(&cfg, gj::gpivchol_kernel, G, ldg, (int)g, W, Rq, piv, rank,
                                      ctl, cv, ci);
   if (e != cudaSuccess) return cuda_status(e, "grid pivoted cholesky launch");
-  return gj_gram_eigh(W, g, piv, rank, g, r, sigma, T, ldt, info, jws,
-                      ws_bytes - (size_t)(jws - (char*)ws), s);
+  *Xo = W;
+  *pivo = piv;
+  *ranko = rank;
+  *rest = jws;
+  *rest_bytes = ws_bytes - (size_t)(jws - (char*)ws);
+  return POD_OK;
+}
+
+int gj_gram_eigh(const double* X, int64_t ldx, const int* piv, const int64_t* rank, int64_t g,
+                 int64_t r, double* sigma, double* T, int64_t ldt, int64_t* info, void* ws,
+                 size_t ws_bytes, cudaStream_t s);
+
+int gj_gram_eigh_large(const double* G, int64_t ldg, int64_t g, int64_t r, double* sigma,
+                       double* T, int64_t ldt, int64_t* info, void* ws, size_t ws_bytes,
+                       cudaStream_t s) {
+  double* X;
+  int* piv;
+  int64_t* rank;
+  void* rest;
+  size_t rest_bytes;
+  int st = gj_pivchol(G, ldg, g, ws, ws_bytes, &X, &piv, &rank, &rest, &rest_bytes, s);
+  if (st) return st;
+  return gj_gram_eigh(X, g, piv, rank, g, r, sigma, T, ldt, info, rest, rest_bytes, s);
 }
 
 int gj_gram_eigh(const double* X, int64_t ldx, const int* piv, const int64_t* rank, int64_t g,

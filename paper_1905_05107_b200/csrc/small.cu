@@ -638,6 +638,8 @@ size_t gj_gram_large_ws_bytes(int64_t g);
 int gj_gram_eigh_large(const double* G, int64_t ldg, int64_t g, int64_t r, double* sigma,
                        double* T, int64_t ldt, int64_t* info, void* ws, size_t ws_bytes,
                        cudaStream_t s);
+int gj_pivchol(const double* G, int64_t ldg, int64_t g, void* ws, size_t ws_bytes, double** Xo,
+               int** pivo, int64_t** ranko, void** rest, size_t* rest_bytes, cudaStream_t s);
 int gj_gram_eigh(const double* X, int64_t ldx, const int* piv, const int64_t* rank, int64_t g,
                  int64_t r, double* sigma, double* T, int64_t ldt, int64_t* info, void* ws,
                  size_t ws_bytes, cudaStream_t s);
@@ -666,8 +668,12 @@ static size_t gram_ws_bytes(int64_t g) {
 // the pivoted Cholesky and run one-sided Jacobi on G itself.
 constexpr int64_t PIVCHOL_MAX_G = 512;
 
+// the single-CTA pivoted Cholesky keeps its packed triangle in shared memory
+// up to this order; beyond it the grid-wide one (gpivchol) runs
+static bool pivchol_in_smem(int64_t g) { return (size_t)g * (g + 1) / 2 * 8 <= SMALL_SMEM_CAP; }
+
 static size_t gram_total_ws(int64_t g) {
-  if (g > PIVCHOL_MAX_G) return gj_gram_large_ws_bytes(g);
+  if (!pivchol_in_smem(g)) return gj_gram_large_ws_bytes(g);
   return gram_ws_bytes(g) + gj_ws_bytes(g, g, 0);
 }
 
@@ -707,8 +713,12 @@ extern "C" int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r,
   int64_t* rank = (int64_t*)(((uintptr_t)(piv + g) + 15) & ~(uintptr_t)15);
   double* scratch = (double*)(((uintptr_t)(rank + 1) + 15) & ~(uintptr_t)15);
   const size_t bytes = (size_t)g * (g + 1) / 2 * 8;  // packed lower triangle
-  const int use_smem = bytes <= SMALL_SMEM_CAP;
-  if (use_smem) {
+  void* jws = (char*)ws + gram_ws_bytes(g);
+  size_t jws_bytes = ws_bytes - gram_ws_bytes(g);
+  if (!pivchol_in_smem(g)) {  // 225 < g <= 512: grid-wide pivoted Cholesky
+    int st = gj_pivchol(G, ldg, g, ws, ws_bytes, &X, &piv, &rank, &jws, &jws_bytes, s);
+    if (st) return st;
+  } else {
     if (g <= 128) {
       int st = set_smem((const void*)pivchol_kernel<true, 4>, bytes);
       if (st) return st;
@@ -720,19 +730,14 @@ extern "C" int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r,
       pivchol_kernel<true, 8><<<1, PIVCHOL_THREADS, bytes, s>>>(G, ldg, (int)g, X, piv, rank,
                                                                 scratch, scratch + (size_t)g * g);
     }
-  } else {
-    pivchol_kernel<false, 16><<<1, PIVCHOL_THREADS, 0, s>>>(G, ldg, (int)g, X, piv, rank, scratch,
-                                                            scratch + (size_t)g * g);
+    POD_CHECK_LAUNCH("pivoted cholesky");
   }
-  POD_CHECK_LAUNCH("pivoted cholesky");
   {
     const int bst = bj_gram_eigh(X, piv, rank, g, r, sigma, T, ldt, info, s);
     if (bst != -1) return bst;  // -1: size not handled by the block solver
   }
   if (cj_fits(g, g, 0)) return cj_gram_eigh(X, piv, rank, g, r, sigma, T, ldt, info, s);
-  const size_t head = gram_ws_bytes(g);
-  return gj_gram_eigh(X, g, piv, rank, g, r, sigma, T, ldt, info, (char*)ws + head,
-                      ws_bytes - head, s);
+  return gj_gram_eigh(X, g, piv, rank, g, r, sigma, T, ldt, info, jws, jws_bytes, s);
 }
 
 extern "C" int pod_cholqr_factor(const double* G, int64_t ldg, int64_t l, int64_t nrows,
