@@ -222,6 +222,28 @@ def cpu_reference_sample(a_host, steps, warmup, n_rounds_full):
     return statistics.mean(est), threads
 
 
+def _host_desc():
+    """CPU model and the BLAS / numpy / scipy versions behind the CPU arm."""
+    model = "unknown CPU"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        import scipy
+        from threadpoolctl import threadpool_info
+
+        blas = ", ".join(sorted({f"{d.get('internal_api')} {d.get('version')}"
+                                 for d in threadpool_info()}))
+        return f"{model}; numpy {np.__version__}, scipy {scipy.__version__}, {blas}"
+    except Exception:
+        return f"{model}; numpy {np.__version__}"
+
+
 def run_reference_arm(args):
     ws, rank, _ = _dist_env()
     if rank != 0:
@@ -254,6 +276,7 @@ def run_reference_arm(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": _config_dict(n_rounds),
         "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port",
+                         "host": _host_desc(),
                          "sample": f"oracle port of podsketch isma_run on the full config-2 "
                                    f"matrix: norm pass + bootstrap + {CPU_SAMPLE_ROUNDS} update "
                                    f"rounds + finalize, extrapolated to {n_rounds} rounds"},
@@ -425,6 +448,7 @@ def main():
             cpu_s, threads = cpu_reference_sample(a_host, 1, 0, n_rounds)
             line["cpu_baseline"] = {
                 "value": cpu_s, "unit": "s", "cores": threads, "kind": "port",
+                "host": _host_desc(),
                 "sample": f"oracle port (numpy/LAPACK) of podsketch isma_run, full config-2 "
                           f"matrix: norm pass + bootstrap + {CPU_SAMPLE_ROUNDS} update rounds + "
                           f"finalize, extrapolated to {n_rounds} rounds"}
