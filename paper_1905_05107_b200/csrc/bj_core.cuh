@@ -186,8 +186,16 @@ struct PairRef {
   double* ny;
 };
 
+// Flags returned by the rotation steps: ROT_DONE = the pair was rotated,
+// ROT_BIG = its cosine exceeded COS_BIG (1e-8).  A sweep in which no pair
+// exceeded COS_BIG ends the iteration: cyclic Jacobi converges
+// quadratically, so the couplings left after it are O(1e-16), below the
+// visit threshold tol -- the next sweep would rotate nothing.
+constexpr int ROT_DONE = 1, ROT_BIG = 2;
+constexpr double COS_BIG2 = 1e-16;
+
 template <int TPP, int RPL>
-__device__ __forceinline__ bool rotate_pair(const PairRef& pr, bool live, int gl, int nrows,
+__device__ __forceinline__ int rotate_pair(const PairRef& pr, bool live, int gl, int nrows,
                                             int njrows, double tol2) {
   constexpr int tpp = TPP;
   double g = 0.0;
@@ -209,8 +217,10 @@ __device__ __forceinline__ bool rotate_pair(const PairRef& pr, bool live, int gl
   const double al = live ? *pr.nx : 0.0, be = live ? *pr.ny : 0.0;
 #pragma unroll
   for (int o = tpp / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o, tpp);
-  if (!live) return false;
-  if (!(g * g > tol2 * al * be && al > 0.0 && be > 0.0)) return false;
+  if (!live) return 0;
+  const double gg = g * g, ab = al * be;
+  const int big = (gg > COS_BIG2 * ab && al > 0.0 && be > 0.0) ? ROT_BIG : 0;
+  if (!(gg > tol2 * ab && al > 0.0 && be > 0.0)) return big;
   double c_, s_;
   rot_params(g, al, be, c_, s_);
   if (RPL > 0) {
@@ -241,7 +251,7 @@ __device__ __forceinline__ bool rotate_pair(const PairRef& pr, bool live, int gl
     *pr.nx = fmax(fma(c2, al, fma(s2, be, -csg)), 0.0);
     *pr.ny = fma(s2, al, fma(c2, be, csg));
   }
-  return true;
+  return ROT_DONE | big;
 }
 
 __device__ __forceinline__ int pow2_floor(int v) {
@@ -253,12 +263,12 @@ __device__ __forceinline__ int pow2_floor(int v) {
 // One sub-round: P disjoint pairs in parallel; pairs produced by `pick(k,
 // &x_slot, &x_col, &y_slot, &y_col)`; returns whether this thread's pair rotated.
 template <int TPP, int RPL, typename Pick>
-__device__ bool sub_round(const Slot& c0, const Slot& c1, const Geo& g, int P, double tol2,
+__device__ int sub_round(const Slot& c0, const Slot& c1, const Geo& g, int P, double tol2,
                           Pick pick) {
   constexpr int tpp = TPP;
   const int grp = threadIdx.x / tpp, gl = threadIdx.x % tpp;
   const int ngrp = blockDim.x / tpp;
-  bool rot = false;
+  int rot = 0;
   // groups beyond P still take part in the shuffles (full-warp masks)
   for (int k0 = 0; k0 < P; k0 += ngrp) {
     const int k = k0 + grp;
@@ -284,7 +294,7 @@ __device__ bool sub_round(const Slot& c0, const Slot& c1, const Geo& g, int P, d
 // in registers when RPL > 0, norm in a register) and meets bottom columns
 // k, k+1, ... (mod bs) in bs sub-rounds.
 template <int TPP, int RPL>
-__device__ bool inter_step(const Slot& c0, const Slot& c1, const Geo& g, double tol2) {
+__device__ int inter_step(const Slot& c0, const Slot& c1, const Geo& g, double tol2) {
   const int bs = g.bs;
   constexpr int tpp = TPP;
   const int grp = threadIdx.x / tpp, gl = threadIdx.x % tpp;
@@ -315,7 +325,7 @@ __device__ bool inter_step(const Slot& c0, const Slot& c1, const Geo& g, double 
     }
   }
   double al = xlive ? c0.nrm[xc] : 0.0;
-  bool rot = false;
+  int rot = 0;
 #ifdef POD_BJ_TIMING
   unsigned long long _bi_last = clock64();
 #endif
@@ -345,6 +355,7 @@ __device__ bool inter_step(const Slot& c0, const Slot& c1, const Geo& g, double 
 #pragma unroll
     for (int o = tpp / 2; o > 0; o >>= 1) gam += __shfl_xor_sync(0xffffffffu, gam, o, tpp);
     BJ_TI(9);
+    if (live && gam * gam > COS_BIG2 * al * be && al > 0.0 && be > 0.0) rot |= ROT_BIG;
     if (live && gam * gam > tol2 * al * be && al > 0.0 && be > 0.0) {
       double c_, s_;
       rot_params(gam, al, be, c_, s_);
@@ -390,7 +401,7 @@ __device__ bool inter_step(const Slot& c0, const Slot& c1, const Geo& g, double 
       const double nal = fmax(fma(c2, al, fma(s2, be, -csg)), 0.0);
       if (gl == 0) c1.nrm[yc] = fma(s2, al, fma(c2, be, csg));
       al = nal;
-      rot = true;
+      rot |= ROT_DONE;
     }
     BJ_TI(10);
     __syncthreads();

@@ -75,7 +75,7 @@ __device__ int run_sweeps(cg::cluster_group& cl, const Geo& g, double* slots, ui
     }
     __syncthreads();
     BJ_T(1);
-    bool rot = false;
+    int rot = 0;
     // intra phase: round-robin inside each owned block (both blocks at once)
     {
       const int B = bs + (bs & 1);
@@ -106,7 +106,7 @@ __device__ int run_sweeps(cg::cluster_group& cl, const Geo& g, double* slots, ui
       const bool last = (st == NB - 2);
       if (last) {
         // cluster-wide OR of "rotated this sweep": write my flag everywhere
-        const int any = __syncthreads_or(rot ? 1 : 0);
+        const int any = __syncthreads_or((rot & ROT_BIG) ? 1 : 0);
         if (threadIdx.x < CL) {
           double* dst = cl.map_shared_rank(&flags[(sweep & 1) * CL + me], (int)threadIdx.x);
           *dst = any ? 1.0 : 0.0;
@@ -124,7 +124,7 @@ __device__ int run_sweeps(cg::cluster_group& cl, const Geo& g, double* slots, ui
         double tot = 0.0;
         for (int c = 0; c < CL; ++c) tot += flags[(sweep & 1) * CL + c];
         converged = (tot == 0.0);
-        rot = false;
+        rot = 0;
       }
       if (last && (converged || sweep + 1 >= max_sweeps)) break;
       // move both blocks to their next owners (set -> next set)

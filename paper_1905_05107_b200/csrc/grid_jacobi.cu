@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(double* ws, int n, int nrows
       s.nrm[c] = a;
     }
     __syncthreads();
-    bool rot = false;
+    int rot = 0;
     {  // intra phase: round-robin inside each owned block
       const int B = bs + (bs & 1);
       for (int step = 0; step < B - 1; ++step) {
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(double* ws, int n, int nrows
       rot |= bj::inter_step<TPP, RPL>(c0, c1, g, tol2);
       const bool last = (st == NB - 2);
       if (last) {
-        const int any = __syncthreads_or(rot ? 1 : 0);
+        const int any = __syncthreads_or((rot & bj::ROT_BIG) ? 1 : 0);
         if (threadIdx.x == 0 && any) atomicOr(&ctl->rot[sweep & 1], 1);
         if (me == 0 && threadIdx.x == 0) ctl->rot[(sweep + 1) & 1] = 0;  // next sweep's flag
       }
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(512) sweep_kernel(double* ws, int n, int nrows
       set = nxt;
       if (last) {
         converged = (*(volatile int*)&ctl->rot[sweep & 1]) == 0;
-        rot = false;
+        rot = 0;
       }
       load_slot(c0.w, gslot(L, ws, set, me, 0).w, g.slot);
       load_slot(c1.w, gslot(L, ws, set, me, 1).w, g.slot);
