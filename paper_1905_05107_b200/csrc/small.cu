@@ -287,9 +287,9 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
       if (threadIdx.x == 0) dr2[j] = rinv;
       for (int k = j + threadIdx.x; k < l; k += blockDim.x) C[j + (int64_t)k * l] = (k == j) ? rjj : C[j + (int64_t)k * l] * rinv;
       __syncthreads();
-      const int rem = l - j - 1;
-      for (int64_t t = threadIdx.x; t < (int64_t)rem * rem; t += blockDim.x) {
-        const int kk = j + 1 + (int)(t / rem), ii = j + 1 + (int)(t % rem);
+      const int rem = l - j - 1;  // rem^2 < 2^31: 32-bit index arithmetic
+      for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
+        const int kk = j + 1 + t / rem, ii = j + 1 + t % rem;
         if (ii <= kk) C[ii + (int64_t)kk * l] -= C[j + (int64_t)ii * l] * C[j + (int64_t)kk * l];
       }
       __syncthreads();
@@ -308,7 +308,29 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
     if (i > j) C[t] = 0.0;
   }
   __syncthreads();
-  upper_inverse(C, l, X, dr2);
+  // X = Rh^-1 by right-looking back substitution: step r scales row r
+  // (columns >= r) and subtracts it from the rows above -- one parallel
+  // update of r (l - r) entries per step instead of a warp-sequential column
+  __shared__ double s_row[1024];
+  for (int t = threadIdx.x; t < l * l; t += blockDim.x) {
+    const int j = t / l, i = t - j * l;
+    X[t] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int r = l - 1; r >= 0; --r) {
+    for (int c = r + threadIdx.x; c < l; c += blockDim.x) {
+      const double v = X[r + (int64_t)c * l] * dr2[r];
+      X[r + (int64_t)c * l] = v;
+      s_row[c] = v;
+    }
+    __syncthreads();
+    const int w = l - r;
+    for (int t = threadIdx.x; t < r * w; t += blockDim.x) {
+      const int c = r + t / r, i = t % r;
+      X[i + (int64_t)c * l] = fma(-C[i + (int64_t)r * l], s_row[c], X[i + (int64_t)c * l]);
+    }
+    __syncthreads();
+  }
   // R = Rh D, Rinv = D^-1 Rh^-1; dead columns -> zero rows / columns
   int ndead = 0;
   for (int64_t t = threadIdx.x; t < (int64_t)l * l; t += blockDim.x) {
@@ -671,10 +693,21 @@ constexpr int64_t PIVCHOL_MAX_G = 512;
 // the single-CTA pivoted Cholesky keeps its packed triangle in shared memory
 // up to this order; beyond it the grid-wide one (gpivchol) runs
 static bool pivchol_in_smem(int64_t g) { return (size_t)g * (g + 1) / 2 * 8 <= SMALL_SMEM_CAP; }
+// order from which the grid-wide pivoted Cholesky replaces the single-CTA
+// global-memory one (POD_GRID_PIVCHOL_MIN overrides)
+static int64_t grid_pivchol_min() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_GRID_PIVCHOL_MIN");
+    v = e ? atoll(e) : 300;
+  }
+  return v;
+}
 
 static size_t gram_total_ws(int64_t g) {
-  if (!pivchol_in_smem(g)) return gj_gram_large_ws_bytes(g);
-  return gram_ws_bytes(g) + gj_ws_bytes(g, g, 0);
+  const size_t small = gram_ws_bytes(g) + gj_ws_bytes(g, g, 0);
+  if (!pivchol_in_smem(g)) return std::max(small, gj_gram_large_ws_bytes(g));
+  return small;
 }
 
 extern "C" size_t pod_small_ws_bytes(int64_t n) {
@@ -715,9 +748,13 @@ extern "C" int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r,
   const size_t bytes = (size_t)g * (g + 1) / 2 * 8;  // packed lower triangle
   void* jws = (char*)ws + gram_ws_bytes(g);
   size_t jws_bytes = ws_bytes - gram_ws_bytes(g);
-  if (!pivchol_in_smem(g)) {  // 225 < g <= 512: grid-wide pivoted Cholesky
+  if (!pivchol_in_smem(g) && g >= grid_pivchol_min()) {  // grid-wide pivoted Cholesky
     int st = gj_pivchol(G, ldg, g, ws, ws_bytes, &X, &piv, &rank, &jws, &jws_bytes, s);
     if (st) return st;
+  } else if (!pivchol_in_smem(g)) {  // one CTA, Schur complement in global memory
+    pivchol_kernel<false, 16><<<1, PIVCHOL_THREADS, 0, s>>>(G, ldg, (int)g, X, piv, rank,
+                                                            scratch, scratch + (size_t)g * g);
+    POD_CHECK_LAUNCH("pivoted cholesky");
   } else {
     if (g <= 128) {
       int st = set_smem((const void*)pivchol_kernel<true, 4>, bytes);
@@ -764,6 +801,7 @@ extern "C" int pod_cholqr_factor2(const double* G, int64_t ldg, int64_t l, int64
     return POD_OK;
   }
   POD_REQUIRE(R, "pod_cholqr_factor: l = %lld > 64 needs the R output", (long long)l);
+  POD_REQUIRE(l <= 1024, "pod_cholqr_factor: l = %lld exceeds 1024", (long long)l);
   const size_t bytes = cholqr_bytes(l);
   const int use_smem = bytes <= SMALL_SMEM_CAP;
   POD_REQUIRE(use_smem || ws_bytes >= bytes, "pod_cholqr_factor: workspace too small");

@@ -10,7 +10,7 @@ from paper_1905_05107_b200.device import dptr, get_ctx  # noqa: E402
 
 ctx = get_ctx()
 dev = ctx.device
-for l in (8, 16, 32, 48, 60, 64, 96):
+for l in (8, 16, 32, 48, 60, 64, 96, 150, 192):
     rng = np.random.default_rng(l)
     w = rng.standard_normal((4 * l, l))
     G = torch.as_tensor((w.T @ w).T.copy().reshape(-1), device=dev)
