@@ -49,6 +49,19 @@ REORTH_TOL = 1e-8  # merge.py:34
 # (measured: caps of 148-200 CTAs and forking the update at the round start
 # instead of after the merge's GEMM phase are within noise or slower)
 UPDATE_GRID_CAP = int(__import__("os").environ.get("POD_UPDATE_GRID_CAP", "0"))
+#: CTA cap for the merge's GEMM phase in pipelined rounds: the side stream's
+#: eigensolve holds an 8-CTA cluster plus the pivoted-Cholesky CTA, so the
+#: one-wave GEMM grids (2 CTAs per SM) are sized for the remaining SMs
+#: instead of spilling a partial second wave (config 2: 57.1 -> 55.2 ms).
+#: Default 2 * (SMs - 9); POD_MERGE_GRID_CAP overrides (0 = no cap).
+MERGE_GRID_CAP_ENV = __import__("os").environ.get("POD_MERGE_GRID_CAP")
+
+
+def merge_grid_cap(device):
+    if MERGE_GRID_CAP_ENV is not None:
+        return int(MERGE_GRID_CAP_ENV)
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    return max(2 * (sms - 9), 0)
 CHOLQR_PASSES = 4  # passes 0-1 always (CholeskyQR2); passes 2..3 gated on the previous pass
 
 MODE_L2N, MODE_UNIFORM, MODE_WEIGHTS, MODE_ORT, MODE_ROWS = 0, 1, 2, 3, 4
@@ -343,6 +356,7 @@ class IsmaEngine(MergeWorkspace):
         self.graph_launches = {}
         self.graph_epoch = -1
         self.side = torch.cuda.Stream(dev)
+        self.merge_cap = merge_grid_cap(dev)
         self.ort = None  # (C = U^T A, residual norms) buffers of the "ort" strategy
         self.frob2 = 0.0
         # host-resident A (page-locked, mapped): the norm pass, ort's U^T A and
@@ -538,9 +552,18 @@ class IsmaEngine(MergeWorkspace):
         if pipelined:
             u1, u2 = (ub + 1) % NSLOT, (ub + 2) % NSLOT
             self.side_ops(lambda: self.eigh_ops(u1), join=False)
-            self.merge_ops(cur, ub, before_core=lambda: self.side_ops(
-                lambda: (self.lift_ops(u1, self.Uupd_b[u1].cols(0, self.r)),
-                         self.draw_gram_ops(mode, u2)), join=False))
+            lib = _lib.load()
+            lib.pod_set_grid_cap(self.merge_cap)
+
+            def before_core():
+                lib.pod_set_grid_cap(0)
+                self.side_ops(lambda: (self.lift_ops(u1, self.Uupd_b[u1].cols(0, self.r)),
+                                       self.draw_gram_ops(mode, u2)), join=False)
+
+            try:
+                self.merge_ops(cur, ub, before_core=before_core)
+            finally:
+                lib.pod_set_grid_cap(0)
             self.cosines_ops(cur, 1 - cur)
             torch.cuda.current_stream(self.ctx.device).wait_stream(self.side)
             self.readback()
