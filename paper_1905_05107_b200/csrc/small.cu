@@ -358,21 +358,18 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
 // diagonal entry H[i][i] itself, so the next pivot needs no extra exchange.
 // Rh^-1 is formed the same way by right-looking back substitution.
 constexpr int CQS_L = 64, CQS_T = 256, CQS_G = CQS_T / CQS_L, CQS_U = CQS_L / CQS_G;
+constexpr int CQS_S = CQS_L + 1;  // padded row stride of Rh: row reads across lanes hit distinct banks
 
-// 1/sqrt(x) for normal positive x: fp32 seed (exactly rescaled by a power
-// of four) and three fp64 Newton steps -- no division or sqrt slow path
-__device__ __forceinline__ double rsqrt_pos(double x) {
-  int e;
-  double m = frexp(x, &e);  // x = m 2^e, m in [0.5, 1)
-  if (e & 1) {
-    m *= 2.0;
-    e -= 1;
-  }
-  double y = (double)rsqrtf((float)m);
-  y = y * fma(-0.5 * m, y * y, 1.5);
-  y = y * fma(-0.5 * m, y * y, 1.5);
-  y = y * fma(-0.5 * m, y * y, 1.5);
-  return ldexp(y, -e / 2);
+// 1/sqrt(x) for normal positive x: the MUFU double approximation and two
+// Newton steps (the pivot chain's latency: ~8 dependent operations instead
+// of an exponent split, an fp32 seed and three Newton steps)
+__device__ __forceinline__ double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = -0.5 * x;
+  y = y * fma(h, y * y, 1.5);
+  y = y * fma(h, y * y, 1.5);
+  return y;
 }
 
 __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
@@ -384,21 +381,30 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
     if (gate_out && threadIdx.x == 0) *gate_out = 0;
     return;
   }
+  extern __shared__ double racc_s[];        // Racc, column-major racc_s[j * 64 + k] (Racc only)
   __shared__ double d[CQS_L];               // column scales sqrt(G_ii)
-  __shared__ double Rs[CQS_L * CQS_L];      // Rh, row-major Rs[j * 64 + k]
-  __shared__ double rowbuf[2][CQS_L];
-  __shared__ double dinv[CQS_L];           // 1 / Rh[j][j]
+  __shared__ double Rs[CQS_L * CQS_S];      // Rh, row-major Rs[j * CQS_S + k] (padded)
+  __shared__ double rowbuf[2][2 * CQS_L];   // broadcast row: [Rh row | Y row]
   __shared__ double red[CQS_T / 32];
   __shared__ int s_fail;
   const int t = threadIdx.x, i = t % CQS_L, q = t / CQS_L;
   const bool live_i = i < l;
   __shared__ double dr[CQS_L];  // 1 / d (0 for dead columns)
+  if (Racc) {  // stage the old Racc asynchronously; consumed after the factorisation
+    for (int e = t; e < l * l; e += CQS_T) {
+      const int k = e % l, j = e / l;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(&racc_s[j * CQS_L + k]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa),
+                   "l"(Racc + k + (int64_t)j * ldacc)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   if (t < CQS_L) {
     const double gii = live_i ? G[i + (int64_t)i * ldg] : 0.0;
     const double di = (gii > 0.0) ? sqrt(gii) : 0.0;
     d[t] = di;
     dr[t] = di > 0.0 ? 1.0 / di : 0.0;
-    rowbuf[0][t] = rowbuf[1][t] = 0.0;
   }
   __syncthreads();
   // H = D^-1 G D^-1 (dead columns -> identity); recomputed for a shifted retry
@@ -425,6 +431,10 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
   for (int w = 0; w < CQS_T / 32; ++w) defect = fmax(defect, red[w]);
   double shift = 0.0;
   int attempt = 0;
+  // Y = Rh^-T is formed by the same elimination: the steps applied to
+  // [H | I] leave [Rh | Rh^-T] (thread (i, q) keeps row i of Y at its
+  // columns), so no separate back substitution is needed
+  double y[CQS_U];
   for (;;) {
     double dg = 0.0;  // this row's diagonal entry, tracked by all CQS_G threads of the row
     if (attempt) {  // shifted retry: rebuild the scaled rows
@@ -434,81 +444,58 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
         h[u] = scaled(j) + ((i == j && live_i) ? shift : 0.0);
       }
     }
+#pragma unroll
+    for (int u = 0; u < CQS_U; ++u) y[u] = (q + CQS_G * u == i) ? 1.0 : 0.0;
     if (live_i) dg = scaled(i) + shift;
     if (t == 0) s_fail = 0;
     __syncthreads();
-    bool fail = false;
     for (int j = 0; j < l; ++j) {
       double* rb = rowbuf[j & 1];
-      // all threads read the pivot of row j from the row's owners' copy: the
-      // owners publish 1 / r_jj with the row
-      // branch-free row work: entries left of the diagonal (c < j for the
-      // owner, c < i in the update) are computed too but never read as
-      // results (R below the diagonal is masked at the output), and every
-      // value involved stays finite
+      // the owners of row j publish it scaled by 1 / r_jj; a non-positive
+      // pivot only raises the flag (checked once after the loop) and keeps
+      // every value finite.  Branch-free row work: entries left of the
+      // diagonal are computed too but never read as results.
       if (i == j) {
-        if (!(dg > 0.0)) {
-          if (q == 0) s_fail = 1;
-        } else {
-          const double inv = rsqrt_pos(dg);  // 1 / r_jj
-          const double rjj = dg * inv;
-          if (q == 0) dinv[j] = inv;
+        // pivots below 1e-290 count as breakdown (shifted retry), so the
+        // flush-to-zero approximation never sees a subnormal
+        const bool ok = dg > 1e-290;
+        if (!ok && q == 0) s_fail = 1;
+        const double inv = ok ? rsqrt_fast(dg) : 0.0;  // 1 / r_jj
+        const double rjj = dg * inv;
 #pragma unroll
-          for (int u = 0; u < CQS_U; ++u) {
-            const int c = q + CQS_G * u;
-            const double v = (c == j) ? rjj : h[u] * inv;
-            rb[c] = v;
-            Rs[j * CQS_L + c] = v;
-          }
+        for (int u = 0; u < CQS_U; ++u) {
+          const int c = q + CQS_G * u;
+          const double v = (c == j) ? rjj : h[u] * inv;
+          y[u] *= inv;
+          rb[c] = v;
+          rb[CQS_L + c] = y[u];
+          Rs[j * CQS_S + c] = v;
         }
       }
       __syncthreads();
-      if (s_fail) {
-        fail = true;
-        break;
-      }
       if (i > j) {
         const double mi = rb[i];
         dg = fma(-mi, mi, dg);
 #pragma unroll
-        for (int u = 0; u < CQS_U; ++u) h[u] = fma(-mi, rb[q + CQS_G * u], h[u]);
+        for (int u = 0; u < CQS_U; ++u) {
+          const double rv = rb[q + CQS_G * u];
+          h[u] = fma(-mi, rv, h[u]);
+          y[u] = fma(-mi, rb[CQS_L + q + CQS_G * u], y[u]);
+        }
       }
     }
-    if (!fail) break;
     __syncthreads();
+    if (!s_fail) break;
+    __syncthreads();  // every thread has read s_fail before the retry resets it
     ++attempt;
     // shifted CholeskyQR (Fukaya et al.): s = 11 (m l + l (l + 1)) u ||H||, ||H|| <= l
     const double base = 11.0 * (nrows * l + (double)l * (l + 1)) * 1.1102230246251565e-16 * l;
     shift = (attempt == 1) ? base : shift * 100.0;
     if (attempt > 8) break;
   }
-  __syncthreads();  // Rs complete; rowbuf free
-  // X = Rh^-1 by right-looking back substitution: thread (k, q) keeps row k
-  // of the accumulated right-hand side at its columns
-  double x[CQS_U];
-#pragma unroll
-  for (int u = 0; u < CQS_U; ++u) x[u] = (q + CQS_G * u == i) ? 1.0 : 0.0;
-  for (int r = l - 1; r >= 0; --r) {
-    double* rb = rowbuf[r & 1];
-    // row r of X is zero left of the diagonal, so the updates need no masks
-    if (i == r) {
-      const double inv = dinv[r];
-#pragma unroll
-      for (int u = 0; u < CQS_U; ++u) {
-        x[u] *= inv;
-        rb[q + CQS_G * u] = x[u];
-      }
-    }
-    __syncthreads();
-    if (i < r) {
-      const double rk = Rs[i * CQS_L + r];
-#pragma unroll
-      for (int u = 0; u < CQS_U; ++u) x[u] = fma(-rk, rb[q + CQS_G * u], x[u]);
-    }
-  }
-  // R = Rh D, Rinv = D^-1 Rh^-1; dead columns -> zero rows / columns
+  // R = Rh D, Rinv = D^-1 Rh^-1 = D^-1 Y^T; dead columns -> zero rows / columns
   auto rk = [&](int a, int b) {  // R[a][b]
-    return (d[a] == 0.0 || d[b] == 0.0 || b < a) ? 0.0 : Rs[a * CQS_L + b] * d[b];
+    return (d[a] == 0.0 || d[b] == 0.0 || b < a) ? 0.0 : Rs[a * CQS_S + b] * d[b];
   };
   if (live_i) {
 #pragma unroll
@@ -517,10 +504,13 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
       if (j >= l) continue;
       const bool dead = d[i] == 0.0 || d[j] == 0.0;
       if (R) R[i + (int64_t)j * ldr] = rk(i, j);
-      Rinv[i + (int64_t)j * ldri] = (dead || j < i) ? 0.0 : x[u] * dr[i];
+      // thread (i, q) holds Y[i][j] = Rh^-1[j][i]
+      Rinv[j + (int64_t)i * ldri] = (dead || j > i) ? 0.0 : y[u] * dr[j];
     }
   }
   if (Racc) {  // Racc <- R Racc (both upper triangular), in place
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
     double acc[CQS_U];
 #pragma unroll
     for (int u = 0; u < CQS_U; ++u) acc[u] = 0.0;
@@ -530,11 +520,10 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
 #pragma unroll
         for (int u = 0; u < CQS_U; ++u) {
           const int j = q + CQS_G * u;
-          if (j < l && k <= j) acc[u] = fma(a, Racc[k + (int64_t)j * ldacc], acc[u]);
+          acc[u] = fma((k <= j) ? a : 0.0, racc_s[j * CQS_L + k], acc[u]);
         }
       }
     }
-    __syncthreads();  // every read of the old Racc precedes the writes
     if (live_i) {
 #pragma unroll
       for (int u = 0; u < CQS_U; ++u) {
@@ -795,7 +784,15 @@ extern "C" int pod_cholqr_factor2(const double* G, int64_t ldg, int64_t l, int64
   POD_REQUIRE(R || Racc, "pod_cholqr_factor: no R output");
   cudaStream_t st = (cudaStream_t)stream;
   if (l <= CQS_L && cqs_enabled()) {
-    cholqr_small_kernel<<<1, CQS_T, 0, st>>>(G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr,
+    const size_t dyn = Racc ? sizeof(double) * CQS_L * CQS_L : 0;
+    static bool dyn_set = false;
+    if (dyn && !dyn_set) {
+      cudaError_t e = cudaFuncSetAttribute((const void*)cholqr_small_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      if (e != cudaSuccess) return cuda_status(e, "cholqr small smem attr");
+      dyn_set = true;
+    }
+    cholqr_small_kernel<<<1, CQS_T, dyn, st>>>(G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr,
                                              Racc, ldacc, dinfo, gate_in, gate_out, first_pass);
     POD_CHECK_LAUNCH("cholqr small");
     return POD_OK;
