@@ -107,6 +107,14 @@ __device__ __forceinline__ double rsqrt_d(double x) {
   return rsqrt_nr2(x);
 }
 
+// One third-order step y (1 + e / 2 + 3 e^2 / 8), e = 1 - x y^2, from an
+// fp32-accurate seed of 1 / sqrt(x): error ~ e^3 ~ 2^-63, the accuracy of two
+// Newton steps at a dependent depth of four operations instead of six
+__device__ __forceinline__ double rsqrt_refine3(double y, double x) {
+  const double e = fma(-x, y * y, 1.0);
+  return fma(y * e, fma(0.375, e, 0.5), y);
+}
+
 // Jacobi rotation (c, s) annihilating gamma between columns with squared
 // norms al, be (|theta| <= pi/4; formulas of cluster_jacobi.cu)
 __device__ __forceinline__ void rot_params(double g, double al, double be, double& c_,
@@ -120,9 +128,7 @@ __device__ __forceinline__ void rot_params(double g, double al, double be, doubl
     const float rhf = rsqrtf((float)h2);
     const float xf = 0.5f * fmaf(fabsf((float)d), rhf, 1.0f);
     const float icf = rsqrtf(xf);
-    rh = (double)rhf;
-    rh = rh * fma(-0.5 * h2, rh * rh, 1.5);
-    rh = rh * fma(-0.5 * h2, rh * rh, 1.5);
+    rh = rsqrt_refine3((double)rhf, h2);
     ic = (double)icf;
   } else {
     rh = rsqrt_nr2(h2);
@@ -130,8 +136,7 @@ __device__ __forceinline__ void rot_params(double g, double al, double be, doubl
   }
   const double x = 0.5 * fma(fabs(d), rh, 1.0);  // in [0.5, 1]
   if (ic < 0.0) ic = (double)rsqrtf((float)x);
-  ic = ic * fma(-0.5 * x, ic * ic, 1.5);
-  ic = ic * fma(-0.5 * x, ic * ic, 1.5);
+  ic = rsqrt_refine3(ic, x);
   c_ = x * ic;
   s_ = copysign(fabs(g) * rh * ic, d * g);
 }
