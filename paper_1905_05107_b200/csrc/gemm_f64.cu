@@ -679,11 +679,14 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p
   int kb = 0, st_c = 0, st_l = ST - 1;
   int64_t c_r0 = (int64_t)blockIdx.x * C::BM;
   for (int64_t it = 0; it < total; ++it) {
+    // stage `it` has landed once at most ST - 2 groups are pending; after the
+    // barrier every warp is done with stage it - 1, which the prefetch below
+    // refills -- one barrier per stage
+    cp_async_wait<ST - 2>();
+    __syncthreads();
     if (it + ST - 1 < total) load_stage(st_l);
     if (++st_l == ST) st_l = 0;
     cp_async_commit();
-    cp_async_wait<ST - 1>();
-    __syncthreads();
     if (kb == 0) {
 #pragma unroll
       for (int f = 0; f < 4; ++f)
@@ -708,7 +711,6 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p
 #pragma unroll
         for (int g = 0; g < C::FN; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
     }
-    __syncthreads();  // this stage is refilled by the next iteration's prefetch
     if (++kb == nkb) {
       kb = 0;
       const int64_t row0 = c_r0 + wm * 32;
