@@ -149,31 +149,62 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
   const int64_t r1 = min(m, r0 + rows_per_split);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  // Each thread loads row (r + lane) of 8 columns per operand per stage.
-  const TX* xp[8];
-  const TY* yp[8];
-  bool xv[8], yv[8];
+  // fp64 operands move row PAIRS with 16-byte copies: thread -> columns
+  // tid / 16 + 16 i (i < 4), rows 2 (tid % 16) and +1 of each stage; other
+  // operand types copy one element (column warp + 8 i, row lane)
+  constexpr bool PAIRS = sizeof(TX) == 8 && sizeof(TY) == 8;
+  constexpr int NPC = PAIRS ? 4 : 8;
+  const TX* xp[NPC];
+  const TY* yp[NPC];
+  bool xv[NPC], yv[NPC], xal[NPC], yal[NPC];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int cx = tp * BP + warp + 8 * i;
-    int cy = tq * BQ + warp + 8 * i;
+  for (int i = 0; i < NPC; ++i) {
+    const int cl = PAIRS ? (int)(threadIdx.x >> 4) + 16 * i : warp + 8 * i;
+    int cx = tp * BP + cl;
+    int cy = tq * BQ + cl;
     xv[i] = cx < p && (!xcols || xcols[cx] >= 0);  // index -1: zero column (padding)
     yv[i] = cy < q && (!ycols || ycols[cy] >= 0);
     xp[i] = xv[i] ? colptr(X, ldx, xcols, cx) : X;
     yp[i] = yv[i] ? colptr(Y, ldy, ycols, cy) : Y;
+    xal[i] = ((uintptr_t)xp[i] & 15) == 0;  // 16-byte copies need an aligned column
+    yal[i] = ((uintptr_t)yp[i] & 15) == 0;
   }
   TX* const xs0 = reinterpret_cast<TX*>(smem_raw);
   TY* const ys0 = reinterpret_cast<TY*>(smem_raw + size_t(STAGES) * TILE_DBL * sizeof(TX));
   auto load_stage = [&](int st, int64_t rb) {
     TX* xs = xs0 + (size_t)st * TILE_DBL;
     TY* ys = ys0 + (size_t)st * TILE_DBL;
-    const int64_t row = rb + lane;
-    const bool rv = row < r1;
+    if constexpr (PAIRS) {
+      const int r2 = 2 * (threadIdx.x & 15);
+      const int64_t row = rb + r2;  // even: splits and stages start at multiples of BK
+      const bool v0 = row < r1, v1 = row + 1 < r1;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int c = warp + 8 * i;
-      cp_async_elem(xs + c * LDS + lane, xv[i] && rv ? xp[i] + row : X, xv[i] && rv);
-      cp_async_elem(ys + c * LDS + lane, yv[i] && rv ? yp[i] + row : Y, yv[i] && rv);
+      for (int i = 0; i < NPC; ++i) {
+        const int c = (int)(threadIdx.x >> 4) + 16 * i;
+        TX* dx = xs + c * LDS + r2;
+        TY* dy = ys + c * LDS + r2;
+        if (xv[i] && v1 && xal[i]) {
+          cp_async16(dx, xp[i] + row, true);
+        } else {
+          cp_async_elem(dx, xv[i] && v0 ? xp[i] + row : X, xv[i] && v0);
+          cp_async_elem(dx + 1, xv[i] && v1 ? xp[i] + row + 1 : X, xv[i] && v1);
+        }
+        if (yv[i] && v1 && yal[i]) {
+          cp_async16(dy, yp[i] + row, true);
+        } else {
+          cp_async_elem(dy, yv[i] && v0 ? yp[i] + row : Y, yv[i] && v0);
+          cp_async_elem(dy + 1, yv[i] && v1 ? yp[i] + row + 1 : Y, yv[i] && v1);
+        }
+      }
+    } else {
+      const int64_t row = rb + lane;
+      const bool rv = row < r1;
+#pragma unroll
+      for (int i = 0; i < NPC; ++i) {
+        const int c = warp + 8 * i;
+        cp_async_elem(xs + c * LDS + lane, xv[i] && rv ? xp[i] + row : X, xv[i] && rv);
+        cp_async_elem(ys + c * LDS + lane, yv[i] && rv ? yp[i] + row : Y, yv[i] && rv);
+      }
     }
   };
 
