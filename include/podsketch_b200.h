@@ -38,6 +38,8 @@ extern "C" {
 #define POD_F32 1
 
 #define POD_OK 0
+/* sticky CholeskyQR-breakdown slot of the dinfo vector */
+#define POD_DINFO_BREAKDOWN 8
 #define POD_EPARAM 2
 #define POD_EFORMAT 3
 #define POD_EDEGENERATE 4
@@ -51,13 +53,29 @@ const char* pod_last_error(void);
 
 /* Squared column norms ||A[:, j]||^2 and a non-finite flag, one HBM pass.
  * Replaces matcore.py:54 (isfinite), isma.py:260 and sampling.py:136
- * (einsum "ij,ij->j").  nonfinite is set to 1 if any entry is NaN/Inf. */
+ * (np.einsum("ij,ij->j", a, a)) BIT-EXACTLY: the sums follow numpy 2.3's
+ * einsum order for a contiguous column (two lanes; per 8-row block
+ * acc_l = x[i+l]^2 + (x[i+2+l]^2 + (x[i+4+l]^2 + (x[i+6+l]^2 + acc_l))),
+ * products and sums each rounded; the m % 8 tail lane-pairwise; acc_0 +
+ * acc_1), see exact_sums.cu.  nonfinite is set to 1 if any entry is NaN/Inf.
+ * Columns are streamed through shared memory with cp.async.bulk when A and
+ * lda * sizeof(element) are 16-byte aligned. */
 int pod_colnorms2_f64(const double* A, int64_t m, int64_t n, int64_t lda, double* norms2,
                       int32_t* nonfinite, void* stream);
-/* Same for a POD_F64 or POD_F32 stored A (fp64 accumulation of the exactly
- * upcast values, as_dense's astype(float64), matcore.py:49). */
+/* Same for a POD_F64 or POD_F32 stored A (the exactly upcast values,
+ * as_dense's astype(float64), matcore.py:49). */
 int pod_colnorms2(int atype, const void* A, int64_t m, int64_t n, int64_t lda, double* norms2,
                   int32_t* nonfinite, void* stream);
+/* The same pass over one ROW SEGMENT of A, continuing the einsum lane state:
+ * state_in (2n doubles: acc_0, acc_1 per column; NULL = zeros) is the state
+ * after the rows above this segment; a non-final segment (last = 0, m a
+ * multiple of 8) writes the state after its rows to state_out, the final
+ * one adds the tail and writes norms2.  The row-sharded engine hands the
+ * state from rank to rank (parallel.py), so sharded norms equal the
+ * single-GPU (and numpy) ones bit for bit.  nonfinite is OR-ed, not reset. */
+int pod_colnorms2_chain(int atype, const void* A, int64_t m, int64_t n, int64_t lda,
+                        const double* state_in, double* state_out, int last, double* norms2,
+                        int32_t* nonfinite, void* stream);
 
 /* Inverse-CDF draw with replacement + unique/counts + retirement.
  * Replaces sampling.py:204-222 (sample_with_replacement) together with the
@@ -74,11 +92,26 @@ int pod_colnorms2(int atype, const void* A, int64_t m, int64_t n, int64_t lda, d
  * Outputs: idx_out[0..g) ascending int32 (idx_out[g..cap) = -1: zero-column
  * padding for the gathered GEMMs), cnt_out[0..g) int64,
  * info[0] = g, info[1] = |S| after the draw, info[2] = status
- * (0 ok, 1 empty S, 2 all weights zero -> DegenerateDistributionError). */
+ * (0 ok, 1 empty S, 2 all weights zero -> DegenerateDistributionError).
+ * Modes 0-3 reproduce numpy's arithmetic exactly (pod_draw_exact), so the
+ * index sets equal the reference's by construction given equal weights. */
 size_t pod_draw_ws_bytes(int64_t n);
 int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n, const double* uniforms,
              int64_t c, int32_t* idx_out, int64_t* cnt_out, int64_t cap, void* ws,
              size_t ws_bytes, int64_t* info, double thr, double* p_out, void* stream);
+
+/* Column draw of modes 0-3 in numpy's exact summation order: the candidate
+ * set compacted in ascending order (setdiff1d), the from_weights total and
+ * the __post_init__ renormalisation as numpy pairwise sums (sampling.py:47-50,
+ * 62-65; blocks of <= 128 with 8 accumulators, split at n/2 rounded down to
+ * a multiple of 8), np.cumsum as a sequential running sum (sampling.py:214),
+ * the pin, searchsorted(side="right") and np.unique (sampling.py:215-221).
+ * Same outputs as pod_draw; p_out is not supported. */
+size_t pod_draw_exact_ws_bytes(int64_t n);
+int pod_draw_exact(int mode, const double* weights, uint8_t* live, int64_t n,
+                   const double* uniforms, int64_t c, int32_t* idx_out, int64_t* cnt_out,
+                   int64_t cap, void* ws, size_t ws_bytes, int64_t* info, double thr,
+                   void* stream);
 
 /* Row sampling (ICRS) building blocks, isma.py:168-176:
  * out[i] = (sum_j X[i, cols[j]]^2) / div (div = *div_dev when non-null) --
@@ -193,7 +226,10 @@ int pod_gram_eigh(const double* G, int64_t ldg, int64_t g, int64_t r, double* si
  * and W = Q R.  Column-scaled, shifted on breakdown, exactly-zero columns
  * dropped (zero R rows).  Replaces the Householder QR of merge.py:70,76 and
  * matcore.py:209.  dinfo[0] = max |D^-1 G D^-1 - I| (input defect),
- * dinfo[1] = shift attempts, dinfo[2] = dropped columns, dinfo[3] = shift.
+ * dinfo[1] = shift attempts, dinfo[2] = dropped columns, dinfo[3] = shift;
+ * dinfo[POD_DINFO_BREAKDOWN] is SET to 1 (never cleared here) when every
+ * shifted retry broke down -- the factor is then unusable and the caller
+ * must raise (the engine checks it with each round's record).
  * Runs iff gate_in is null or *gate_in != 0; gate_out (nullable) receives
  * whether ANOTHER pass is needed: 1 after a first pass, else
  * (ran && (defect > 1e-4 || shifted)). */

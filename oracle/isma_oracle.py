@@ -98,6 +98,70 @@ def column_norms2(a):
     return np.einsum("ij,ij->j", a, a)
 
 
+def einsum_lane_state(a, state=None):
+    """numpy's einsum("ij,ij->j") order (einsum_sumprod.c.src,
+    sum_of_products_contig_contig_outstride0_two at the x86-64 SSE2 baseline:
+    two lanes, separately rounded mul and add) over the 8-row blocks of the
+    row segment `a` (rows a multiple of 8), continuing the lane state
+    (2, n) of the rows above.  Vectorised over columns; the GPU's chained
+    norm pass (pod_colnorms2_chain) hands the same state between row shards."""
+    a = np.asarray(a, dtype=np.float64)
+    m, n = a.shape
+    if m % 8:
+        raise OracleParamError("a non-final segment needs a multiple of 8 rows")
+    st = np.zeros((2, n)) if state is None else np.array(state, dtype=np.float64)
+    a0, a1 = st[0], st[1]
+    for i in range(0, m, 8):
+        for lane_hi in (6, 4, 2, 0):
+            x0, x1 = a[i + lane_hi], a[i + lane_hi + 1]
+            a0 = x0 * x0 + a0
+            a1 = x1 * x1 + a1
+    return np.stack([a0, a1])
+
+
+def einsum_lane_finish(a_tail, state):
+    """The m % 8 tail of einsum's loop (lane pairs, zero filled) and acc0 + acc1."""
+    a_tail = np.asarray(a_tail, dtype=np.float64)
+    a0, a1 = np.array(state[0]), np.array(state[1])
+    t = a_tail.shape[0]
+    for i in range(0, t, 2):
+        a0 = a_tail[i] * a_tail[i] + a0
+        nxt = a_tail[i + 1] * a_tail[i + 1] if i + 1 < t else np.zeros_like(a0)
+        a1 = nxt + a1
+    return a0 + a1
+
+
+def pairwise_sum(x):
+    """numpy's pairwise summation of a contiguous float64 vector
+    (loops_utils.h.src: blocks <= 128 with 8 accumulators, split at n/2
+    rounded down to a multiple of 8), as ndarray.sum() does it."""
+    x = [float(v) for v in np.asarray(x, dtype=np.float64)]
+
+    def pw(lo, n):
+        if n < 8:
+            res = 0.0
+            for i in range(n):
+                res = res + x[lo + i]
+            return res
+        if n <= 128:
+            r = x[lo:lo + 8]
+            i = 8
+            while i < n - n % 8:
+                for j in range(8):
+                    r[j] = r[j] + x[lo + i + j]
+                i += 8
+            res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+            while i < n:
+                res = res + x[lo + i]
+                i += 1
+            return res
+        n2 = n // 2
+        n2 -= n2 % 8
+        return pw(lo, n2) + pw(lo + n2, n - n2)
+
+    return 0.0 + pw(0, len(x)) if x else 0.0
+
+
 def normalized_weights(raw):
     """sampling.py:55-65 (from_weights) followed by sampling.py:34-53
     (__post_init__): raw/sum, then renormalised by the new sum."""

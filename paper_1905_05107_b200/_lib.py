@@ -35,7 +35,11 @@ SIGNATURES = {
     "pod_last_error": (ctypes.c_char_p, []),
     "pod_colnorms2_f64": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "pod_colnorms2": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
+    "pod_colnorms2_chain": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp, _vp, _vp]),
     "pod_draw_ws_bytes": (_sz, [_i64]),
+    "pod_draw_exact_ws_bytes": (_sz, [_i64]),
+    "pod_draw_exact": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp,
+                              _f64, _vp]),
     "pod_draw": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp, _f64,
                         _vp, _vp]),
     "pod_rownorms2": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _f64, _vp, _vp, _vp]),

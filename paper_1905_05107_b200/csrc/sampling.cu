@@ -278,47 +278,15 @@ __global__ void __launch_bounds__(DRAW_THREADS) draw_kernel(
 
 using namespace pod;
 
-extern "C" int pod_colnorms2_f64(const double* A, int64_t m, int64_t n, int64_t lda,
-                                 double* norms2, int32_t* nonfinite, void* stream) {
-  POD_REQUIRE(m > 0 && n > 0 && lda >= m, "pod_colnorms2_f64: bad shape m=%lld n=%lld lda=%lld",
-              (long long)m, (long long)n, (long long)lda);
-  cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s);
-  if (e != cudaSuccess) return cuda_status(e, "colnorms memset");
-  if (m >= 4096) {
-    const bool vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 2 == 0);
-    int grid = (int)std::min<int64_t>(n, 148 * 64);
-    if (vec)
-      colnorms_block_kernel<true><<<grid, 256, 0, s>>>(A, m, n, lda, norms2, nonfinite);
-    else
-      colnorms_block_kernel<false><<<grid, 256, 0, s>>>(A, m, n, lda, norms2, nonfinite);
-  } else {
-    int grid = (int)std::min<int64_t>(ceil_div(n, 8), 148 * 16);
-    colnorms_warp_kernel<<<grid, 256, 0, s>>>(A, m, n, lda, norms2, nonfinite);
-  }
-  POD_CHECK_LAUNCH("colnorms");
-  return POD_OK;
-}
-
-extern "C" int pod_colnorms2(int atype, const void* A, int64_t m, int64_t n, int64_t lda,
-                             double* norms2, int32_t* nonfinite, void* stream) {
-  POD_REQUIRE(atype == POD_F64 || atype == POD_F32, "pod_colnorms2: bad operand type");
-  if (atype == POD_F64)
-    return pod_colnorms2_f64((const double*)A, m, n, lda, norms2, nonfinite, stream);
-  POD_REQUIRE(m > 0 && n > 0 && lda >= m, "pod_colnorms2: bad shape m=%lld n=%lld lda=%lld",
-              (long long)m, (long long)n, (long long)lda);
-  cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e = cudaMemsetAsync(nonfinite, 0, sizeof(int32_t), s);
-  if (e != cudaSuccess) return cuda_status(e, "colnorms memset");
-  const int vec = ((reinterpret_cast<uintptr_t>(A) & 15) == 0) && (lda % 4 == 0);
-  const int grid = (int)std::min<int64_t>(n, 148 * 64);
-  colnorms_f32_kernel<<<grid, 256, 0, s>>>((const float*)A, m, n, lda, vec, norms2, nonfinite);
-  POD_CHECK_LAUNCH("colnorms f32");
-  return POD_OK;
-}
+extern "C" size_t pod_draw_exact_ws_bytes(int64_t n);
+extern "C" int pod_draw_exact(int mode, const double* weights, uint8_t* live, int64_t n,
+                              const double* uniforms, int64_t c, int32_t* idx_out,
+                              int64_t* cnt_out, int64_t cap, void* ws, size_t ws_bytes,
+                              int64_t* info, double thr, void* stream);
 
 extern "C" size_t pod_draw_ws_bytes(int64_t n) {
-  return (size_t)n * (sizeof(double) + sizeof(int32_t)) + 64;
+  return std::max((size_t)n * (sizeof(double) + sizeof(int32_t)) + 64,
+                  pod_draw_exact_ws_bytes(n));
 }
 
 extern "C" int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n,
@@ -333,7 +301,10 @@ extern "C" int pod_draw(int mode, const double* weights, uint8_t* live, int64_t 
               (long long)cap);
   POD_REQUIRE(mode == 1 || weights != nullptr, "pod_draw: weights required");
   POD_REQUIRE(mode == 2 || mode == 4 || live != nullptr, "pod_draw: live mask required");
-  POD_REQUIRE(p_out == nullptr || mode == 4 || mode == 0, "pod_draw: p_out needs mode 0 or 4");
+  POD_REQUIRE(p_out == nullptr || mode == 4, "pod_draw: p_out needs mode 4");
+  if (mode != 4)  // column draws: numpy's exact summation order (exact_sums.cu)
+    return pod_draw_exact(mode, weights, live, n, uniforms, c, idx_out, cnt_out, cap, ws, ws_bytes,
+                          info, thr, stream);
   double* cum = (double*)ws;
   int32_t* counts = (int32_t*)(cum + n);
   draw_kernel<<<1, DRAW_THREADS, 0, (cudaStream_t)stream>>>(mode, weights, live, n, uniforms, c,

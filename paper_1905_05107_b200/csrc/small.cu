@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
     dinfo[1] = (double)attempt;
     dinfo[2] = (double)ndead;
     dinfo[3] = shift;
+    if (s_fail) dinfo[POD_DINFO_BREAKDOWN] = 1.0;  // sticky: the host raises after the round
     if (gate_out) *gate_out = first_pass ? 1 : ((s_defect > 1e-4 || attempt > 0) ? 1 : 0);
   }
 }
@@ -539,6 +540,7 @@ __global__ void __launch_bounds__(CQS_T) cholqr_small_kernel(
     dinfo[1] = (double)attempt;
     dinfo[2] = (double)ndead;
     dinfo[3] = shift;
+    if (s_fail) dinfo[POD_DINFO_BREAKDOWN] = 1.0;  // sticky: the host raises after the round
     if (gate_out) *gate_out = first_pass ? 1 : ((defect > 1e-4 || attempt > 0) ? 1 : 0);
   }
 }

@@ -153,6 +153,12 @@ class Ctx:
         self._call("colnorms2", 1, 2.0 * A.m * A.ncols, A.esize * A.m * A.ncols, "pod_colnorms2",
                    A.code, A.ptr, A.m, A.ncols, A.ld, _ptr(out), _ptr(flag), self.stream)
 
+    def colnorms2_chain(self, A, state_in, state_out, last, out, flag):
+        """One row segment of the einsum-order norm pass (pod_colnorms2_chain)."""
+        self._call("colnorms2", 1, 2.0 * A.m * A.ncols, A.esize * A.m * A.ncols,
+                   "pod_colnorms2_chain", A.code, A.ptr, A.m, A.ncols, A.ld, _ptr(state_in),
+                   _ptr(state_out), int(last), _ptr(out), _ptr(flag), self.stream)
+
     def draw(self, mode, weights, live, n, uniforms, c, idx, cnt, info=None, thr=0.0, p_out=None):
         ws = self.ws("draw", _lib.load().pod_draw_ws_bytes(n))
         self._call("draw", 1, 0.0, 24.0 * n + 8.0 * c, "pod_draw", mode, _ptr(weights),

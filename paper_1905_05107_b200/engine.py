@@ -82,6 +82,14 @@ G_RQR = 6           # second-projection CholeskyQR passes: slots 6..10
 G_FQR = 11          # finalize CholeskyQR passes: 11..15
 N_GATES = 16
 
+DINFO_BREAKDOWN = 8  # POD_DINFO_BREAKDOWN (include/podsketch_b200.h)
+
+#: debug/parity switch: when set, every run copies each round's drawn index
+#: set and counts (the draw slot's idx/cnt, still intact when the round's
+#: record is read) to the host -> IsmaEngine.draw_log, isma.LAST_DRAWS.
+#: Costs one small synchronous D2H per round; off for timed runs.
+RECORD_DRAWS = False
+
 
 #: update slots of the ISMA engine: round t merges slot t % 3 while its side
 #: stream finishes update(t+1) (eigensolve + lift, slot (t+1) % 3) and starts
@@ -133,6 +141,8 @@ class MergeWorkspace:
         self.rec = torch.zeros((1 + nupd, REC_LEN), dtype=torch.int64, device=dev)
         self.h_rec = torch.zeros((1 + nupd, REC_LEN), dtype=torch.int64).pin_memory()
         self.h_xi = torch.zeros(kk, dtype=torch.float64).pin_memory()
+        # sticky CholeskyQR breakdown flag (dinfo[POD_DINFO_BREAKDOWN]), read with the record
+        self.h_breakdown = torch.zeros(1, dtype=torch.float64).pin_memory()
         self.leak = torch.zeros(1, **f64)
         self._qscratch = {}
         self.cur = 0
@@ -263,11 +273,22 @@ class MergeWorkspace:
     def readback(self):
         self.h_rec.copy_(self.rec, non_blocking=True)
         self.h_xi.copy_(self.xi, non_blocking=True)
+        self.h_breakdown.copy_(self.ctx.dinfo[DINFO_BREAKDOWN:DINFO_BREAKDOWN + 1],
+                               non_blocking=True)
+
+    def clear_breakdown(self):
+        self.ctx.dinfo[DINFO_BREAKDOWN:DINFO_BREAKDOWN + 1].zero_()
 
     def read_record(self, ub=0):
         """(record, cosines): merge fields from rec[0], update fields of
         buffer `ub` from rec[1 + ub]."""
         torch.cuda.current_stream(self.ctx.device).synchronize()
+        if self.h_breakdown[0] != 0.0:
+            # every shifted CholeskyQR retry broke down: the factor is unusable
+            # (LAPACK's Householder QR cannot fail; report it like a LAPACK error)
+            self.clear_breakdown()
+            raise np.linalg.LinAlgError("CholeskyQR breakdown: the merge residual could not be "
+                                        "factored after 8 shifted retries")
         hr = self.h_rec.tolist()
         rec = [int(x) for x in hr[0]]
         for i in UPDATE_FIELDS:
@@ -363,6 +384,7 @@ class IsmaEngine(MergeWorkspace):
         # finalize's A^T U stream it over PCIe; each round copies its sampled
         # columns into an HBM block D (multi-pass streamed ISMA)
         self.host_A = not A.t.is_cuda
+        self.draw_log = None
         self._hbuf = None
         self.D = [ColMat.zeros(A.m, g, dev, dtype=A.t.dtype) for _ in range(len(self.Uupd_b))] \
             if self.host_A else None
@@ -395,8 +417,24 @@ class IsmaEngine(MergeWorkspace):
     # ------------------------------------------------------------ pieces --
     def norm_pass(self):
         """Fused validate + column norms (matcore.py:54, isma.py:260)."""
-        self.ctx.colnorms2(self.A, self.norms2, self.nonfinite)
-        self.comm.allreduce_sum_(self.norms2)
+        self.clear_breakdown()
+        comm = self.comm
+        if comm.active:
+            # chained einsum-order pass over the row shards (parallel.py)
+            st_in = st_out = None
+            if comm.rank > 0:
+                st_in = comm.recv(torch.empty(2 * self.n, dtype=torch.float64,
+                                              device=self.ctx.device), comm.rank - 1)
+            last = comm.rank == comm.world - 1
+            if not last:
+                st_out = torch.empty(2 * self.n, dtype=torch.float64, device=self.ctx.device)
+            self.nonfinite.zero_()
+            self.ctx.colnorms2_chain(self.A, st_in, st_out, last, self.norms2, self.nonfinite)
+            if not last:
+                comm.send(st_out, comm.rank + 1)
+            comm.broadcast_(self.norms2, comm.world - 1)
+        else:
+            self.ctx.colnorms2(self.A, self.norms2, self.nonfinite)
         self.comm.allreduce_max_(self.nonfinite)
         flag = int(self.nonfinite.item())
         if flag:
@@ -651,17 +689,31 @@ class IsmaEngine(MergeWorkspace):
             raise ParameterError("generator returned a batch of the wrong shape")
         self.h_uni[b].numpy()[:] = u
         if rows:
+            # the reference raises on a zero row distribution AFTER the column
+            # batch and BEFORE the row batch (isma.py:162-173, sampling.py:62-64)
+            bg = getattr(rng, "bit_generator", None)
+            self._state_before_rows = bg.state if bg is not None else None
             u = np.asarray(rng.random(int(self.w)), dtype=np.float64)
             if u.shape != (self.w,):
                 raise ParameterError("generator returned a batch of the wrong shape")
             self.h_uniw[b].numpy()[:] = u
 
+    def _log_draw(self, b, rec):
+        """RECORD_DRAWS: the index set and counts drawn into slot b this round."""
+        if self.draw_log is None:
+            return
+        g = rec[REC_G]
+        self.draw_log.append((self.idx[b][:g].cpu().numpy().astype(np.int64),
+                              self.cnt[b][:g].cpu().numpy().astype(np.int64)))
+
     def _check_rows(self, rec, rng, state):
-        """A zero row distribution raises (sampling.py:62-64) before the row
-        batch is drawn in the reference: restore the generator, then raise."""
+        """A zero row distribution raises (sampling.py:62-64) after the column
+        batch and before the row batch is drawn in the reference: put the
+        generator back between the two batches, then raise."""
         if rec[REC_HSTATUS] == 2:
-            if state is not None:
-                rng.bit_generator.state = state
+            mid = getattr(self, "_state_before_rows", None)
+            if state is not None and mid is not None:
+                rng.bit_generator.state = mid
             raise DegenerateDistributionError("all row weights are zero")
 
     def _orthonormalize_ops(self, cur, l):
@@ -717,6 +769,8 @@ class IsmaEngine(MergeWorkspace):
         self.sig[cur].copy_(self.sig_upd_b[0][:r])
         self.readback()
         rec, _ = self.read_record(0)
+        self.draw_log = [] if RECORD_DRAWS else None
+        self._log_draw(0, rec)
         if pipelined:
             torch.cuda.current_stream(self.ctx.device).wait_stream(self.side)
         if rows:
@@ -751,6 +805,7 @@ class IsmaEngine(MergeWorkspace):
             self.launch_round(mode, cur, ub, pipelined, rowsrc)
             ran = it
             rec, xi = self.read_record(ub)
+            self._log_draw(ub, rec)
             if rows:
                 self._check_rows(rec, rng, state)
             g, rem = rec[REC_G], rec[REC_REM]
@@ -777,6 +832,9 @@ class IsmaEngine(MergeWorkspace):
         return traces, v
 
     def result(self, keep, v=None):
+        if float(self.ctx.dinfo[DINFO_BREAKDOWN].item()) != 0.0:  # finalize's CholeskyQR
+            self.clear_breakdown()
+            raise np.linalg.LinAlgError("CholeskyQR breakdown in finalize (QR of A^T U)")
         l = min(self.l, keep)
         u = self.gather_rows(self.S[self.cur], l, self.m_total) if l else np.zeros((self.m_total, 0))
         s = self.sig[self.cur][:l].cpu().numpy().copy()

@@ -27,6 +27,7 @@ from .sampling import ctsvd_sample_count, ltsvd_sample_count
 
 STRATEGIES = ("l2n", "unf", "ort", "ls")
 LAST_STATS = {}  # engine statistics of the most recent isma_run (diagnostics)
+LAST_DRAWS = None  # per-round (indices, counts) of the last run when engine.RECORD_DRAWS
 CRITERIA = ("modes", "subspace")
 
 
@@ -172,7 +173,10 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
         raise ParameterError("residency must be 'auto', 'device' or 'host'")
     on_host = not isinstance(a, ColMat) and not (isinstance(a, torch.Tensor) and a.is_cuda)
     if on_host and residency == "auto":
-        nbytes = int(np.prod(getattr(a, "shape", (0,)))) * 8
+        # device storage keeps float32 as float32 (to_device_colmajor)
+        dt = getattr(a, "dtype", None)
+        itemsize = 4 if dt in (np.float32, torch.float32) else 8
+        nbytes = int(np.prod(getattr(a, "shape", (0,)))) * itemsize
         free, _ = torch.cuda.mem_get_info(ctx.device)
         residency = "host" if nbytes > 0.7 * free else "device"
     if on_host and residency == "host" and not comm.active:
@@ -197,8 +201,9 @@ def _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m, r
     u, s, vv = eng.result(keep, v)
     eng.A = None  # the cached engine must not keep the caller's matrix alive
     factor = TruncatedFactor(u, s, vv)
-    global LAST_STATS
+    global LAST_STATS, LAST_DRAWS
     LAST_STATS = eng.stats
+    LAST_DRAWS = eng.draw_log  # per-round (indices, counts) when engine.RECORD_DRAWS
     if return_device:
         return factor, traces, eng
     return factor, traces

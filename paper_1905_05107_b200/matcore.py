@@ -250,6 +250,19 @@ def _svd_device(ctx, A):
     return U, sig, V
 
 
+def _polish_orthonormal(ctx, U, l):
+    """One-sided Jacobi's left vectors w_j / sigma_j are orthogonal to ~2e-14
+    (measured on the reference's acceptance-2 inputs; LAPACK: 2e-15), which
+    the arccos-based principal angles (quality.py:49-57) turn into 1e-5 deg.
+    A CholeskyQR of the l nonzero columns (R = I + O(1e-14), positive
+    diagonal) restores working-precision orthonormality and moves each column
+    by O(1e-14)."""
+    if l < 1:
+        return
+    Q, _ = _qr_device(ctx, U.cols(0, l), l)
+    U.t[U.col0:U.col0 + l, :U.m].copy_(Q.t[Q.col0:Q.col0 + l, :Q.m])
+
+
 def _square(t, n):
     from .device import ColMat
 
@@ -273,6 +286,7 @@ def dense_svd(a):
         A = _transpose(A)
     U, sig, V = _svd_device(ctx, A)
     l = A.ncols
+    _polish_orthonormal(ctx, U, int((sig > 0).sum().item()))
     Vm = _square(V, l)
     ctx.fix_signs(Vm if flip else U, l, U if flip else Vm, U.m if flip else l)
     u, v = U.to_numpy(), Vm.to_numpy()

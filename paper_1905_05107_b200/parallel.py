@@ -6,7 +6,11 @@ follows the same row partition, every r/g/n-sized object is replicated.
 The reference algorithm exchanges data only through a few small reductions
 per round, which become collectives here:
 
-  norms           allreduce(sum) of the n-vector of partial squared norms
+  norms           a chained pass: rank p continues numpy's einsum lane state
+                  (2 n doubles) from rank p - 1 and hands it on (send/recv),
+                  the last rank's norms are broadcast -- the sharded norms
+                  equal the single-GPU and numpy ones bit for bit, so the
+                  draws are the reference's on any rank count
   draw            recomputed on every rank from the identical reduced norms
                   and the identically seeded generator (no broadcast)
   Gram D^T D      allreduce(sum) g x g, then the eigensolver is replicated
@@ -29,9 +33,19 @@ from __future__ import annotations
 import torch
 
 
+#: inner shard boundaries are multiples of this (numpy's einsum works in
+#: 8-row blocks, so a chained norm segment must start on a block boundary)
+ROW_ALIGN = 8
+
+
 def shard_rows(m, world, rank):
-    """Contiguous balanced row range [r0, r1) of `rank` (like ooc.py:61-66)."""
-    return (rank * m) // world, ((rank + 1) * m) // world
+    """Contiguous balanced row range [r0, r1) of `rank` (like ooc.py:61-66),
+    inner boundaries rounded down to a multiple of ROW_ALIGN."""
+    def bound(k):
+        if k >= world:
+            return m
+        return ((k * m) // world) // ROW_ALIGN * ROW_ALIGN
+    return bound(rank), bound(rank + 1)
 
 
 class Comm:
@@ -60,6 +74,27 @@ class Comm:
     def allreduce_max_(self, t):
         if self.world > 1:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return t
+
+    def _host_p2p(self, t):
+        # gloo's point-to-point ops take host tensors only (NCCL takes device ones)
+        return t.is_cuda and self.dist.get_backend(self.group) == "gloo"
+
+    def send(self, t, dst):
+        self.dist.send(t.cpu() if self._host_p2p(t) else t, dst, group=self.group)
+
+    def recv(self, t, src):
+        if self._host_p2p(t):
+            h = torch.empty(t.shape, dtype=t.dtype)
+            self.dist.recv(h, src, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.recv(t, src, group=self.group)
+        return t
+
+    def broadcast_(self, t, src):
+        if self.world > 1:
+            self.dist.broadcast(t, src, group=self.group)
         return t
 
     def allgather(self, t):

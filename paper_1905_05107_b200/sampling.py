@@ -156,18 +156,26 @@ def _check_count_params(k, epsilon, delta):
         raise ParameterError("delta must lie strictly between 0 and 1")
 
 
+def _ltsvd_count_raw(k, epsilon, delta):
+    """Eq. 8a before the ceiling (sampling.py:270-271; the test oracles pin it)."""
+    return 4.0 * k * (1.0 + math.sqrt(8.0 * math.log(1.0 / delta))) ** 2 / epsilon ** 2
+
+
+def _ctsvd_count_raw(k, epsilon, delta):
+    """Eq. 8b before the ceiling (sampling.py:274-275)."""
+    return float(k * k) * (1.0 + math.sqrt(math.log(2.0 / delta))) ** 2 / epsilon ** 4
+
+
 def ltsvd_sample_count(k, epsilon, delta):
     """c = ceil(4k (1 + sqrt(8 ln(1/delta)))^2 / eps^2) (sampling.py:270-276)."""
     _check_count_params(k, epsilon, delta)
-    return int(math.ceil(4.0 * k * (1.0 + math.sqrt(8.0 * math.log(1.0 / delta))) ** 2
-                         / epsilon ** 2))
+    return int(math.ceil(_ltsvd_count_raw(k, epsilon, delta)))
 
 
 def ctsvd_sample_count(k, epsilon, delta):
     """c = w = ceil(k^2 (1 + sqrt(ln(2/delta)))^2 / eps^4) (sampling.py:288-291)."""
     _check_count_params(k, epsilon, delta)
-    return int(math.ceil(float(k * k) * (1.0 + math.sqrt(math.log(2.0 / delta))) ** 2
-                         / epsilon ** 4))
+    return int(math.ceil(_ctsvd_count_raw(k, epsilon, delta)))
 
 
 # ---------------------------------------------------------------------------

@@ -92,15 +92,15 @@ def test_factor_round_trip_and_format_errors(rng):
 def test_read_matrix_validation(tmp_path):
     p = tmp_path / "nan.podm"
     with open(p, "wb") as f:
-        f.write(podio._HEADER.pack(b"PODM", 1, 1, 2))
+        f.write(podio.Podm(1, 2).pack())
         f.write(np.array([1.0, np.nan]).tobytes())
     with pytest.raises(pod.FormatError, match="non-finite"):
         pod.read_matrix(str(p))
     with open(p, "wb") as f:
-        f.write(podio._HEADER.pack(b"PODX", 1, 1, 1))
+        f.write(podio._LAYOUT.pack(b"PODX", 1, 1, 1))
     with pytest.raises(pod.FormatError, match="magic"):
         pod.read_matrix(str(p))
-    a = pod.read_matrix(io.BytesIO(podio._HEADER.pack(b"PODM", 1, 2, 1) + b"\0" * 16))
+    a = pod.read_matrix(io.BytesIO(podio._LAYOUT.pack(b"PODM", 1, 2, 1) + b"\0" * 16))
     assert a.shape == (2, 1) and not a.flags.writeable
 
 

@@ -99,3 +99,34 @@ def test_config2_generator_is_shard_invariant():
         parts = [workloads.config2_torch(3, side=96, n=25, rows=shard_rows(m, world, r))
                  for r in range(world)]
         assert torch.equal(full, torch.cat(parts, 1))
+
+
+def _chained_norms(comm):
+    """The engine's sharded norm protocol (engine.IsmaEngine.norm_pass): rank p
+    continues numpy's einsum lane state from rank p - 1 (recv), hands it on
+    (send), the last rank's norms are broadcast -- here with the oracle's
+    restatement of the lane order standing in for pod_colnorms2_chain."""
+    rng = np.random.default_rng(3)
+    m, n = 1003, 9
+    a = np.asfortranarray(rng.standard_normal((m, n)))
+    r0, r1 = shard_rows(m, comm.world, comm.rank)
+    seg = a[r0:r1]
+    st = None
+    if comm.rank > 0:
+        st = comm.recv(torch.empty(2 * n, dtype=torch.float64), comm.rank - 1).numpy().reshape(2, n)
+    last = comm.rank == comm.world - 1
+    body = seg.shape[0] - (seg.shape[0] % 8 if last else 0)
+    st = orc.einsum_lane_state(seg[:body], st)
+    norms = torch.zeros(n, dtype=torch.float64)
+    if last:
+        norms = torch.as_tensor(orc.einsum_lane_finish(seg[body:], st))
+    else:
+        comm.send(torch.as_tensor(st.reshape(-1).copy()), comm.rank + 1)
+    comm.broadcast_(norms, comm.world - 1)
+    return norms.numpy(), np.einsum("ij,ij->j", a, a)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_chained_norm_pass_over_ranks_equals_numpy(world):
+    for got, ref in run_world(_chained_norms, world=world):
+        assert np.array_equal(got, ref)

@@ -8,7 +8,7 @@ import warnings
 
 import numpy as np
 import pytest
-from conftest import load_golden
+from podtest_util import load_golden
 from parity_util import ANGLE_TOL_RAD, SIGMA_RTOL, principal_angles_sin, sigma_relerr
 
 pytestmark = pytest.mark.gpu

@@ -10,7 +10,7 @@ import sys
 
 import numpy as np
 import pytest
-from conftest import make_low_rank
+from podtest_util import make_low_rank
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")

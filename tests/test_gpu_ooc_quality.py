@@ -5,7 +5,7 @@ import os
 
 import numpy as np
 import pytest
-from conftest import load_golden, make_low_rank, make_noisy_low_rank
+from podtest_util import load_golden, make_low_rank, make_noisy_low_rank
 from parity_util import ANGLE_TOL_RAD, SIGMA_RTOL, principal_angles_sin, sigma_relerr
 
 pytestmark = pytest.mark.gpu

@@ -4,7 +4,7 @@ CPU oracle on the same seeded inputs."""
 
 import numpy as np
 import pytest
-from conftest import load_golden, make_low_rank, make_noisy_low_rank, random_orthonormal
+from podtest_util import load_golden, make_low_rank, make_noisy_low_rank, random_orthonormal
 from parity_util import ANGLE_TOL_RAD, SIGMA_RTOL, principal_angles_sin, sigma_relerr
 
 pytestmark = pytest.mark.gpu

@@ -5,7 +5,7 @@ parity with the CPU oracle on the same generator stream."""
 
 import numpy as np
 import pytest
-from conftest import make_low_rank, make_noisy_low_rank
+from podtest_util import make_low_rank, make_noisy_low_rank
 from parity_util import ANGLE_TOL_RAD, SIGMA_RTOL, principal_angles_sin, sigma_relerr
 
 pytestmark = pytest.mark.gpu
@@ -164,3 +164,26 @@ def test_rows_zero_block_raises_degenerate():
         pod.isma_run(a, cfg)
     with pytest.raises(orc.OracleDegenerate):
         orc.run(a, 1, c=1, tau=1.0, strategy="unf", seed=0, rows=True, w=10)
+
+
+@pytest.mark.gpu
+def test_rows_zero_block_leaves_generator_where_reference_does():
+    """The reference consumes the column batch, then raises on the zero row
+    distribution before drawing the row batch (isma.py:162-173): a caller-owned
+    generator must end in the same state (rollback point)."""
+    a = np.zeros((40, 30))
+    a[:, 0] = np.linspace(1.0, 2.0, 40)
+    cfg = pod.IsmaConfig(k=1, c=1, w=10, tau=1.0, strategy="unf", rows=True, seed=0)
+    for seed in range(6):
+        g_gpu, g_orc = np.random.default_rng(seed), np.random.default_rng(seed)
+        raised = []
+        try:
+            pod.isma_run(a, cfg, rng=g_gpu)
+        except pod.DegenerateDistributionError:
+            raised.append("gpu")
+        try:
+            orc.run(a, 1, c=1, tau=1.0, strategy="unf", rng=g_orc, rows=True, w=10)
+        except orc.OracleDegenerate:
+            raised.append("orc")
+        assert raised in ([], ["gpu", "orc"])
+        assert g_gpu.bit_generator.state == g_orc.bit_generator.state

@@ -4,7 +4,7 @@ reference package) and to the reference test suite's known-answer vectors."""
 
 import numpy as np
 import pytest
-from conftest import load_golden
+from podtest_util import load_golden
 
 from oracle import isma_oracle as orc
 from paper_1905_05107_b200 import workloads
