@@ -37,15 +37,12 @@ def _gram_eigh_dev(D, r):
     ctx = get_ctx()
     dev = ctx.device
     g = D.ncols
-    gmax = int(_lib.load().pod_gram_eigh_max_g())
-    if g > gmax:
-        raise ParameterError(f"sampled Gram of {g} columns exceeds the eigensolver's {gmax}")
     G = torch.empty(g * g, dtype=torch.float64, device=dev)
     ctx.tn(g, g, 1.0, D, D, dptr(G), g, tag="tn_gram")
     sig = torch.empty(g, dtype=torch.float64, device=dev)
     T = torch.empty(g * r, dtype=torch.float64, device=dev)
     info = torch.zeros(4, dtype=torch.int64, device=dev)
-    ctx.gram_eigh(dptr(G), g, g, r, sig, dptr(T), g, info=info)
+    ctx.gram_eigh_any(G, g, r, sig, T, info)
     return sig.cpu().numpy(), T
 
 

@@ -226,6 +226,39 @@ class Ctx:
                    _ptr(self.info if info is None else info), _ptr(ws),
                   ws.numel(), self.stream)
 
+    def gram_eigh_any(self, G, g, r, sigma, T, info):
+        """gram_eigh for any order g: the hand-written solver (pod_gram_eigh)
+        up to pod_gram_eigh_max_g, beyond it cuSOLVER's symmetric eigensolver
+        through torch with the same post-processing (baselines.py:43-48,
+        60-63: descending, clipped, dust <= 1e-12 lambda_1 zeroed, rank =
+        #sigma > 1e-14 sigma_1, keep = min(r, rank), T = V[:, :keep] / sigma,
+        info = (rank, keep, 0)).  G, sigma, T, info are torch tensors; the
+        library branch synchronises (no graph capture).  Used only for
+        column budgets that can draw > 2044 distinct columns (the reference's
+        default budget for k >= 28)."""
+        from . import _lib
+
+        if g <= int(_lib.load().pod_gram_eigh_max_g()):
+            self.gram_eigh(dptr(G), g, g, r, sigma, dptr(T), g, info=info)
+            return
+        w, vec = torch.linalg.eigh(G[:g * g].view(g, g))  # symmetric: layout-agnostic
+        w = w.flip(0).clamp(min=0.0)
+        tiny = torch.finfo(torch.float64).tiny
+        w = torch.where(w <= 1e-12 * torch.clamp(w[0], min=tiny), torch.zeros_like(w), w)
+        sig = w.sqrt()
+        sigma[:g].copy_(sig)
+        s1 = sig[0]
+        rank = torch.where(s1 > 0, (sig > 1e-14 * s1).sum(), torch.zeros_like(s1, dtype=torch.int64))
+        keep = torch.clamp(rank, max=r)
+        cols = torch.arange(r, device=self.device)
+        ok = (cols < keep)[:, None]
+        vr = vec.flip(1)[:, :r].T  # (r, g): row j = eigenvector j
+        denom = torch.where(sig[:r] > 0, sig[:r], torch.ones_like(sig[:r]))[:, None]
+        T[:r * g].view(r, g).copy_(torch.where(ok, vr / denom, torch.zeros_like(vr)))
+        info[0] = rank
+        info[1] = keep
+        info[2] = 0
+
     def cholqr_factor(self, G, ldg, l, nrows, Rinv, ldri, R, ldr, gate_in=None, gate_out=None,
                       first_pass=0):
         ws = self.small_ws(l)

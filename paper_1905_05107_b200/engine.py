@@ -351,10 +351,12 @@ class IsmaEngine(MergeWorkspace):
         self.n = A.ncols
         self.c = int(c)
         gcap = min(self.c, A.ncols)
-        gmax = int(_lib.load().pod_gram_eigh_max_g())
-        if gcap > gmax:
-            raise ParameterError(f"column budget c={self.c} can draw {gcap} distinct columns; "
-                                 f"the sampled-Gram eigensolver takes at most {gmax}")
+        # beyond the hand-written eigensolver's order the library one runs
+        # (Ctx.gram_eigh_any): it synchronises, so such runs are eager and
+        # unpipelined (the reference's default budget for k >= 28)
+        self.big_gram = gcap > int(_lib.load().pod_gram_eigh_max_g())
+        if self.big_gram:
+            use_graphs = False
         super().__init__(ctx, A.m, r, k=k, criterion=criterion, upd_cap=gcap, comm=comm,
                          row_offset=row_offset, nupd=NSLOT)
         self.m_total = A.m if m_total is None else int(m_total)
@@ -552,8 +554,8 @@ class IsmaEngine(MergeWorkspace):
 
     def eigh_ops(self, b):
         g, r = self.gcap, self.r
-        self.ctx.gram_eigh(dptr(self.G[b]), g, g, r, self.sig_upd_b[b], dptr(self.Tl[b]), g,
-                           info=self.rec[1 + b, REC_RANK:])                  # baselines.py:44-48
+        self.ctx.gram_eigh_any(self.G[b], g, r, self.sig_upd_b[b], self.Tl[b],
+                               self.rec[1 + b, REC_RANK:])                   # baselines.py:44-48
 
     def lift_ops(self, b, dest):
         g, r = self.gcap, self.r
@@ -745,7 +747,7 @@ class IsmaEngine(MergeWorkspace):
         # Row-sharded runs pipeline too: every rank issues its collectives in
         # the same program order (update Gram after the merge's GEMM-phase
         # reductions), which the backend serialises on its own stream.
-        pipelined = bitgen is not None and mode != MODE_ORT and not rows
+        pipelined = bitgen is not None and mode != MODE_ORT and not rows and not self.big_gram
         state = bitgen.state if (rows and bitgen is not None) else None
         self._stage_uniforms(rng, 0, rows)
         # generator state before each speculatively staged batch (round -> state)

@@ -278,8 +278,9 @@ def get_update(a, s, u_prev, dist, c, w, rows, rng, r):
         ctx.tn(g, g, 1.0, Y, Y, dptr(G), g)                     # gram_spectrum(y)
     sig = torch.empty(g, dtype=torch.float64, device=dev)
     T = torch.empty(g * int(r), dtype=torch.float64, device=dev)
-    ctx.gram_eigh(dptr(G), g, g, int(r), sig, dptr(T), g)
-    _, keep, _ = ctx.read_info(3)
+    info = torch.zeros(4, dtype=torch.int64, device=dev)
+    ctx.gram_eigh_any(G, g, int(r), sig, T, info)
+    keep = int(info[1].item())
     if keep == 0:
         return TruncatedFactor.empty(m), remaining, g, h
     U = ColMat.zeros(m, keep, dev)

