@@ -179,7 +179,13 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
         nbytes = int(np.prod(getattr(a, "shape", (0,)))) * itemsize
         free, _ = torch.cuda.mem_get_info(ctx.device)
         residency = "host" if nbytes > 0.7 * free else "device"
-    if on_host and residency == "host" and not comm.active:
+    if on_host and residency == "host":
+        # multi-pass streamed ISMA, also row-sharded: each rank
+        # streams its own row block from its page-locked host memory
+        if comm.active and config.strategy == "ort":
+            raise ParameterError("strategy 'ort' with a host-resident row-sharded matrix is not "
+                                 "supported (its C = U^T A must be reduced over ranks before "
+                                 "the residual pass)")
         with HostResident(a) as A:
             return _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m,
                                return_device)

@@ -18,6 +18,9 @@ Noise "N(0, x)" is read as variance x.
   n = 8192, stored float32 (the reference upcasts to float64 in as_dense;
   the kernels upcast exactly, so the fp64 oracle on the upcast is the
   parity reference).
+* ``config5_host`` -- the out-of-core workload: rank-100 exp(-i/20) spectrum
+  + N(0, 1e-5), stored float32 in page-locked host memory, generated block
+  by block (4096-row chunks on the device, copied into the host block).
 * ``config3`` -- power-law low-rank-plus-noise: A = U diag(i^-1.5) V^T +
   N(0, 1e-6), rank 200, m=1,000,000, n=20,000 (160 GB fp64), generated on
   the device.  U is Haar: G R^-1 with G ~ N(0,1) per 4096-row chunk and R the
@@ -176,6 +179,58 @@ def config3_torch(seed=0, m=1_000_000, n=20_000, rank=200, noise_var=1e-6, devic
         at[:, lo - r0:hi - r0].copy_(blk[:, lo - c0:hi - c0])
         del blk, uc
     return at
+
+
+CFG5 = dict(m=4_000_000, n=50_000, rank=100, k=32, r=96, c=128, tol=1e-8)
+
+
+def config5_host(seed=0, m=4_000_000, n=50_000, rank=100, noise_var=1e-5, rows=None,
+                 device="cuda", chunk=NOISE_CHUNK):
+    """BASELINE config 5: A = U diag(exp(-i/20)) V^T + N(0, 1e-5), rank 100,
+    STORED float32 in page-locked HOST memory (800 GB at full size; the
+    out-of-core workload), rows [r0, r1) of it as a pinned torch tensor with
+    storage (n, r1 - r0) -- column-major rows, like ``config2_torch``.
+    Generated block by block from the seed: each 4096-row chunk is made on
+    `device` (the same per-chunk construction as ``config3_torch``: Haar U
+    = G R^-1 with R from the Gram summed over all chunks, Haar V replicated),
+    rounded to float32 once and copied into the host block, so host memory
+    never holds more than the result and any row partition yields the same
+    matrix."""
+    import torch
+
+    dt = torch.float64
+    r0, r1 = (0, m) if rows is None else (int(rows[0]), int(rows[1]))
+    nchunk = (m + chunk - 1) // chunk
+    gv = _chunk_gen(device, seed, 0, 11)
+    v = torch.linalg.qr(torch.randn((n, rank), generator=gv, dtype=dt, device=device))[0]
+    sig = torch.exp(-torch.arange(rank, dtype=dt, device=device) / 20.0)
+    vs = (v * sig).T.contiguous()  # rank x n
+    del v
+
+    def gauss(c):
+        c0, c1 = c * chunk, min(m, (c + 1) * chunk)
+        return torch.randn((c1 - c0, rank), generator=_chunk_gen(device, seed, c, 5), dtype=dt,
+                           device=device)
+
+    gram = torch.zeros((rank, rank), dtype=dt, device=device)
+    for c in range(nchunk):
+        gc = gauss(c)
+        gram += gc.T @ gc
+    rf = torch.linalg.cholesky(gram, upper=True)
+    sd = math.sqrt(noise_var)
+    host = torch.empty((n, r1 - r0), dtype=torch.float32, pin_memory=True)
+    for c in range(r0 // chunk, (r1 + chunk - 1) // chunk):
+        c0, c1 = c * chunk, min(m, (c + 1) * chunk)
+        uc = torch.linalg.solve_triangular(rf, gauss(c), upper=True, left=False)
+        blk = (uc @ vs).T.contiguous()  # n x chunk
+        blk.add_(torch.randn((n, c1 - c0), generator=_chunk_gen(device, seed, c, 3), dtype=dt,
+                             device=device), alpha=sd)
+        lo, hi = max(c0, r0), min(c1, r1)
+        host[:, lo - r0:hi - r0].copy_(blk[:, lo - c0:hi - c0].to(torch.float32))
+        del blk, uc
+    if str(device).startswith("cuda"):
+        torch.cuda.synchronize(device)
+    return host
 
 
 def config3(seed=0, m=20_000, n=2_000, rank=200, noise_var=1e-6):

@@ -70,3 +70,51 @@ def test_two_rank_row_sharded_run_matches_single_gpu(crit):
         assert principal_angles_sin(u, f.u).max() <= ANGLE_TOL_RAD
         assert principal_angles_sin(v, f.v).max() <= ANGLE_TOL_RAD
     np.testing.assert_array_equal(res[0][1], res[1][1])  # identical on every rank
+
+
+def _host_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import paper_1905_05107_b200 as pod
+    from paper_1905_05107_b200 import workloads
+    from paper_1905_05107_b200.parallel import Comm, shard_rows
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = 60_000
+        r0, r1 = shard_rows(m, world, rank)
+        blk = workloads.config5_host(seed=3, m=m, n=900, rows=(r0, r1), device="cuda")
+        cfg = pod.IsmaConfig(k=16, r=48, c=64, tau=1 - 1e-8, strategy="l2n", seed=5)
+        f, tr = pod.isma_run(blk.T, cfg, comm=Comm(), m_total=m, residency="host")
+        q.put((rank, (f.u, f.sigma, f.v, [t.remaining for t in tr])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_host_resident_config5_matches_oracle():
+    """Config 5's layout on two ranks: each rank's row block of the fp32
+    matrix stays in its page-locked host memory (residency="host"), the norm
+    pass is chained over the ranks, rounds gather sampled columns from host
+    memory; identical bookkeeping and factors to the CPU oracle."""
+    from oracle import isma_oracle as orc
+    from paper_1905_05107_b200 import workloads
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_host_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a = workloads.config5_host(seed=3, m=60_000, n=900, device="cuda").numpy().T
+    o = orc.run(a.astype(np.float64), 16, r=48, c=64, tau=1 - 1e-8, strategy="l2n", seed=5)
+    for rank in (0, 1):
+        u, s, v, rem = res[rank]
+        assert rem == [t["remaining"] for t in o["trace"]]
+        assert sigma_relerr(s, o["sigma"]) <= SIGMA_RTOL
+        assert principal_angles_sin(u, o["u"]).max() <= ANGLE_TOL_RAD
+        assert principal_angles_sin(v, o["v"]).max() <= ANGLE_TOL_RAD
