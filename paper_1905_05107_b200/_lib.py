@@ -36,6 +36,10 @@ SIGNATURES = {
     "pod_colnorms2_f64": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "pod_colnorms2": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "pod_colnorms2_chain": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _vp, _i32, _vp, _vp, _vp]),
+    "pod_tc_tn_ws_bytes": (_sz, [_i64, _i64, _i64]),
+    "pod_gemm_tn_tf32x3": (_i32, [_i64, _i64, _i64, _f64, _vp, _vp, _i64, _vp, _vp, _vp, _i64, _vp,
+                                  _vp, _i64, _vp, _sz, _vp]),
+    "pod_split_tf32": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "pod_draw_ws_bytes": (_sz, [_i64]),
     "pod_draw_exact_ws_bytes": (_sz, [_i64]),
     "pod_draw_exact": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp,

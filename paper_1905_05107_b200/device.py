@@ -226,6 +226,24 @@ class Ctx:
                    _ptr(self.info if info is None else info), _ptr(ws),
                   ws.numel(), self.stream)
 
+    def tn_tf32x3(self, p, q, alpha, X, Y, C, ldc, xcols=None, ycols=None, Xlo=None, Ylo=None,
+                  tag="tc_tn"):
+        """C (p x q) = alpha X^T Y on the tcgen05 tensor cores, 3xTF32 with
+        fp32 accumulation over <= 8192-row chunks and an fp64 chunk
+        reduction (pod_gemm_tn_tf32x3): X, Y float32 ColMats (or their fp32
+        hi parts with Xlo / Ylo the lo parts), optional column index lists."""
+        K = X.m
+        ws = self.ws("tc_tn", _lib.load().pod_tc_tn_ws_bytes(p, q, K))
+        self._call(tag, 2, 2.0 * K * p * q, 4.0 * K * (p + q), "pod_gemm_tn_tf32x3", p, q, K,
+                   float(alpha), X.ptr, _ptr(Xlo) if Xlo is not None else None, X.ld,
+                   _ptr(xcols), Y.ptr, _ptr(Ylo) if Ylo is not None else None, Y.ld,
+                   _ptr(ycols), C, ldc, _ptr(ws), ws.numel(), self.stream)
+
+    def split_tf32(self, U, q, hi, lo):
+        """fp64 U (m x q ColMat) -> fp32 (hi, lo) TF32 split arrays (m x q, ld m)."""
+        self._call("split_tf32", 1, 0.0, 16.0 * U.m * q, "pod_split_tf32", U.ptr, U.m, q, U.ld,
+                   _ptr(hi), _ptr(lo), self.stream)
+
     def gram_eigh_any(self, G, g, r, sigma, T, info):
         """gram_eigh for any order g: the hand-written solver (pod_gram_eigh)
         up to pod_gram_eigh_max_g, beyond it cuSOLVER's symmetric eigensolver

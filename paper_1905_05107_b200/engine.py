@@ -346,8 +346,14 @@ class IsmaEngine(MergeWorkspace):
     pipeline)."""
 
     def __init__(self, ctx, A, *, k, r, c, criterion="modes", use_graphs=True, comm=None,
-                 row_offset=0, m_total=None, w=0):
+                 row_offset=0, m_total=None, w=0, precision="fp64"):
         self.A = A
+        # precision="mixed" (BASELINE config 4): the A-reading TN products of a
+        # float32-stored A -- the sampled Gram and finalize's A^T U -- run on
+        # the tcgen05 tensor cores in 3xTF32 (pod_gemm_tn_tf32x3); every other
+        # product stays fp64 DMMA
+        self.mixed = (precision == "mixed" and A.code == 1 and A.ld % 4 == 0
+                      and A.m % 4 == 0 and A.t.is_cuda)
         self.n = A.ncols
         self.c = int(c)
         gcap = min(self.c, A.ncols)
@@ -529,8 +535,12 @@ class IsmaEngine(MergeWorkspace):
         else:
             src, cols = A, self.idx[b]
         if rowsrc is None:
-            ctx.tn(g, g, 1.0, src, src, dptr(self.G[b]), g, xcols=cols, ycols=cols,
-                   tag="tn_gram_gather")                                     # baselines.py:43
+            if self.mixed:                                                   # tensor cores
+                ctx.tn_tf32x3(g, g, 1.0, src, src, dptr(self.G[b]), g, xcols=cols, ycols=cols,
+                              tag="tc_gram_gather")
+            else:
+                ctx.tn(g, g, 1.0, src, src, dptr(self.G[b]), g, xcols=cols, ycols=cols,
+                       tag="tn_gram_gather")                                 # baselines.py:43
             self.comm.allreduce_sum_(self.G[b])
             return
         self.uniw[b].copy_(self.h_uniw[b], non_blocking=True)
@@ -662,6 +672,14 @@ class IsmaEngine(MergeWorkspace):
         if self.host_A:                                                      # A^T U, streamed
             self._stream_columns(lambda Ach, j0, j1: ctx.tn(
                 j1 - j0, r, 1.0, Ach, U, dptr(Cm.t[0], j0), n, tag="tn_finalize_AtU"))
+        elif self.mixed:                                    # A^T U on the tensor cores
+            m = U.m
+            hi = torch.empty(m * r, dtype=torch.float32, device=dev)
+            lo = torch.empty(m * r, dtype=torch.float32, device=dev)
+            ctx.split_tf32(U, r, hi, lo)
+            ctx.tn_tf32x3(n, r, 1.0, self.A, ColMat(hi.view(r, m), m, r), Cm.ptr, n, Ylo=lo,
+                          tag="tc_finalize_AtU")
+            del hi, lo
         else:
             ctx.tn(n, r, 1.0, self.A, U, Cm.ptr, n, tag="tn_finalize_AtU")  # A^T U
         self.comm.allreduce_sum_(Cm.t)
@@ -849,7 +867,7 @@ ENGINE_CACHE_SIZE = 2  # per device: e.g. the two block widths of a column-block
 
 
 def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=0, m_total=None,
-               w=0):
+               w=0, precision="fp64"):
     """Reuse an engine (buffers + captured round graphs) of an earlier run
     when the matrix shape and configuration match (LRU, two per device).
     The graphs are kept per matrix buffer (they bake its pointer in) and read
@@ -858,7 +876,7 @@ def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=
     world = 1 if comm is None else comm.world
     key = (A.m, A.ncols, A.ld, A.code, A.t.is_cuda, int(k), int(r), int(c), criterion,
            bool(use_graphs),
-           ctx.device.index, world, int(row_offset), m_total, int(w))
+           ctx.device.index, world, int(row_offset), m_total, int(w), precision)
     lru = _ENGINE_CACHE.setdefault(ctx.device.index, [])
     for i, eng in enumerate(lru):
         if eng.key == key:
@@ -870,12 +888,14 @@ def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=
         lru.pop(0)
     try:
         eng = IsmaEngine(ctx, A, k=k, r=r, c=c, criterion=criterion, use_graphs=use_graphs,
-                         comm=comm, row_offset=row_offset, m_total=m_total, w=w)
+                         comm=comm, row_offset=row_offset, m_total=m_total, w=w,
+                         precision=precision)
     except torch.OutOfMemoryError:
         lru.clear()  # cached engines hold their buffers: drop them and retry once
         torch.cuda.empty_cache()
         eng = IsmaEngine(ctx, A, k=k, r=r, c=c, criterion=criterion, use_graphs=use_graphs,
-                         comm=comm, row_offset=row_offset, m_total=m_total, w=w)
+                         comm=comm, row_offset=row_offset, m_total=m_total, w=w,
+                         precision=precision)
     eng.key = key
     lru.append(eng)
     return eng

@@ -125,7 +125,7 @@ def _validate_shape(a):
 
 
 def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False,
-             use_graphs=True, comm=None, m_total=None, residency="auto"):
+             use_graphs=True, comm=None, m_total=None, residency="auto", precision="fp64"):
     """Run the full iteration (isma.py:225-303) on the GPU.
 
     ``a`` may be a numpy array (copied host->device), a CUDA torch tensor
@@ -139,6 +139,13 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
     finalize (and one per round for "ort") -- for matrices larger than HBM.
     Results are bit-identical to the device-resident run.  "auto" picks
     "host" when the matrix would not leave headroom on the device.
+
+    ``precision`` ("fp64" | "mixed"): "mixed" (BASELINE config 4) runs the
+    products that read a float32-stored A -- the sampled Gram D^T D and
+    finalize's A^T U -- on the tcgen05 tensor cores in 3xTF32 with fp32
+    accumulation (relative error ~2e-6 per product; north_star tolerance
+    sigma 1e-4, angles 1e-3); index sets are unchanged (the norms and draws
+    are exact).  Ignored for float64 storage.
 
     Row-sharded multi-GPU (parallel.py): pass ``comm=parallel.Comm()`` and
     this rank's row block ``a`` = A[r0:r1] with r0, r1 = shard_rows(m_total,
@@ -169,6 +176,8 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
     if rng is None:
         rng = np.random.default_rng(config.seed)
     ctx = get_ctx(device)
+    if precision not in ("fp64", "mixed"):
+        raise ParameterError("precision must be 'fp64' or 'mixed'")
     if residency not in ("auto", "device", "host"):
         raise ParameterError("residency must be 'auto', 'device' or 'host'")
     on_host = not isinstance(a, ColMat) and not (isinstance(a, torch.Tensor) and a.is_cuda)
@@ -188,20 +197,21 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
                                  "the residual pass)")
         with HostResident(a) as A:
             return _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m,
-                               return_device)
+                               return_device, precision)
     A = to_device_colmajor(a, ctx.device)
     return _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m,
-                       return_device)
+                       return_device, precision)
 
 
-def _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m, return_device):
+def _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m, return_device,
+                precision="fp64"):
     from .engine import get_engine
     from .matcore import TruncatedFactor
 
     eng = get_engine(ctx, A, k=k, r=config.r, c=config.column_budget(),
                      criterion=config.criterion, use_graphs=use_graphs, comm=comm,
                      row_offset=row_offset, m_total=m if comm.active else None,
-                     w=config.row_budget() if config.rows else 0)
+                     w=config.row_budget() if config.rows else 0, precision=precision)
     traces, v = eng.run(rng, strategy=config.strategy, tau=config.tau,
                         finalize=config.finalize, keep=keep, trace_cls=IterationTrace)
     u, s, vv = eng.result(keep, v)

@@ -12,6 +12,7 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -29,6 +30,7 @@ def main():
     ap.add_argument("--criterion", default="modes")
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--runs", type=int, default=2)
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "mixed"])
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     free, total = torch.cuda.mem_get_info(dev)
@@ -53,7 +55,7 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        f, tr = pod.isma_run(A, cfg)
+        f, tr = pod.isma_run(A, cfg, precision=args.precision)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
@@ -77,7 +79,13 @@ def main():
     ctx = get_ctx(dev)
     prof = KernelProfile()
     ctx.prof = prof
-    pod.isma_run(A, cfg, rng=NoRollback(7))
+    pod.isma_run(A, cfg, rng=NoRollback(7), precision=args.precision)
+    if args.precision == "mixed":  # the same run in fp64: the mixed path's errors
+        from parity_util import principal_angles_sin, sigma_relerr
+        fm = f
+        fd, _ = pod.isma_run(A, cfg)
+        out["mixed_vs_fp64"] = {"sigma_rel_err": sigma_relerr(fm.sigma, fd.sigma),
+                                "max_angle_rad": float(principal_angles_sin(fm.u, fd.u).max())}
     ctx.prof = None
     kern = prof.summary()
     print(json.dumps(out))
