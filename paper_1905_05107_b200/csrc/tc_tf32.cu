@@ -25,6 +25,7 @@
 // Y, K = 8 per instruction) and commits them to the stage's mbarrier; the
 // four warps read the accumulator back with tcgen05.ld (32 lanes each).
 #include <cuda.h>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -405,7 +406,12 @@ bool make_tmap(CUtensorMap* tm, const float* base, int64_t K, int64_t ncols, int
 // K split: enough CTAs for ~2 per SM, each at least 2048 rows
 int64_t tc_nsplit(int64_t P, int64_t Q, int64_t K) {
   const int64_t tiles = ((P + pod::tc::BM - 1) / pod::tc::BM) * ((Q + 63) / 64);
-  int64_t ns = std::max<int64_t>(1, (2 * 148 + tiles - 1) / tiles);
+  static int64_t target = -1;  // CTAs to aim for (POD_TC_CTAS overrides; A/B measurement)
+  if (target < 0) {
+    const char* e = getenv("POD_TC_CTAS");
+    target = e ? std::max(1, atoi(e)) : 2 * 148;
+  }
+  int64_t ns = std::max<int64_t>(1, (target + tiles - 1) / tiles);
   ns = std::min<int64_t>(ns, std::max<int64_t>(1, K / 2048));
   return std::min<int64_t>(ns, 65535);
 }

@@ -84,6 +84,12 @@ N_GATES = 16
 
 DINFO_BREAKDOWN = 8  # POD_DINFO_BREAKDOWN (include/podsketch_b200.h)
 
+#: precision="mixed": finalize's A^T U runs on the tcgen05 kernel; the sampled
+#: Gram too only with POD_TC_GRAM=1 -- measured at config 4 (r02): 2.0 s with
+#: it vs 1.46 s without (the pipelined Gram's long 192-KB-smem CTAs crowd the
+#: merge chain off the SMs), so the Gram stays on fp64 DMMA by default
+TC_GRAM = __import__("os").environ.get("POD_TC_GRAM", "0") == "1"
+
 #: debug/parity switch: when set, every run copies each round's drawn index
 #: set and counts (the draw slot's idx/cnt, still intact when the round's
 #: record is read) to the host -> IsmaEngine.draw_log, isma.LAST_DRAWS.
@@ -535,7 +541,7 @@ class IsmaEngine(MergeWorkspace):
         else:
             src, cols = A, self.idx[b]
         if rowsrc is None:
-            if self.mixed:                                                   # tensor cores
+            if self.mixed and TC_GRAM:                                       # tensor cores
                 ctx.tn_tf32x3(g, g, 1.0, src, src, dptr(self.G[b]), g, xcols=cols, ycols=cols,
                               tag="tc_gram_gather")
             else:

@@ -79,8 +79,9 @@ def test_tn_tf32x3_gathered_gram_and_split_fp64():
 
 
 def test_mixed_precision_isma_config4_proxy():
-    """precision="mixed" on a float32-stored config-4 proxy: the sampled Gram
-    and finalize's A^T U on the tcgen05 tensor cores (3xTF32).  Against the
+    """precision="mixed" on a float32-stored config-4 proxy: finalize's A^T U
+    on the tcgen05 tensor cores (3xTF32; the sampled Gram too with
+    POD_TC_GRAM=1).  Against the
     fp64 oracle on the exact upcast: identical draws in every round (the
     norms and the draw are exact), sigma within 1e-4 relative and principal
     angles below 1e-3 rad (north_star's mixed-precision tolerances; measured
