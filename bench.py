@@ -525,6 +525,63 @@ def north_star_block(args, pod, torch, dev, comm, ws, rank):
     return out
 
 
+def config4_block(args, pod, torch, dev):
+    """Config 4 (the config-2 generator at 1024^2 x 8192, STORED float32, 34 GB;
+    k = 64, r = 192, c = 256): precision="mixed" -- finalize's A^T U on the
+    tcgen05 tensor cores (3xTF32, TMEM accumulators) -- against the fp64
+    path on the same matrix: both times, the mixed path's sigma / angle errors
+    against the fp64 run, and the tcgen05 kernel's throughput."""
+    from paper_1905_05107_b200 import engine as eng_mod, workloads
+    from paper_1905_05107_b200.device import ColMat, get_ctx
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from parity_util import principal_angles_sin, sigma_relerr
+
+    eng_mod._ENGINE_CACHE.clear()
+    torch.cuda.empty_cache()
+    w = workloads.CFG4
+    at = workloads.config4_torch(7, w["side"], w["n"], device=dev)
+    m = w["side"] ** 2
+    A = ColMat(at, m)
+    cfg = pod.IsmaConfig(k=w["k"], r=w["r"], c=w["c"], tau=1 - w["tol"], strategy="l2n", seed=7)
+    stream = torch.cuda.current_stream(dev)
+    out = {"workload": "config4 snapshot field 1024x1024 -> m=1048576, n=8192, stored fp32 "
+                       "(34 GB); k=64, r=192, c=256, l2n, modes, tau=1-1e-8, finalize"}
+    res = {}
+    steps = max(1, min(args.steps, args.ns_steps))
+    for prec in ("mixed", "fp64"):
+        def run(prec=prec):
+            res[prec] = pod.isma_run(A, cfg, precision=prec)
+        for _ in range(args.warmup):
+            run()
+        t = _timed_runs(run, steps, stream, torch)
+        out[f"{prec}_s"] = statistics.mean(t)
+        out[f"{prec}_runs_s"] = t
+    fm, fd = res["mixed"][0], res["fp64"][0]
+    out["mixed_vs_fp64"] = {"sigma_rel_err": sigma_relerr(fm.sigma, fd.sigma),
+                            "max_angle_rad": float(principal_angles_sin(fm.u, fd.u).max()),
+                            "tolerance": "north_star mixed precision: sigma 1e-4, angles 1e-3"}
+    kern = _profile_run(pod, A, cfg, {"precision": "mixed"})
+    tc = kern.get("tc_finalize_AtU")
+    if tc:
+        peaks = _peaks()
+        pk = 0.5 * peaks.get("bf16_tflops", 2250.0)
+        ach = tc["flops"] / (tc["ms"] / 1e3) / tc["calls"] / 1e12
+        out["tc_kernel"] = {
+            "kernel": "tc_finalize_AtU (tcgen05.mma kind::tf32, 3 MMAs per product)",
+            "ms": tc["ms"] / tc["calls"], "algorithmic_tflops": ach,
+            "mma_tflops": 3 * ach, "peak_tf32_tflops": pk,
+            "frac_of_tf32_peak": 3 * ach / pk,
+            "peak_source": "0.5 x MEASURED_PEAKS.json bf16_tflops (dense TF32 = half of BF16)"}
+        fd64 = kern.get("tn_finalize_AtU")
+        if fd64:
+            out["tc_kernel"]["fp64_dmma_ms"] = fd64["ms"] / fd64["calls"]
+    del A, at
+    eng_mod._ENGINE_CACHE.clear()
+    torch.cuda.empty_cache()
+    return out
+
+
 def gpu_arm(args):
     import torch
 
@@ -617,6 +674,8 @@ def gpu_arm(args):
         del host, a_pinned
     if not args.no_north_star:
         line["north_star"] = north_star_block(args, pod, torch, dev, comm, ws, rank)
+    if ws == 1 and not args.no_config4:
+        line["config4_mixed"] = config4_block(args, pod, torch, dev)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_pair(a_host)
     if rank == 0:
@@ -636,6 +695,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-north-star", action="store_true")
+    ap.add_argument("--no-config4", action="store_true")
     ap.add_argument("--ns-steps", type=int, default=5, help="timed config-3 runs (<= --steps)")
     ap.add_argument("--ns-e2e-steps", type=int, default=2)
     args = ap.parse_args()

@@ -93,7 +93,7 @@ int pod_colnorms2_chain(int atype, const void* A, int64_t m, int64_t n, int64_t 
  * padding for the gathered GEMMs), cnt_out[0..g) int64,
  * info[0] = g, info[1] = |S| after the draw, info[2] = status
  * (0 ok, 1 empty S, 2 all weights zero -> DegenerateDistributionError).
- * Modes 0-3 reproduce numpy's arithmetic exactly (pod_draw_exact), so the
+ * Every mode reproduces numpy's arithmetic exactly (pod_draw_exact), so the
  * index sets equal the reference's by construction given equal weights. */
 size_t pod_draw_ws_bytes(int64_t n);
 int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n, const double* uniforms,
@@ -106,12 +106,13 @@ int pod_draw(int mode, const double* weights, uint8_t* live, int64_t n, const do
  * 62-65; blocks of <= 128 with 8 accumulators, split at n/2 rounded down to
  * a multiple of 8), np.cumsum as a sequential running sum (sampling.py:214),
  * the pin, searchsorted(side="right") and np.unique (sampling.py:215-221).
- * Same outputs as pod_draw; p_out is not supported. */
+ * Same outputs and modes as pod_draw (mode 4: the row draw, p_out = the
+ * drawn positions' normalised weights). */
 size_t pod_draw_exact_ws_bytes(int64_t n);
 int pod_draw_exact(int mode, const double* weights, uint8_t* live, int64_t n,
                    const double* uniforms, int64_t c, int32_t* idx_out, int64_t* cnt_out,
                    int64_t cap, void* ws, size_t ws_bytes, int64_t* info, double thr,
-                   void* stream);
+                   double* p_out, void* stream);
 
 /* Row sampling (ICRS) building blocks, isma.py:168-176:
  * out[i] = (sum_j X[i, cols[j]]^2) / div (div = *div_dev when non-null) --

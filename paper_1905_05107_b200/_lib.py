@@ -43,7 +43,7 @@ SIGNATURES = {
     "pod_draw_ws_bytes": (_sz, [_i64]),
     "pod_draw_exact_ws_bytes": (_sz, [_i64]),
     "pod_draw_exact": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp,
-                              _f64, _vp]),
+                              _f64, _vp, _vp]),
     "pod_draw": (_i32, [_i32, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _sz, _vp, _f64,
                         _vp, _vp]),
     "pod_rownorms2": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _f64, _vp, _vp, _vp]),

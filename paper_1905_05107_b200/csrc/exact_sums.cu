@@ -487,12 +487,16 @@ __global__ void __launch_bounds__(XD_THREADS) draw_exact_kernel(
     const double* __restrict__ uni, int64_t c, int32_t* __restrict__ idx_out,
     int64_t* __restrict__ cnt_out, int64_t cap, double* __restrict__ w,
     double* __restrict__ cum, int32_t* __restrict__ cidx, int32_t* __restrict__ counts,
-    PwTree tree, int64_t* __restrict__ info, double thr) {
+    PwTree tree, int64_t* __restrict__ info, double thr, double* __restrict__ p_out) {
   __shared__ int64_t shi[XD_THREADS];
   const int t = threadIdx.x;
   const int64_t chunk = (n + XD_THREADS - 1) / XD_THREADS;
   const int64_t j0 = min(n, t * chunk), j1 = min(n, j0 + chunk);
-  const bool all = (mode == 2);
+  // mode 4 (row draw, isma.py:168-173): from_weights over ALL positions
+  // (normalised like l2n), no retirement, p_out = the drawn positions' weights
+  const bool rows = (mode == 4);
+  if (rows) mode = 0;
+  const bool all = rows || (mode == 2);
   // compaction of the candidate set S (ascending, like setdiff1d's output)
   int64_t loc = 0;
   for (int64_t j = j0; j < j1; ++j) loc += all ? 1 : (live[j] != 0);
@@ -611,6 +615,7 @@ __global__ void __launch_bounds__(XD_THREADS) draw_exact_kernel(
       const int32_t jj = cidx[q];
       idx_out[pos] = jj;
       cnt_out[pos] = counts[q];
+      if (p_out) p_out[pos] = w[q];  // Distribution.weight_of (sampling.py:226)
       ++pos;
       if (!all) live[jj] = 0;
     }
@@ -734,15 +739,16 @@ extern "C" size_t pod_draw_exact_ws_bytes(int64_t n) {
 extern "C" int pod_draw_exact(int mode, const double* weights, uint8_t* live, int64_t n,
                               const double* uniforms, int64_t c, int32_t* idx_out,
                               int64_t* cnt_out, int64_t cap, void* ws, size_t ws_bytes,
-                              int64_t* info, double thr, void* stream) {
-  POD_REQUIRE(mode >= 0 && mode <= 3, "pod_draw_exact: bad mode %d", mode);
+                              int64_t* info, double thr, double* p_out, void* stream) {
+  POD_REQUIRE(mode >= 0 && mode <= 4, "pod_draw_exact: bad mode %d", mode);
+  POD_REQUIRE(p_out == nullptr || mode == 4, "pod_draw_exact: p_out needs mode 4");
   POD_REQUIRE(n > 0 && n < (int64_t)INT32_MAX, "pod_draw_exact: bad n");
   POD_REQUIRE(c >= 1, "sample count must be >= 1");
   POD_REQUIRE(ws_bytes >= pod_draw_exact_ws_bytes(n), "pod_draw_exact: workspace too small");
   POD_REQUIRE(cap >= imin64(c, n), "pod_draw_exact: output capacity %lld < min(c, n)",
               (long long)cap);
   POD_REQUIRE(mode == 1 || weights != nullptr, "pod_draw_exact: weights required");
-  POD_REQUIRE(mode == 2 || live != nullptr, "pod_draw_exact: live mask required");
+  POD_REQUIRE(mode == 2 || mode == 4 || live != nullptr, "pod_draw_exact: live mask required");
   const int64_t nodes = 2 * (n / 64 + 2);
   double* w = (double*)ws;
   double* cum = w + n;
@@ -755,7 +761,7 @@ extern "C" int pod_draw_exact(int mode, const double* weights, uint8_t* live, in
   tree.child = tree.len + nodes;
   draw_exact_kernel<<<1, XD_THREADS, 0, (cudaStream_t)stream>>>(
       mode, weights, live, n, uniforms, c, idx_out, cnt_out, cap, w, cum, cidx, counts, tree,
-      info, thr);
+      info, thr, p_out);
   POD_CHECK_LAUNCH("draw_exact");
   return POD_OK;
 }

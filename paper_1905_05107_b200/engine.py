@@ -729,8 +729,13 @@ class IsmaEngine(MergeWorkspace):
         if self.draw_log is None:
             return
         g = rec[REC_G]
-        self.draw_log.append((self.idx[b][:g].cpu().numpy().astype(np.int64),
-                              self.cnt[b][:g].cpu().numpy().astype(np.int64)))
+        entry = (self.idx[b][:g].cpu().numpy().astype(np.int64),
+                 self.cnt[b][:g].cpu().numpy().astype(np.int64))
+        if self.w:  # ICRS: the round's row draw too (isma.py:168-173)
+            h = rec[REC_H]
+            entry += (self.ridx[b][:h].cpu().numpy().astype(np.int64),
+                      self.rcnt[b][:h].cpu().numpy().astype(np.int64))
+        self.draw_log.append(entry)
 
     def _check_rows(self, rec, rng, state):
         """A zero row distribution raises (sampling.py:62-64) after the column

@@ -162,7 +162,7 @@ def test_draw_weights_cdf_and_indices_bitwise(n, mode):
         info = torch.zeros(4, dtype=torch.int64, device=dev)
         _lib.call("pod_draw_exact", mode, _ptr(raw_d), _ptr(live_d), n, _ptr(uni_d), c,
                   _ptr(idx), _ptr(cnt), cap, _ptr(ws), ws.numel(), _ptr(info), 0.0,
-                  ctx.stream)
+                  None, ctx.stream)
         g, rem, status = (int(x) for x in info[:3].cpu())
         assert status == 0
         s = w_ref.size
@@ -192,9 +192,15 @@ def test_engine_draws_equal_reference_draws(name, record_draws):
     ref = [(g["draw_idx"][off[i]:off[i + 1]], g["draw_cnt"][off[i]:off[i + 1]])
            for i in range(0, len(off) - 1, step)]
     assert len(log) == len(ref) == int(g["n_rounds"])
-    for rnd, ((gi, gc), (ri, rc)) in enumerate(zip(log, ref)):
-        assert np.array_equal(gi, ri), f"round {rnd}"
-        assert np.array_equal(gc, rc), f"round {rnd}"
+    for rnd, (entry, (ri, rc)) in enumerate(zip(log, ref)):
+        assert np.array_equal(entry[0], ri), f"round {rnd}"
+        assert np.array_equal(entry[1], rc), f"round {rnd}"
+    if w > 0:  # ICRS: the row draws too (row norms / leverage in einsum order)
+        rref = [(g["draw_idx"][off[i]:off[i + 1]], g["draw_cnt"][off[i]:off[i + 1]])
+                for i in range(1, len(off) - 1, 2)]
+        for rnd, (entry, (ri, rc)) in enumerate(zip(log, rref)):
+            assert np.array_equal(entry[2], ri), f"row draw, round {rnd}"
+            assert np.array_equal(entry[3], rc), f"row draw, round {rnd}"
 
 
 @pytest.mark.parametrize("strategy", ["l2n", "unf"])
@@ -216,5 +222,5 @@ def test_engine_draws_equal_oracle_draws_pipelined_and_not(strategy, record_draw
         pod.isma_run(a, cfg, rng=rng)
         log = pod.isma.LAST_DRAWS
         assert len(log) == len(o["trace"])
-        for (gi, gc), t in zip(log, o["trace"]):
-            assert np.array_equal(gi, t["unique"]) and np.array_equal(gc, t["counts"])
+        for entry, t in zip(log, o["trace"]):
+            assert np.array_equal(entry[0], t["unique"]) and np.array_equal(entry[1], t["counts"])

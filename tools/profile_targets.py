@@ -33,20 +33,29 @@ Wt = W.t[:r, :m]
 Gq = (Wt @ Wt.T).T.contiguous().reshape(-1)
 Rinv = torch.empty(r * r, dtype=torch.float64, device=dev)
 Rk = torch.empty(r * r, dtype=torch.float64, device=dev)
+live = torch.ones(n, dtype=torch.uint8, device=dev)
+uni = torch.rand(c := 100, dtype=torch.float64, device=dev)
+didx = torch.empty(g, dtype=torch.int32, device=dev)
+dcnt = torch.empty(g, dtype=torch.int64, device=dev)
 ops = [
-    ("colnorms", lambda: ctx.colnorms2(A, norms, flag)),
+    ("colnorms2", lambda: ctx.colnorms2(A, norms, flag)),
+    ("draw", lambda: (live.fill_(1), ctx.draw(0, norms, live, n, uni, c, didx, dcnt))),
     ("tn_gram_gather", lambda: ctx.tn(g, g, 1.0, A, A, dptr(C), g, xcols=idx, ycols=idx)),
-    ("tn_proj", lambda: ctx.tn(r, r, 1.0, S.cols(0, r), U2, dptr(C), r)),
-    ("tn_sym_cholqr", lambda: ctx.tn(r, r, 1.0, W, W, dptr(C), r)),
+    ("tn_merge_proj", lambda: ctx.tn(r, r, 1.0, S.cols(0, r), U2, dptr(C), r)),
+    ("tn_cholqr_gram", lambda: ctx.tn(r, r, 1.0, W, W, dptr(C), r)),
     ("nn_lift_gather", lambda: ctx.nn(g, r, 1.0, A, dptr(Tg), g, W, xcols=idx)),
-    ("nn_resid", lambda: ctx.nn(r, r, -1.0, S.cols(0, r), dptr(T), r, W, beta=1.0, Z=U2)),
-    ("nn_rotate", lambda: ctx.nn(2 * r, r, 1.0, S, dptr(T), 2 * r, W)),
+    ("nn_merge_resid", lambda: ctx.nn(r, r, -1.0, S.cols(0, r), dptr(T), r, W, beta=1.0, Z=U2)),
+    ("nn_merge_rotate", lambda: ctx.nn(2 * r, r, 1.0, S, dptr(T), 2 * r, W)),
     ("gram_eigh", lambda: ctx.gram_eigh(dptr(G), g, g, r, sig, dptr(Tl), g)),
     ("merge_core", lambda: ctx.merge_core(dptr(sig1), r, dptr(M), r, dptr(R), r, dptr(sig1), r, r, r,
                                           dptr(Tm), 2 * r, r, dptr(sn))),
     ("cholqr_factor", lambda: ctx.cholqr_factor(dptr(Gq), r, r, m, dptr(Rinv), r, dptr(Rk), r)),
 ]
+import sys as _s
+only = _s.argv[1:]  # optional subset of op names
 for name, fn in ops:
+    if only and name not in only:
+        continue
     fn(); fn()
 torch.cuda.synchronize()
 print("ok")
