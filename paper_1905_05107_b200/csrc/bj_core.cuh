@@ -198,6 +198,7 @@ struct PairRef {
 // visit threshold tol) leaves couplings of O(1e-12).  Measured at config 2
 // (r02): 1e-6 instead of 1e-8 saves ~0.6 sweeps per solve (merge 9.4 -> 8.8,
 // Gram 11.1 -> 10.5; 52.1 -> 51.3 ms per run) with the parity suite green.
+constexpr int ROT_DONE = 1, ROT_BIG = 2;
 #ifndef POD_COS_BIG2
 #define POD_COS_BIG2 1e-12
 #endif
