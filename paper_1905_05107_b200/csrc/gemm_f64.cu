@@ -593,13 +593,19 @@ constexpr int THREADS = 256;
 constexpr int BK = 16;
 constexpr int LDT = BK + 4;  // T chunk stored [j][k]
 
+#ifndef POD_NN80_WIDE
+#define POD_NN80_WIDE 0
+#endif
 template <int BN, typename TX = double>
 struct Cfg {
-  // BN = 80 (column groups of 80: q = 150 -> 160 instead of 192) runs 10 warps
-  static constexpr int NWARP = (BN == 80) ? 10 : 8;
+  // BN = 80 (column groups of 80: q = 150 -> 160 instead of 192) runs 10
+  // warps of 32 x 16 tiles, or (POD_NN80_WIDE) 8 warps of 32 x 40 tiles on
+  // 128-row blocks (20 DMMAs per 9 fragment loads instead of 8 per 6)
+  static constexpr bool W80 = (BN == 80) && POD_NN80_WIDE;
+  static constexpr int NWARP = (BN == 80 && !W80) ? 10 : 8;
   static constexpr int NTHREADS = NWARP * 32;
-  static constexpr int STAGES = (BN == 128) ? 3 : 4;
-  static constexpr int BM = (BN == 64) ? 128 : 64;  // rows per block (T reuse)
+  static constexpr int STAGES = (BN == 128 || W80) ? 3 : 4;
+  static constexpr int BM = (BN == 64 || W80) ? 128 : 64;  // rows per block (T reuse)
   // X chunk stored [k][row] in X's own type (fp32 storage converted exactly
   // at the fragment loads); padding keeps the fragment loads conflict-free
   static constexpr int LDX = BM + (sizeof(TX) == 8 ? 4 : 8);

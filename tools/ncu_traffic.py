@@ -20,7 +20,7 @@ data = rows[2:]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 print("# ncu --set full --clock-control none, tools/profile_targets.py on one B200 (round 2):")
 print("# DRAM traffic per call of each hot op (its second, warm call), config-2 shapes")
-print("op | dram_rd | unit | dram_wr | unit | dur_us | kernels")
+print(f"op | dram_rd | unit | dram_wr | unit | dur [{units[it]}] | kernels")
 pos = 0
 for name, nk in OPS:
     calls = []
@@ -32,6 +32,4 @@ for name, nk in OPS:
         dt = sum(float(r[it]) for r in ks)
         calls.append((rd, wr, dt, "+".join(r[ki].split("(")[0][-40:] for r in ks)))
     rd, wr, dt, kn = calls[-1]
-    tu = units[it]
-    dus = dt / 1e3 if tu == "nsecond" else (dt * 1e3 if tu == "msecond" else dt)
-    print(f"{name} | {rd / 1e6:.3f} | Mbyte | {wr / 1e6:.3f} | Mbyte | {dus:.1f} | {kn}")
+    print(f"{name} | {rd / 1e6:.3f} | Mbyte | {wr / 1e6:.3f} | Mbyte | {dt:.4g} | {kn}")
