@@ -335,6 +335,191 @@ __global__ void __launch_bounds__(THREADS, 1) tn_tf32x3_kernel(
                  "n"(TCOLS));
 }
 
+// Warp-specialized variant for the all-TMA case (X raw fp32, Y pre-split:
+// finalize's A^T U).  The phased kernel above serialises load -> split ->
+// MMA -> drain inside one loop and kept the tensor pipe 21 % busy; here
+// the roles run concurrently on mbarriers:
+//   warp 0 lane 0   TMA producer: waits empty[s], loads X / Yh / Yl -> full[s]
+//   warp 1 lane 0   MMA issuer:   waits conv[s] (and accfree[b] at a group
+//                                 start), 12 MMAs, commits empty[s] (and
+//                                 accbar[b] at a group end)
+//   warps 4..7      convert + drain: wait full[s], split X into hi / lo in
+//                                 place, fence to the async proxy, arrive
+//                                 conv[s]; at each group start drain the
+//                                 previous group's TMEM buffer into the fp32
+//                                 master accumulator and arrive accfree[b]
+// (warps 4..7 own TMEM lane quarters 0..3 = rows 0..127 of the tile)
+constexpr int WS_THREADS = 256;
+#ifndef POD_TC_WS_GROUP
+#define POD_TC_WS_GROUP 1
+#endif
+
+template <int NQ>
+__global__ void __launch_bounds__(WS_THREADS, 1) tn_tf32x3_ws_kernel(
+    int P, int64_t K, int64_t kchunk, float* __restrict__ part, int64_t ldp, int Q,
+    const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmyh,
+    const __grid_constant__ CUtensorMap tmyl) {
+  constexpr int GROUP = POD_TC_WS_GROUP;
+  constexpr int ST = stages_for(NQ);
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int xbytes = BM * 128, ybytes = NQ * 128;
+  constexpr int sbytes = 2 * xbytes + 2 * ybytes;
+  constexpr int TCOLS = (2 * NQ <= 32) ? 32 : (2 * NQ <= 64 ? 64 : (2 * NQ <= 128 ? 128 : 256));
+  __shared__ uint64_t full[ST], conv[ST], empty[ST], accbar[2], accfree[2];
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int p0 = blockIdx.x * BM, q0 = blockIdx.y * NQ;
+  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
+  const int64_t kend = (K < kbeg + kchunk) ? K : kbeg + kchunk;
+  const int nk = (int)((kend - kbeg + BK - 1) / BK);
+  const int ngroups = (nk + GROUP - 1) / GROUP;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     saddr(&tmem_base_s)),
+                 "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init1(&full[s]);
+      mbar_init1(&empty[s]);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(saddr(&conv[s])));
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init1(&accbar[b]);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(saddr(&accfree[b])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base_s;
+  auto xh = [&](int s) { return smem + (size_t)s * sbytes; };
+  auto xl = [&](int s) { return smem + (size_t)s * sbytes + xbytes; };
+  auto yh = [&](int s) { return smem + (size_t)s * sbytes + 2 * xbytes; };
+  auto yl = [&](int s) { return smem + (size_t)s * sbytes + 2 * xbytes + ybytes; };
+  auto tma2d = [&](const CUtensorMap* tm, unsigned char* dst, int64_t k, int row, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+        "{%2, %3}], [%4];" ::"r"(saddr(dst)), "l"(reinterpret_cast<uint64_t>(tm)), "r"((int)k),
+        "r"(row), "r"(saddr(bar))
+        : "memory");
+  };
+
+  if (warp == 0) {  // ------------------------------------------ TMA producer
+    if (lane == 0) {
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % ST;
+        if (kt >= ST) mbar_wait(&empty[s], (uint32_t)((kt / ST - 1) & 1));
+        asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         saddr(&full[s])), "r"((uint32_t)(xbytes + 2 * ybytes)) : "memory");
+        const int64_t k0 = kbeg + (int64_t)kt * BK;
+        tma2d(&tmx, xh(s), k0, p0, &full[s]);
+        tma2d(&tmyh, yh(s), k0, q0, &full[s]);
+        tma2d(&tmyl, yl(s), k0, q0, &full[s]);
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_tf32(NQ);
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % ST, grp = kt / GROUP, buf = grp & 1;
+        if (kt % GROUP == 0 && grp >= 2) mbar_wait(&accfree[buf], (uint32_t)((grp / 2 - 1) & 1));
+        mbar_wait(&conv[s], (uint32_t)((kt / ST) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t ah = saddr(xh(s)), al = saddr(xl(s)), bh = saddr(yh(s)), bl = saddr(yl(s));
+        const uint32_t td = tmem + (uint32_t)(buf * NQ);
+#pragma unroll
+        for (int ks = 0; ks < BK / 8; ++ks) {
+          const uint32_t off = ks * 32;
+          const uint32_t acc0 = (kt % GROUP > 0 || ks > 0) ? 1u : 0u;
+          mma_tf32(td, sw128_desc(ah + off), sw128_desc(bh + off), idesc, acc0);
+          mma_tf32(td, sw128_desc(al + off), sw128_desc(bh + off), idesc, 1u);
+          mma_tf32(td, sw128_desc(ah + off), sw128_desc(bl + off), idesc, 1u);
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                saddr(&empty[s]))
+            : "memory");
+        if (kt % GROUP == GROUP - 1 || kt == nk - 1)
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                  saddr(&accbar[buf]))
+              : "memory");
+      }
+    }
+  } else if (warp >= 4) {  // --------------------------- convert + drain
+    const int t = threadIdx.x - 128, wq = warp - 4;  // TMEM lane quarter
+    float master[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) master[j] = 0.0f;
+    auto drain = [&](int b, uint32_t parity) {
+      mbar_wait(&accbar[b], parity);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c0 = 0; c0 < NQ; c0 += 16) {
+        uint32_t v[16];
+        const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(b * NQ + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+            "%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) master[c0 + j] += __uint_as_float(v[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(&accfree[b])) : "memory");
+    };
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % ST;
+      mbar_wait(&full[s], (uint32_t)((kt / ST) & 1));
+      float4* h = reinterpret_cast<float4*>(xh(s));
+      float4* l = reinterpret_cast<float4*>(xl(s));
+#pragma unroll
+      for (int e = t; e < BM * 8; e += 128) {
+        const float4 v = h[e];
+        float4 a, b;
+        a.x = tf32_hi(v.x); b.x = v.x - a.x;
+        a.y = tf32_hi(v.y); b.y = v.y - a.y;
+        a.z = tf32_hi(v.z); b.z = v.z - a.z;
+        a.w = tf32_hi(v.w); b.w = v.w - a.w;
+        h[e] = a;
+        l[e] = b;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(&conv[s])) : "memory");
+      const int grp = kt / GROUP;
+      if (kt % GROUP == 0 && grp >= 1) {  // the previous group is complete soon
+        const int pg = grp - 1;
+        drain(pg & 1, (uint32_t)((pg / 2) & 1));
+      }
+    }
+    if (ngroups >= 1) {
+      const int lg = ngroups - 1;
+      drain(lg & 1, (uint32_t)((lg / 2) & 1));
+    }
+    const int row = p0 + t;
+    if (row < P) {
+      float* out = part + (size_t)blockIdx.z * ldp * (size_t)Q;
+#pragma unroll
+      for (int j = 0; j < NQ; ++j)
+        if (q0 + j < Q) out[row + (size_t)(q0 + j) * ldp] = master[j];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(TCOLS));
+}
+
 // C (P x Q, ldc) = alpha * sum over splits of part[s] (fixed order, fp64)
 __global__ void reduce_parts_kernel(const float* __restrict__ part, int nsplit, int P, int Q,
                                     int64_t ldp, double alpha, double* __restrict__ C,
@@ -403,6 +588,40 @@ bool make_tmap(CUtensorMap* tm, const float* base, int64_t K, int64_t ncols, int
          CUDA_SUCCESS;
 }
 
+// POD_TC_WS=0 forces the phased kernel (A/B measurement)
+bool ws_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_TC_WS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int NQ>
+cudaError_t launch_ws_t(dim3 grid, size_t smem, int64_t P, int64_t K, int64_t kchunk, float* part,
+                        int Q, const CUtensorMap& tx, const CUtensorMap& tyh,
+                        const CUtensorMap& tyl, cudaStream_t s) {
+  static bool done = false;
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(pod::tc::tn_tf32x3_ws_kernel<NQ>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  pod::tc::tn_tf32x3_ws_kernel<NQ><<<grid, pod::tc::WS_THREADS, smem, s>>>(
+      (int)P, K, kchunk, part, P, Q, tx, tyh, tyl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ws(int nq, dim3 grid, size_t smem, int64_t P, int64_t K, int64_t kchunk,
+                      float* part, int Q, const CUtensorMap& tx, const CUtensorMap& tyh,
+                      const CUtensorMap& tyl, cudaStream_t s) {
+  if (nq == 64) return launch_ws_t<64>(grid, smem, P, K, kchunk, part, Q, tx, tyh, tyl, s);
+  if (nq == 96) return launch_ws_t<96>(grid, smem, P, K, kchunk, part, Q, tx, tyh, tyl, s);
+  return launch_ws_t<128>(grid, smem, P, K, kchunk, part, Q, tx, tyh, tyl, s);
+}
+
 // K split: enough CTAs for ~2 per SM, each at least 2048 rows
 int64_t tc_nsplit(int64_t P, int64_t Q, int64_t K) {
   const int64_t tiles = ((P + pod::tc::BM - 1) / pod::tc::BM) * ((Q + 63) / 64);
@@ -459,6 +678,11 @@ extern "C" int pod_gemm_tn_tf32x3(int64_t P, int64_t Q, int64_t K, double alpha,
                    (!Xlo || make_tmap(&tmxl, Xlo, K, P, ldx, BM));
     const int ty = !ycols && make_tmap(&tmyh, Y, K, Q, ldy, nq) &&
                    (!Ylo || make_tmap(&tmyl, Ylo, K, Q, ldy, nq));
+    if (tx && ty && !Xlo && Ylo && ws_enabled()) {  // all-TMA: the warp-specialized kernel
+      cudaError_t e = launch_ws(nq, grid, smem, P, K, kchunk, part, (int)Q, tmxh, tmyh, tmyl, s);
+      if (e != cudaSuccess) return cuda_status(e, "tn_tf32x3 ws");
+      return POD_OK;
+    }
     kern<<<grid, THREADS, smem, s>>>(xo, yo, K, kchunk, part, P, (int)Q, tmxh, tmxl, tmyh, tmyl,
                                      tx, ty);
     POD_CHECK_LAUNCH("tn_tf32x3");
