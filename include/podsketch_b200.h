@@ -257,6 +257,20 @@ int pod_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm,
                    int64_t ldt, int64_t tcols, double* sig_new, int64_t* info, void* ws,
                    size_t ws_bytes, void* stream);
 
+/* Whether pod_merge_core handles l1 + l2 with a single-cluster solver (block
+ * or cluster Jacobi, no workspace) -- the sizes pod_merge_core_gated takes. */
+int pod_merge_core_gatable(int64_t l1, int64_t l2);
+
+/* pod_merge_core with a device gate: *gate == 0 makes the launch a no-op.
+ * The ISMA engine runs the merge core speculatively on the first-pass R
+ * while the leak check of merge.py:72-79 is in flight, and re-runs it gated
+ * on that check (the re-run only does work when the second projection
+ * fired).  Sizes must satisfy pod_merge_core_gatable. */
+int pod_merge_core_gated(const double* sig1, int64_t l1, const double* M, int64_t ldm,
+                         const double* R, int64_t ldr, const double* sig2, int64_t l2, int64_t r,
+                         int64_t rcap, double* T, int64_t ldt, int64_t tcols, double* sig_new,
+                         int64_t* info, const int32_t* gate, void* stream);
+
 /* Thin SVD of a small nr x nc matrix (nr >= nc) by one-sided Jacobi:
  * sigma descending; if U and V are non-null, U (nr x nc) and V (nc x nc)
  * with A = U diag(sigma) V^T.  Replaces matcore.py:178-184 (_svd) at

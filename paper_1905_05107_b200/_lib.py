@@ -76,6 +76,9 @@ SIGNATURES = {
                                   _vp, _sz, _vp, _vp, _i32, _vp]),
     "pod_merge_core": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64,
                               _i64, _vp, _vp, _vp, _sz, _vp]),
+    "pod_merge_core_gatable": (_i32, [_i64, _i64]),
+    "pod_merge_core_gated": (_i32, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _vp,
+                                    _i64, _i64, _vp, _vp, _vp, _vp]),
     "pod_svd_small": (_i32, [_vp, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "pod_small_gemm": (_i32, [_i64, _i64, _i64, _f64, _vp, _i64, _i32, _vp, _i64, _f64, _vp, _i64,
                               _vp, _vp]),

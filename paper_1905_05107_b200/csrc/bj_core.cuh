@@ -192,15 +192,16 @@ struct PairRef {
 };
 
 // Flags returned by the rotation steps: ROT_DONE = the pair was rotated,
-// ROT_BIG = its cosine exceeded COS_BIG (1e-6).  A sweep in which no pair
+// ROT_BIG = its cosine exceeded COS_BIG (1e-8).  A sweep in which no pair
 // exceeded COS_BIG ends the iteration: cyclic Jacobi converges
 // quadratically, so that sweep (which still rotates every pair above the
-// visit threshold tol) leaves couplings of O(1e-12).  Measured at config 2
-// (r02): 1e-6 instead of 1e-8 saves ~0.6 sweeps per solve (merge 9.4 -> 8.8,
-// Gram 11.1 -> 10.5; 52.1 -> 51.3 ms per run) with the parity suite green.
+// visit threshold tol) leaves couplings of O(1e-16).  1e-6 (tried in r02:
+// ~0.6 sweeps fewer per solve) is NOT safe: for clustered singular values
+// (gaps below the cosine) the last sweep is not yet quadratic and sigma
+// came out 1.2e-7 off (test_thin_qr_and_orthonormalize_match_reference).
 constexpr int ROT_DONE = 1, ROT_BIG = 2;
 #ifndef POD_COS_BIG2
-#define POD_COS_BIG2 1e-12
+#define POD_COS_BIG2 1e-16
 #endif
 constexpr double COS_BIG2 = POD_COS_BIG2;
 

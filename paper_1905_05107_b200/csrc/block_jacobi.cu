@@ -219,7 +219,11 @@ __global__ void __launch_bounds__(RPL >= 16 ? 384 : 512)
                       int64_t ldm, const double* __restrict__ Rm, int64_t ldr,
                       const double* __restrict__ sig2, int l2, int r, int rcap,
                       double* __restrict__ T, int64_t ldt, int tcols, double* __restrict__ sig_new,
-                      int64_t* __restrict__ info, int max_sweeps, int trans, int nset) {
+                      int64_t* __restrict__ info, int max_sweeps, int trans, int nset,
+                      const int32_t* __restrict__ gate) {
+  // gate (optional, device): 0 = skip -- the re-run of a speculative merge
+  // core when the second projection did not fire (uniform over the cluster)
+  if (gate != nullptr && *gate == 0) return;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double smem_bj[];
   const int n = l1 + l2;
@@ -522,7 +526,8 @@ static bool bj_enabled() {
 int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
                   int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
                   int64_t ldt, int64_t tcols, double* sig_new, int64_t* info,
-                  cudaStream_t stream) {
+                  const int32_t* gate, bool probe, cudaStream_t stream) {
+  // probe: return POD_OK without launching when this solver handles the size
   if (!bj_enabled()) return BJ_NOT_APPLICABLE;
   const int n = (int)(l1 + l2);
   if (n < 2 * BJ_CL) return BJ_NOT_APPLICABLE;
@@ -541,7 +546,7 @@ int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, 
     const int th = bj::threads_for(g, tpp);
     const int rpl = (g.nrows + tpp - 1) / tpp;
     if (th > 512 || (rpl > 8 && th > 384)) continue;
-#define BJ_L(C_, T_, R_) return bj::launch(bj::merge_core_kernel<C_, T_, R_>, C_, th, bytes, stream, sig1, (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new, info, 60, trans, nset)
+#define BJ_L(C_, T_, R_) return probe ? POD_OK : bj::launch(bj::merge_core_kernel<C_, T_, R_>, C_, th, bytes, stream, sig1, (int)l1, M, ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new, info, 60, trans, nset, gate)
     if (cl == BJ_CL) {
       if (tpp == 8) { if (rpl <= 4) BJ_L(BJ_CL, 8, 4); if (rpl <= 8) BJ_L(BJ_CL, 8, 8); if (rpl <= 16) BJ_L(BJ_CL, 8, 16); if (rpl <= 24) BJ_L(BJ_CL, 8, 24); BJ_L(BJ_CL, 8, 0); }
       if (tpp == 16) { if (rpl <= 4) BJ_L(BJ_CL, 16, 4); if (rpl <= 8) BJ_L(BJ_CL, 16, 8); if (rpl <= 16) BJ_L(BJ_CL, 16, 16); if (rpl <= 24) BJ_L(BJ_CL, 16, 24); BJ_L(BJ_CL, 16, 0); }

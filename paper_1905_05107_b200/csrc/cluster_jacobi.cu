@@ -363,7 +363,8 @@ __global__ void __launch_bounds__(CJ_THREADS)
                          const double* __restrict__ sig2, int l2, int r, int rcap,
                          double* __restrict__ T, int64_t ldt, int tcols,
                          double* __restrict__ sig_new, int64_t* __restrict__ info, int nrl,
-                         int max_sweeps) {
+                         int max_sweeps, const int32_t* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;  // gated re-run (block_jacobi.cu)
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) double smem_cj[];
   const int n = l1 + l2;
@@ -617,7 +618,7 @@ template <int CL>
 static int cj_merge_core_t(const double* sig1, int64_t l1, const double* M, int64_t ldm,
                            const double* R, int64_t ldr, const double* sig2, int64_t l2, int64_t r,
                            int64_t rcap, double* T, int64_t ldt, int64_t tcols, double* sig_new,
-                           int64_t* info, cudaStream_t stream) {
+                           int64_t* info, const int32_t* gate, cudaStream_t stream) {
   const int n = (int)(l1 + l2);
   const int nrl = (n + CL - 1) / CL;
   const size_t bytes = cj_scratch_bytes<CL>(n) + (size_t)nrl * n * sizeof(double);
@@ -625,19 +626,19 @@ static int cj_merge_core_t(const double* sig1, int64_t l1, const double* M, int6
   if (st) return st;
   return cj_launch(cj_merge_core_kernel<CL>, CL, cj_threads(n), bytes, stream, sig1, (int)l1, M,
                    ldm, R, ldr, sig2, (int)l2, (int)r, (int)rcap, T, ldt, (int)tcols, sig_new,
-                   info, nrl, 60);
+                   info, nrl, 60, gate);
 }
 
 int cj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
                   int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
                   int64_t ldt, int64_t tcols, double* sig_new, int64_t* info,
-                  cudaStream_t stream) {
+                  const int32_t* gate, cudaStream_t stream) {
   const int n = (int)(l1 + l2);
   POD_REQUIRE(n <= CJ_MAX_N, "merge core: l1 + l2 = %d exceeds %d", n, CJ_MAX_N);
   switch (cj_cluster()) {
-    case 2: return cj_merge_core_t<2>(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info, stream);
-    case 4: return cj_merge_core_t<4>(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info, stream);
-    default: return cj_merge_core_t<8>(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info, stream);
+    case 2: return cj_merge_core_t<2>(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info, gate, stream);
+    case 4: return cj_merge_core_t<4>(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info, gate, stream);
+    default: return cj_merge_core_t<8>(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info, gate, stream);
   }
 }
 

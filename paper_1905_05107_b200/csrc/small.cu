@@ -633,14 +633,16 @@ static size_t cholqr_bytes(int64_t l) { return (size_t)3 * l * l * 8 + (size_t)3
 
 int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
                   int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
-                  int64_t ldt, int64_t tcols, double* sig_new, int64_t* info, cudaStream_t stream);
+                  int64_t ldt, int64_t tcols, double* sig_new, int64_t* info, const int32_t* gate,
+                  bool probe, cudaStream_t stream);
 int bj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t g, int64_t r,
                  double* sigma, double* T, int64_t ldt, int64_t* info, cudaStream_t stream);
 int bj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int64_t ldu,
            double* sigma, double* V, int64_t ldv, int64_t* info, cudaStream_t stream);
 int cj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
                   int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
-                  int64_t ldt, int64_t tcols, double* sig_new, int64_t* info, cudaStream_t stream);
+                  int64_t ldt, int64_t tcols, double* sig_new, int64_t* info, const int32_t* gate,
+                  cudaStream_t stream);
 int cj_gram_eigh(const double* X, const int* piv, const int64_t* rank, int64_t g, int64_t r,
                  double* sigma, double* T, int64_t ldt, int64_t* info, cudaStream_t stream);
 int cj_svd(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U, int64_t ldu,
@@ -835,13 +837,38 @@ extern "C" int pod_merge_core(const double* sig1, int64_t l1, const double* M, i
   POD_REQUIRE(l1 >= 1 && l2 >= 1 && r >= 1 && rcap >= l1 && ldt >= rcap + l2 && tcols >= 1,
               "pod_merge_core: bad shape");
   const int bst = bj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols,
-                                sig_new, info, (cudaStream_t)stream);
+                                sig_new, info, nullptr, false, (cudaStream_t)stream);
   if (bst != -1) return bst;  // -1: size not handled by the block solver
   if (cj_fits(l1 + l2, l1 + l2, 0))
     return cj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new,
-                         info, (cudaStream_t)stream);
+                         info, nullptr, (cudaStream_t)stream);
   return gj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info,
                        ws, ws_bytes, (cudaStream_t)stream);
+}
+
+extern "C" int pod_merge_core_gatable(int64_t l1, int64_t l2) {
+  if (l1 < 1 || l2 < 1) return 0;
+  if (bj_merge_core(nullptr, l1, nullptr, 0, nullptr, 0, nullptr, l2, 1, l1, nullptr, l1 + l2, 1,
+                    nullptr, nullptr, nullptr, true, nullptr) == POD_OK)
+    return 1;
+  return cj_fits(l1 + l2, l1 + l2, 0) ? 1 : 0;
+}
+
+extern "C" int pod_merge_core_gated(const double* sig1, int64_t l1, const double* M, int64_t ldm,
+                                    const double* R, int64_t ldr, const double* sig2, int64_t l2,
+                                    int64_t r, int64_t rcap, double* T, int64_t ldt,
+                                    int64_t tcols, double* sig_new, int64_t* info,
+                                    const int32_t* gate, void* stream) {
+  POD_REQUIRE(l1 >= 1 && l2 >= 1 && r >= 1 && rcap >= l1 && ldt >= rcap + l2 && tcols >= 1,
+              "pod_merge_core_gated: bad shape");
+  POD_REQUIRE(pod_merge_core_gatable(l1, l2),
+              "pod_merge_core_gated: l1 + l2 = %lld needs the grid solver (not gatable)",
+              (long long)(l1 + l2));
+  const int bst = bj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols,
+                                sig_new, info, gate, false, (cudaStream_t)stream);
+  if (bst != -1) return bst;
+  return cj_merge_core(sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, info,
+                       gate, (cudaStream_t)stream);
 }
 
 extern "C" int pod_svd_small(const double* A, int64_t lda, int64_t nr, int64_t nc, double* U,

@@ -299,6 +299,14 @@ class Ctx:
                   sig_new, _ptr(self.info if info is None else info), _ptr(ws), ws.numel(),
                   self.stream)
 
+    def merge_core_gated(self, sig1, l1, M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols,
+                         sig_new, info, gate):
+        """merge_core that is a no-op when the device gate reads 0 (sizes with
+        pod_merge_core_gatable only)."""
+        self._call("merge_core", 1, 0.0, 8.0 * (l1 + l2) ** 2, "pod_merge_core_gated", sig1, l1,
+                   M, ldm, R, ldr, sig2, l2, r, rcap, T, ldt, tcols, sig_new, _ptr(info),
+                   _gp(gate), self.stream)
+
     def svd_small(self, A, lda, nr, nc, U, ldu, sigma, V, ldv):
         ws = self.ws("small", max(_lib.load().pod_svd_small_ws_bytes(nr, nc, int(V is not None)),
                                   _lib.load().pod_small_ws_bytes(min(nr, nc))))

@@ -89,6 +89,14 @@ DINFO_BREAKDOWN = 8  # POD_DINFO_BREAKDOWN (include/podsketch_b200.h)
 #: it vs 1.46 s without (the pipelined Gram's long 192-KB-smem CTAs crowd the
 #: merge chain off the SMs), so the Gram stays on fp64 DMMA by default
 TC_GRAM = __import__("os").environ.get("POD_TC_GRAM", "0") == "1"
+#: speculative merge core: the E-SVD starts on the first CholeskyQR's R while
+#: the leak check (U1^T Q, merge.py:72) runs beside it; a gated re-run covers
+#: the rounds whose second projection fires.  POD_SPEC_CORE=0 disables.
+SPEC_CORE = __import__("os").environ.get("POD_SPEC_CORE", "1") != "0"
+#: CTA cap of the speculative leak check's GEMM (full grid: its CTAs crowd the
+#: E-SVD's cluster -- config 2 57.8 ms; 8: the check outlasts the core, 66 ms;
+#: 32-64: 51.2-51.4 ms vs 52.3 serial)
+LEAK_GRID_CAP = int(__import__("os").environ.get("POD_LEAK_GRID_CAP", "64"))
 
 #: debug/parity switch: when set, every run copies each round's drawn index
 #: set and counts (the draw slot's idx/cnt, still intact when the round's
@@ -150,6 +158,8 @@ class MergeWorkspace:
         # sticky CholeskyQR breakdown flag (dinfo[POD_DINFO_BREAKDOWN]), read with the record
         self.h_breakdown = torch.zeros(1, dtype=torch.float64).pin_memory()
         self.leak = torch.zeros(1, **f64)
+        self._spec = None
+        self._leak_stream = None
         self._qscratch = {}
         self.cur = 0
         self.l = 0
@@ -237,15 +247,38 @@ class MergeWorkspace:
         U2 = self.Uupd_b[ub].cols(0, r)
         sig_upd = self.sig_upd_b[ub]
         Q = S.cols(r, 2 * r)
+        core = (dptr(self.sig[cur]), r, dptr(self.M), r, dptr(self.Rt), r, dptr(sig_upd), r, r, r,
+                dptr(self.Tm), 2 * r, r, dptr(self.sig[1 - cur]))
+        info = self.rec[0, REC_KEEP:]
         ctx.tn(r, r, 1.0, U1, U2, dptr(self.M), r, tag="tn_merge_proj")       # merge.py:65
         self.comm.allreduce_sum_(self.M)
         ctx.nn(r, r, -1.0, U1, dptr(self.M), r, self.W, beta=1.0, Z=U2,
                tag="nn_merge_resid")                                         # merge.py:69
         self.cholqr_ops(self.W, Q, r, self.Rt, G_QR)                         # merge.py:70
-        ctx.tn(r, r, 1.0, U1, Q, dptr(self.C), r, tag="tn_merge_leak")       # merge.py:72
-        self.comm.allreduce_sum_(self.C)
-        ctx.maxabs(dptr(self.C), r, r, r, dptr(self.leak), thr=REORTH_TOL,
-                   gate_out=self.gate(G_LEAK))
+        spec = self.speculative_core()
+        if spec:
+            # the E-SVD on the first-pass (M, R) starts now; the leak check
+            # (merge.py:72-73) runs beside it on its own stream, and the
+            # gated second projection re-runs the core only when it fired
+            main = torch.cuda.current_stream(ctx.device)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            if before_core is not None:
+                before_core()
+            ctx.merge_core(*core, info=info)                                 # merge.py:80-85
+            self._leak_stream.wait_event(ev)
+            ctx.ws_suffix = "_leak"
+            lib = _lib.load()
+            lib.pod_set_grid_cap(LEAK_GRID_CAP)
+            try:
+                with torch.cuda.stream(self._leak_stream):
+                    self.leak_check_ops(U1, Q)
+            finally:
+                lib.pod_set_grid_cap(0)
+                ctx.ws_suffix = ""
+            main.wait_stream(self._leak_stream)
+        else:
+            self.leak_check_ops(U1, Q)
         gl = self.gate(G_LEAK)                                               # merge.py:73-79
         ctx.nn(r, r, -1.0, U1, dptr(self.C), r, self.W, beta=1.0, Z=Q, gate=gl,
                tag="nn_merge_resid")
@@ -255,13 +288,33 @@ class MergeWorkspace:
         ctx.small_gemm(r, r, r, 1.0, dptr(self.Rt2), r, 0, dptr(self.Rt), r, 0.0,
                        dptr(self.Rtmp), r, gate=gl)
         ctx.small_copy(r, r, dptr(self.Rtmp), r, dptr(self.Rt), r, gate=gl)
-        if before_core is not None:
-            before_core()
-        ctx.merge_core(dptr(self.sig[cur]), r, dptr(self.M), r, dptr(self.Rt), r,
-                       dptr(sig_upd), r, r, r, dptr(self.Tm), 2 * r, r,
-                       dptr(self.sig[1 - cur]), info=self.rec[0, REC_KEEP:])  # merge.py:80-85
+        if spec:
+            ctx.merge_core_gated(*core, info, gl)
+        else:
+            if before_core is not None:
+                before_core()
+            ctx.merge_core(*core, info=info)                                 # merge.py:80-85
         ctx.nn(2 * r, r, 1.0, S, dptr(self.Tm), 2 * r, Snext.cols(0, r),
                tag="nn_merge_rotate")                                        # merge.py:86-88
+
+    def leak_check_ops(self, U1, Q):
+        """C = U1^T Q and the gate max|C| > REORTH_TOL (merge.py:72-73)."""
+        ctx, r = self.ctx, self.r
+        ctx.tn(r, r, 1.0, U1, Q, dptr(self.C), r, tag="tn_merge_leak")
+        self.comm.allreduce_sum_(self.C)
+        ctx.maxabs(dptr(self.C), r, r, r, dptr(self.leak), thr=REORTH_TOL,
+                   gate_out=self.gate(G_LEAK))
+
+    def speculative_core(self):
+        """Whether the merge core runs speculatively beside the leak check:
+        single shard (no collective on the side stream), a single-cluster
+        E-SVD (pod_merge_core_gatable), POD_SPEC_CORE not 0."""
+        if self._spec is None:
+            self._spec = (SPEC_CORE and not self.comm.active
+                          and bool(_lib.load().pod_merge_core_gatable(self.r, self.r)))
+            if self._spec:
+                self._leak_stream = torch.cuda.Stream(self.ctx.device)
+        return self._spec
 
     def cosines_ops(self, old, new):
         """convergence_cosines (isma.py:181-201) into self.xi (length k);
