@@ -457,8 +457,21 @@ static int set_smem(const void* fn) {
   return POD_OK;
 }
 
+// Each solver CTA reserves the whole shared-memory carve-out (POD_BJ_EXCLUSIVE,
+// default on): no CTA of a concurrent GEMM can then be co-resident on the
+// cluster's SMs and stretch the latency-bound rotation chain.
+static bool exclusive_sms() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_BJ_EXCLUSIVE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <typename K, typename... Args>
 static int launch(K kernel, int cl, int threads, size_t smem, cudaStream_t stream, Args... args) {
+  if (exclusive_sms()) smem = SMEM_CAP;
   int st = set_smem((const void*)kernel);
   if (st) return st;
   if (cl > 8) {  // 16-CTA clusters are a non-portable size on sm_100a

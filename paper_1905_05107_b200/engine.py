@@ -93,6 +93,12 @@ TC_GRAM = __import__("os").environ.get("POD_TC_GRAM", "0") == "1"
 #: the leak check (U1^T Q, merge.py:72) runs beside it; a gated re-run covers
 #: the rounds whose second projection fires.  POD_SPEC_CORE=0 disables.
 SPEC_CORE = __import__("os").environ.get("POD_SPEC_CORE", "1") != "0"
+#: largest E (2r columns) the core runs speculatively for.  Measured
+#: (tools/spec_probe.py): config 2 (120) 51.9 -> 49.7 ms; config 3 (300)
+#: neutral (the side-stream update chain sets the round there); config 4
+#: (384): U1^T Q sits at ~1e-8, next to the threshold, the check fires in
+#: 4-19 of 34 rounds and every fire re-runs a 5-7 ms core (1.53 -> 2.05 s)
+SPEC_MAX_N = 256
 #: CTA cap of the speculative leak check's GEMM (full grid: its CTAs crowd the
 #: E-SVD's cluster -- config 2 57.8 ms; 8: the check outlasts the core, 66 ms;
 #: 32-64: 51.2-51.4 ms vs 52.3 serial)
@@ -308,9 +314,10 @@ class MergeWorkspace:
     def speculative_core(self):
         """Whether the merge core runs speculatively beside the leak check:
         single shard (no collective on the side stream), a single-cluster
-        E-SVD (pod_merge_core_gatable), POD_SPEC_CORE not 0."""
+        E-SVD (pod_merge_core_gatable) of at most SPEC_MAX_N columns,
+        POD_SPEC_CORE not 0."""
         if self._spec is None:
-            self._spec = (SPEC_CORE and not self.comm.active
+            self._spec = (SPEC_CORE and not self.comm.active and 2 * self.r <= SPEC_MAX_N
                           and bool(_lib.load().pod_merge_core_gatable(self.r, self.r)))
             if self._spec:
                 self._leak_stream = torch.cuda.Stream(self.ctx.device)
