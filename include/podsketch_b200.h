@@ -138,6 +138,18 @@ int pod_resid_colnorms2(int atype, int64_t m, int64_t n, const void* A, int64_t 
                         const double* C, int64_t ldc, double* out, void* ws, size_t ws_bytes,
                         void* stream);
 
+/* Fused Wedin residuals (one pass over A): out2[0] = ||A V - U diag(sigma)||_F^2,
+ * out2[1] = ||A^T U - V diag(sigma)||_F^2 for U m x k, V n x k, 1 <= k <= 64.
+ * Each A tile feeds both FP64 DMMA products from shared memory; R stays in
+ * registers, S is reduced across a thread-block cluster (DSMEM) into row-range
+ * partials.  Deterministic.  Replaces quality.py:104-107 (r, s and their
+ * np.linalg.norm in wedin_measure). */
+size_t pod_wedin_ws_bytes(int64_t m, int64_t n, int64_t k);
+int pod_wedin_residuals(int atype, const void* A, int64_t m, int64_t n, int64_t lda,
+                        const double* U, int64_t ldu, const double* V, int64_t ldv,
+                        const double* sigma, int64_t k, double* out2, void* ws,
+                        size_t ws_bytes, void* stream);
+
 /* Gates: every compute entry point below that takes `gate` (device int32,
  * nullable) does nothing when *gate == 0, so a round's launch sequence is
  * static (capturable in a CUDA graph) while data-dependent branches of the

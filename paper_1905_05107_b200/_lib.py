@@ -52,6 +52,9 @@ SIGNATURES = {
     "pod_resid_ws_bytes": (_sz, [_i64, _i64]),
     "pod_resid_colnorms2": (_i32, [_i32, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp, _i64,
                                    _vp, _vp, _sz, _vp]),
+    "pod_wedin_ws_bytes": (_sz, [_i64, _i64, _i64]),
+    "pod_wedin_residuals": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp,
+                                   _i64, _vp, _vp, _sz, _vp]),
     "pod_gemm_tn_ws_bytes": (_sz, [_i64, _i64, _i64]),
     "pod_gemm_tn_f64": (_i32, [_i64, _i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                                _vp, _sz, _vp, _vp]),

@@ -185,6 +185,15 @@ class Ctx:
                    "pod_gather_scale_cols", A.code, A.ptr, A.m, A.ld, _ptr(idx64), _ptr(f), g,
                    D.ptr, D.ld, self.stream)
 
+    def wedin(self, A, U, V, sigma, k, out2):
+        """out2 = [||A V_k - U_k S_k||_F^2, ||A^T U_k - V_k S_k||_F^2] in one
+        pass over A (pod_wedin_residuals)."""
+        n = A.ncols
+        ws = self.ws("wedin", _lib.load().pod_wedin_ws_bytes(A.m, n, k))
+        self._call("wedin", 3, 4.0 * A.m * n * k, A.esize * A.m * n, "pod_wedin_residuals",
+                   A.code, A.ptr, A.m, n, A.ld, U.ptr, U.ld, V.ptr, V.ld, _ptr(sigma), k,
+                   _ptr(out2), _ptr(ws), ws.numel(), self.stream)
+
     def resid_colnorms2(self, A, n, U, r, C, ldc, out, cols=None):
         ws = self.ws("resid", _lib.load().pod_resid_ws_bytes(A.m, n))
         self._call("resid_colnorms2", 2, 2.0 * A.m * n * r, A.m * (A.esize * n + 8.0 * r),

@@ -1,11 +1,13 @@
 """Accuracy metrics on the GPU -- drop-in for ``podsketch.quality``
 (quality.py:1-118).
 
-``wedin_measure`` computes the residuals R = A V_k - U_k S_k and
-S = A^T U_k - V_k S_k with the FP64 DMMA GEMMs of the ISMA path (NN for
-A V_k, split-K TN for A^T U_k) and their Frobenius norms with the column-norm
-reduction; ``principal_angles`` / ``mode_angles`` use the TN GEMM + Jacobi
-singular values and the column dot kernel.
+``wedin_measure`` computes ||R||_F and ||S||_F of the residuals
+R = A V_k - U_k S_k and S = A^T U_k - V_k S_k in ONE pass over A
+(``pod_wedin_residuals``: every A tile feeds both FP64 DMMA products from
+shared memory, R is reduced in the epilogue without being written, S across a
+thread-block cluster); k > 64 falls back to two GPU passes (NN for A V_k,
+split-K TN for A^T U_k).  ``principal_angles`` / ``mode_angles`` use the TN
+GEMM + Jacobi singular values and the column dot kernel.
 """
 
 from __future__ import annotations
@@ -17,6 +19,9 @@ import numpy as np
 
 from .errors import ParameterError
 from .matcore import ZERO_SIGMA_RTOL
+
+#: largest k of the fused single-pass residual kernel (pod_wedin_residuals)
+WEDIN_FUSED_MAX_K = 64
 
 #: quality.py:15-19
 DEGENERATE_OMEGA_ADVICE = (
@@ -127,6 +132,30 @@ def wedin_measure(a, factor, k):
     Uk = to_device_colmajor(np.asfortranarray(factor.u[:, :k]), dev)
     Vk = to_device_colmajor(np.asfortranarray(factor.v[:, :k]), dev)
     sk = np.asarray(factor.sigma[:k], dtype=np.float64)
+    if k <= WEDIN_FUSED_MAX_K:
+        # quality.py:104-107 fused: one pass over A, Frobenius sums in the epilogues
+        sig_d = torch.as_tensor(sk, device=dev)
+        out2 = torch.zeros(2, dtype=torch.float64, device=dev)
+        ctx.wedin(A, Uk, Vk, sig_d, k, out2)
+        r2, s2 = out2.cpu().numpy()
+        r_norm, s_norm = math.sqrt(r2), math.sqrt(s2)
+    else:
+        r_norm, s_norm = _wedin_two_pass(ctx, A, Uk, Vk, sk, m, n, k)
+    sig = factor.sigma
+    omega_hat = float(min(abs(sig[k - 1] - sig[k]), sig[k - 1]))
+    degenerate = bool(omega_hat <= ZERO_SIGMA_RTOL * max(sig[0], 1e-300))
+    measure = math.inf if degenerate else math.hypot(r_norm, s_norm) / omega_hat
+    return WedinReport(r_norm=r_norm, s_norm=s_norm, omega_hat=omega_hat, measure=measure,
+                       ceiling=math.sqrt(2.0 * k), degenerate=degenerate)
+
+
+def _wedin_two_pass(ctx, A, Uk, Vk, sk, m, n, k):
+    """k > 64: R and S materialised by the NN / TN GEMMs (two passes over A)."""
+    import torch
+
+    from .device import ColMat, dptr
+
+    dev = ctx.device
     D = torch.as_tensor(np.diag(sk).T.copy().reshape(-1), device=dev)  # k x k, column-major
     # R = A V_k - U_k S_k   (quality.py:104)
     Rm = ColMat.zeros(m, k, dev)
@@ -136,11 +165,4 @@ def wedin_measure(a, factor, k):
     Sm = ColMat.zeros(n, k, dev)
     ctx.tn(n, k, 1.0, A, Uk, Sm.ptr, Sm.ld, tag="tn_wedin_AtU")
     ctx.small_gemm(n, k, k, -1.0, Vk.ptr, Vk.ld, 0, dptr(D), k, 1.0, Sm.ptr, Sm.ld)
-    r_norm = _frobenius(ctx, Rm)
-    s_norm = _frobenius(ctx, Sm)
-    sig = factor.sigma
-    omega_hat = float(min(abs(sig[k - 1] - sig[k]), sig[k - 1]))
-    degenerate = bool(omega_hat <= ZERO_SIGMA_RTOL * max(sig[0], 1e-300))
-    measure = math.inf if degenerate else math.hypot(r_norm, s_norm) / omega_hat
-    return WedinReport(r_norm=r_norm, s_norm=s_norm, omega_hat=omega_hat, measure=measure,
-                       ceiling=math.sqrt(2.0 * k), degenerate=degenerate)
+    return _frobenius(ctx, Rm), _frobenius(ctx, Sm)
