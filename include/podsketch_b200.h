@@ -183,6 +183,30 @@ int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, const double*
                     const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* gate,
                     void* stream);
 /* Typed X (POD_F64 or POD_F32 storage, exact fp64 arithmetic); T, Z, Y fp64. */
+/* Y = alpha X T (pod_gemm_nn_f64, streamed kernel, no gather, Y not aliasing
+ * X) that also returns dots[j] = sum_i Y[i, j] X[i, j] for j < kdot, formed
+ * in the GEMM's epilogue from the stored values (fixed-order reduction).
+ * With X = [U_old Q] and Y = U_new = X U_E these are the raw convergence
+ * cosines u_old_j . u_new_j of isma.py:195-198 (criterion "modes"): the
+ * rotation and the cosine pass become one pass.  gate must be NULL. */
+size_t pod_gemm_nn_dots_ws_bytes(int64_t kdot);
+int pod_gemm_nn_dots(int64_t m, int64_t p, int64_t q, double alpha, const double* X, int64_t ldx,
+                     const double* T, int64_t ldt, double* Y, int64_t ldy, int64_t kdot,
+                     double* dots, void* ws, size_t ws_bytes, const int32_t* gate, void* stream);
+
+/* pod_gemm_nn_f64 (no gather) that also returns G (q x q) = Y^T Y, formed
+ * from each output tile while it is on chip (fixed-order split reduction,
+ * exactly symmetric): the Gram of the block a CholeskyQR pass consumes next,
+ * without a TN pass over it.  Shapes with pod_gemm_nn_gram_ok(p, q) only
+ * (q <= 64, p >= q, T resident in shared memory).  Replaces the Gram of
+ * merge.py:70 (QR of the residual U2 - U1 M) and of the second CholeskyQR
+ * pass. */
+int pod_gemm_nn_gram_ok(int64_t p, int64_t q);
+size_t pod_gemm_nn_gram_ws_bytes(int64_t m, int64_t q);
+int pod_gemm_nn_gram(int64_t m, int64_t p, int64_t q, double alpha, const double* X, int64_t ldx,
+                     const double* T, int64_t ldt, double beta, const double* Z, int64_t ldz,
+                     double* Y, int64_t ldy, double* G, int64_t ldg, void* ws, size_t ws_bytes,
+                     const int32_t* gate, void* stream);
 int pod_gemm_nn(int xtype, int64_t m, int64_t p, int64_t q, double alpha, const void* X,
                 int64_t ldx, const int32_t* xcols, const double* T, int64_t ldt, double beta,
                 const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* gate,

@@ -55,6 +55,13 @@ SIGNATURES = {
     "pod_wedin_ws_bytes": (_sz, [_i64, _i64, _i64]),
     "pod_wedin_residuals": (_i32, [_i32, _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp,
                                    _i64, _vp, _vp, _sz, _vp]),
+    "pod_gemm_nn_dots_ws_bytes": (_sz, [_i64]),
+    "pod_gemm_nn_dots": (_i32, [_i64, _i64, _i64, _f64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _vp,
+                                _vp, _sz, _vp, _vp]),
+    "pod_gemm_nn_gram_ok": (_i32, [_i64, _i64]),
+    "pod_gemm_nn_gram_ws_bytes": (_sz, [_i64, _i64]),
+    "pod_gemm_nn_gram": (_i32, [_i64, _i64, _i64, _f64, _vp, _i64, _vp, _i64, _f64, _vp, _i64,
+                                _vp, _i64, _vp, _i64, _vp, _sz, _vp, _vp]),
     "pod_gemm_tn_ws_bytes": (_sz, [_i64, _i64, _i64]),
     "pod_gemm_tn_f64": (_i32, [_i64, _i64, _i64, _f64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _i64,
                                _vp, _sz, _vp, _vp]),

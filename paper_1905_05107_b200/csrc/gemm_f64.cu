@@ -98,6 +98,41 @@ __device__ __forceinline__ void nn_epilogue(const double (&acc)[4][FN][2], int64
   }
 }
 
+// nn_epilogue that also accumulates, for local output columns j < kdl, the
+// products Y[i, j] X[i, j] of the stored value with X's same-index column
+// (read back from L2: the convergence cosines of isma.py:195-198 when
+// X = [U_old Q] and Y = U_new, formed inside the rotation GEMM)
+template <int FN>
+__device__ __forceinline__ void nn_epilogue_dots(const double (&acc)[4][FN][2], int64_t row0,
+                                                 int col0, int lane, int64_t m, int q,
+                                                 double alpha, double* Y, int64_t ldy,
+                                                 const double* __restrict__ DX, int64_t dldx,
+                                                 int kdl, double (&dacc)[FN][2]) {
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t i = row0 + f * 8 + (lane >> 2);
+    double xr[FN][2];
+#pragma unroll
+    for (int g = 0; g < FN; ++g)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = col0 + g * 8 + 2 * (lane & 3) + e;
+        xr[g][e] = (i < m && j < kdl) ? __ldg(DX + i + (int64_t)j * dldx) : 0.0;
+      }
+#pragma unroll
+    for (int g = 0; g < FN; ++g)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = col0 + g * 8 + 2 * (lane & 3) + e;
+        if (i < m && j < q) {
+          const double v = alpha * acc[f][g][e];
+          Y[i + (int64_t)j * ldy] = v;
+          dacc[g][e] = fma(v, xr[g][e], dacc[g][e]);
+        }
+      }
+  }
+}
+
 // Grid cap for the persistent / split-K GEMMs launched while it is set
 // (pod_set_grid_cap): lets a concurrent, off-critical-path stream (the
 // pipelined update of the next round) leave SMs to the critical path.  0 = all.
@@ -473,15 +508,23 @@ inline size_t smem_bytes(int p, int bn) {
   return ((size_t)2 * kpad(p) * LDX + (size_t)bn * ldt(p)) * sizeof(double);
 }
 
-template <int BN>
+// GRAM (BN = 64, p >= q): the output tile, while still on chip, is also
+// multiplied by its own transpose -- G_cta += Y_blk^T Y_blk over the CTA's
+// row blocks (upper-triangular 8 x 8 fragments, 36 at q = 64, dealt over the
+// 8 warps) -- so the CholeskyQR pass that consumes Y needs no TN pass over it
+// (merge.py:70 QR of the residual; the Gram of CholeskyQR2's second pass).
+// gws[blockIdx.x] receives the CTA's q x q partial (column-major, upper part).
+template <int BN, bool GRAM = false>
 __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, double alpha,
                                                   const double* X, int64_t ldx,
                                                   const int32_t* __restrict__ xcols,
                                                   const double* __restrict__ T, int64_t ldT,
                                                   double beta, const double* Z, int64_t ldz,
                                                   double* Y, int64_t ldy,
-                                                  const int32_t* __restrict__ gate, int vec16) {
+                                                  const int32_t* __restrict__ gate, int vec16,
+                                                  double* __restrict__ gws = nullptr) {
   using C = Cfg<BN>;
+  static_assert(!GRAM || BN == 64, "Gram epilogue: one 64-column group");
   if (gate && *gate == 0) return;
   extern __shared__ __align__(16) double smem[];
   const int KP = kpad(p), LT = ldt(p);
@@ -532,6 +575,30 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
     }
   };
   const int wm = warp % C::WM, wn = warp / C::WM;
+  // Gram fragments of this warp: upper-triangular (fi <= fj) among NQ^2
+  constexpr int GF = GRAM ? 5 : 1;  // ceil(36 / 8)
+  const int NQ = (q + 7) >> 3;
+  int gfi[GF], gfj[GF];
+  double gacc[GF][2];
+#pragma unroll
+  for (int f = 0; f < GF; ++f) {
+    gfi[f] = gfj[f] = -1;
+    gacc[f][0] = gacc[f][1] = 0.0;
+  }
+  if constexpr (GRAM) {
+#pragma unroll
+    for (int f = 0; f < GF; ++f) {  // upper fragment idx = warp + 8 f, column-ordered
+      int idx = warp + 8 * f, fj = 0;
+      while (idx > fj) {
+        idx -= fj + 1;
+        ++fj;
+      }
+      if (fj < NQ) {
+        gfi[f] = idx;
+        gfj[f] = fj;
+      }
+    }
+  }
   int64_t rb = blockIdx.x;
   if (rb < nblk) load_block(xs0, rb);
   cp_async_commit();
@@ -574,9 +641,49 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
       nn_store<C::FN>(acc, zv, row0, wn * (BN / C::WN), lane, m, q, alpha, beta, Y, ldy);
     else
       nn_epilogue<C::FN>(acc, row0, wn * (BN / C::WN), lane, m, q, alpha, beta, Z, ldz, Y, ldy);
+    if constexpr (GRAM) {
+      // the tile as stored (zero outside m x q) -> the consumed X buffer,
+      // [col][row] with ld LDX; then the CTA's Gram fragments over its 64 rows
+      double* ys = const_cast<double*>(xs);
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int g = 0; g < C::FN; ++g)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int il = wm * 32 + f * 8 + (lane >> 2);
+            const int j = wn * (BN / C::WN) + g * 8 + 2 * (lane & 3) + e;
+            double v = alpha * acc[f][g][e];
+            if (beta != 0.0) v += beta * zv[f][g][e];
+            if (j < NQ * 8) ys[j * LDX + il] = (rb * BM + il < m && j < q) ? v : 0.0;
+          }
+      __syncthreads();
+#pragma unroll
+      for (int f = 0; f < GF; ++f) {
+        if (gfi[f] < 0) continue;
+        const double* ya = ys + (gfi[f] * 8 + (lane >> 2)) * LDX + (lane & 3);
+        const double* yb = ys + (gfj[f] * 8 + (lane >> 2)) * LDX + (lane & 3);
+#pragma unroll 4
+        for (int k0 = 0; k0 < BM; k0 += 4) dmma8x8x4(gacc[f][0], gacc[f][1], ya[k0], yb[k0]);
+      }
+      __syncthreads();  // ys (this block's X buffer) is the next prefetch's target
+    }
     buf ^= 1;
   }
   cp_async_wait<0>();
+  if constexpr (GRAM) {
+    double* out = gws + (size_t)blockIdx.x * q * q;
+#pragma unroll
+    for (int f = 0; f < GF; ++f) {
+      if (gfi[f] < 0) continue;
+      const int i = gfi[f] * 8 + (lane >> 2);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = gfj[f] * 8 + 2 * (lane & 3) + e;
+        if (i < q && j < q) out[(size_t)j * q + i] = gacc[f][e];
+      }
+    }
+  }
 }
 }  // namespace nnp
 
@@ -621,7 +728,7 @@ struct Cfg {
 // than one group only when Y aliases neither X nor Z (a group writes its
 // columns of a row block while another group may still be reading X there).
 
-template <int BN, typename TX = double>
+template <int BN, typename TX = double, bool DOTS = false>
 __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p, int q,
                                                                  double alpha,
                                                   const TX* X, int64_t ldx,
@@ -629,7 +736,10 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p
                                                   const double* __restrict__ T, int64_t ldT,
                                                   double beta, const double* Z, int64_t ldz,
                                                   double* Y, int64_t ldy,
-                                                  const int32_t* __restrict__ gate, int vx, int vt) {
+                                                  const int32_t* __restrict__ gate, int vx, int vt,
+                                                  const double* __restrict__ DX = nullptr,
+                                                  int64_t dldx = 0, int kdot = 0,
+                                                  double* __restrict__ dws = nullptr) {
   using C = Cfg<BN, TX>;
   constexpr int ST = C::STAGES;
   if (gate && *gate == 0) return;
@@ -641,18 +751,25 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p
     return reinterpret_cast<double*>(smem_raw + (size_t)st * (C::XBYTES + C::TT * sizeof(double)) +
                                      C::XBYTES);
   };
+  // column dots (kdot > 0, fp64 X): local columns j < kdl of this group
+  const int q0 = blockIdx.y * BN;
+  const int kdl = DOTS ? min(kdot - q0, BN) : 0;
   {
-    const int q0 = blockIdx.y * BN;
     T += (int64_t)q0 * ldT;
     Y += (int64_t)q0 * ldy;
     if (Z) Z += (int64_t)q0 * ldz;
+    if (kdl > 0) DX += (int64_t)q0 * dldx;
     q = min(BN, q - q0);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nkb = (p + BK - 1) / BK;
   const int64_t nblk = (m + C::BM - 1) / C::BM;
   const int64_t G = gridDim.x;
-  if ((int64_t)blockIdx.x >= nblk) return;
+  if ((int64_t)blockIdx.x >= nblk) {
+    for (int j = threadIdx.x; j < kdl; j += C::NTHREADS)
+      dws[(int64_t)(q0 + j) * gridDim.x + blockIdx.x] = 0.0;
+    return;
+  }
   const int64_t nmine = (nblk - blockIdx.x + G - 1) / G;
   const int64_t total = nmine * nkb;
 
@@ -708,6 +825,9 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p
 
   const int wm = warp % C::WM, wn = warp / C::WM;
   double acc[4][C::FN][2];
+  double dacc[C::FN][2];
+#pragma unroll
+  for (int g = 0; g < C::FN; ++g) dacc[g][0] = dacc[g][1] = 0.0;
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) {
     if (s < total) load_stage(s);
@@ -752,10 +872,46 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p
       kb = 0;
       const int64_t row0 = c_r0 + wm * 32;
       c_r0 += G * C::BM;
-      nn_epilogue<C::FN>(acc, row0, wn * (BN / C::WN), lane, m, q, alpha, beta, Z, ldz, Y, ldy);
+      if constexpr (DOTS)  // beta = 0 (pod_gemm_nn_dots)
+        nn_epilogue_dots<C::FN>(acc, row0, wn * (BN / C::WN), lane, m, q, alpha, Y, ldy, DX, dldx,
+                                kdl, dacc);
+      else
+        nn_epilogue<C::FN>(acc, row0, wn * (BN / C::WN), lane, m, q, alpha, beta, Z, ldz, Y, ldy);
     }
   }
   cp_async_wait<0>();
+  if (DOTS && kdl > 0) {
+    // CTA column sums in a fixed order: lanes sharing a column, then the
+    // WM warps along M through shared memory (the stages are free now)
+    __syncthreads();
+    double* red = reinterpret_cast<double*>(smem_raw);  // WM x BN
+#pragma unroll
+    for (int g = 0; g < C::FN; ++g)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double v = dacc[g][e];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        if (lane < 4) red[wm * BN + wn * (BN / C::WN) + g * 8 + 2 * lane + e] = v;
+      }
+    __syncthreads();
+    for (int j = threadIdx.x; j < kdl; j += C::NTHREADS) {
+      double t = 0.0;
+      for (int w = 0; w < C::WM; ++w) t += red[w * BN + j];
+      dws[(int64_t)(q0 + j) * gridDim.x + blockIdx.x] = t;
+    }
+  }
+}
+
+// out[j] = sum over the CTAs of dws[j][cta] (fixed order), j < k
+__global__ void dots_final_kernel(const double* __restrict__ dws, int nchunk, int k,
+                                  double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= k) return;
+  double t = 0.0;
+  for (int c = 0; c < nchunk; ++c) t += dws[(int64_t)j * nchunk + c];
+  out[j] = t;
 }
 }  // namespace nns
 
@@ -815,12 +971,24 @@ static int ensure_attrs() {
   TN80_ATTR(float, double)
   TN80_ATTR(double, float)
 #undef TN80_ATTR
+  e = cudaFuncSetAttribute((const void*)nnp::kernel<64, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e != cudaSuccess) return cuda_status(e, "nnp gram attr");
   for (int bn : {64, 128, 192}) {
     const void* fn = bn == 64 ? (const void*)nnp::kernel<64>
                    : bn == 128 ? (const void*)nnp::kernel<128> : (const void*)nnp::kernel<192>;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return cuda_status(e, "nnp attr");
   }
+#define NNS_DOTS_ATTR(BN_)                                                                 \
+  e = cudaFuncSetAttribute(nns::kernel<BN_, double, true>,                                 \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nns::Cfg<BN_>::SMEM); \
+  if (e != cudaSuccess) return cuda_status(e, "nns dots attr");
+  NNS_DOTS_ATTR(64)
+  NNS_DOTS_ATTR(80)
+  NNS_DOTS_ATTR(128)
+  NNS_DOTS_ATTR(192)
+#undef NNS_DOTS_ATTR
   e = cudaFuncSetAttribute(nns::kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)nns::Cfg<64>::SMEM);
   if (e != cudaSuccess) return cuda_status(e, "nns attr");
@@ -846,6 +1014,12 @@ static int ensure_attrs() {
 }  // namespace pod
 
 using namespace pod;
+
+static int nn_streamed(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
+                       int64_t ldx, const int32_t* xcols, const double* T, int64_t ldt,
+                       double beta, const double* Z, int64_t ldz, double* Y, int64_t ldy,
+                       const int32_t* gate, cudaStream_t s, const double* DX, int64_t dldx,
+                       int kdot, double* dws, int64_t* nchunk_out);
 
 extern "C" size_t pod_gemm_tn_ws_bytes(int64_t m, int64_t p, int64_t q) {
   if (m <= 0 || p <= 0 || q <= 0) return 0;
@@ -999,6 +1173,18 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
       return POD_OK;
     }
   }
+  int64_t nchunk = 0;
+  return nn_streamed(m, p, q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, s, nullptr,
+                     0, 0, nullptr, &nchunk);
+}
+
+// The streamed (nns) launches of pod_gemm_nn_f64, with optional column dots
+// (kdot > 0: dws[j][cta] partials; *nchunk_out = CTAs along the rows).
+static int nn_streamed(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
+                       int64_t ldx, const int32_t* xcols, const double* T, int64_t ldt,
+                       double beta, const double* Z, int64_t ldz, double* Y, int64_t ldy,
+                       const int32_t* gate, cudaStream_t s, const double* DX, int64_t dldx,
+                       int kdot, double* dws, int64_t* nchunk_out) {
   {
     const int vx = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && (ldx % 2 == 0);
     const int vt = ((reinterpret_cast<uintptr_t>(T) & 15) == 0) && (ldt % 2 == 0);
@@ -1022,30 +1208,112 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
         const unsigned gy = (unsigned)ceil_div(q, 80);
         const int64_t per = std::max<int64_t>(1, capped(C80::PER_SM * 148) / gy);
         const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
-        nns::kernel<80><<<grid, C80::NTHREADS, C80::SMEM, s>>>(
-            m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+        *nchunk_out = grid.x;
+        (kdot > 0 ? nns::kernel<80, double, true> : nns::kernel<80, double, false>)<<<grid, C80::NTHREADS, C80::SMEM, s>>>(
+            m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt,
+            DX, dldx, kdot, dws);
       } else {
         const int64_t nblk = ceil_div(m, nns::Cfg<64>::BM);
         const unsigned gy = (unsigned)ceil_div(q, 64);
         const int64_t per = std::max<int64_t>(1, capped(nns::Cfg<64>::PER_SM * 148) / gy);
         const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
-        nns::kernel<64><<<grid, nns::THREADS, nns::Cfg<64>::SMEM, s>>>(
-            m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+        *nchunk_out = grid.x;
+        (kdot > 0 ? nns::kernel<64, double, true> : nns::kernel<64, double, false>)<<<grid, nns::THREADS, nns::Cfg<64>::SMEM, s>>>(
+            m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt,
+            DX, dldx, kdot, dws);
       }
     } else if (q <= 128) {
       const int64_t nblk = ceil_div(m, nns::Cfg<128>::BM);
       const unsigned grid = (unsigned)std::min<int64_t>(nblk, capped(nns::Cfg<128>::PER_SM * 148));
-      nns::kernel<128><<<grid, nns::THREADS, nns::Cfg<128>::SMEM, s>>>(
-          m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+      *nchunk_out = grid;
+      (kdot > 0 ? nns::kernel<128, double, true> : nns::kernel<128, double, false>)<<<grid, nns::THREADS, nns::Cfg<128>::SMEM, s>>>(
+          m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt,
+          DX, dldx, kdot, dws);
     } else {
       const int64_t nblk = ceil_div(m, nns::Cfg<192>::BM);
       const unsigned grid = (unsigned)std::min<int64_t>(nblk, capped(nns::Cfg<192>::PER_SM * 148));
-      nns::kernel<192><<<grid, nns::THREADS, nns::Cfg<192>::SMEM, s>>>(
-          m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+      *nchunk_out = grid;
+      (kdot > 0 ? nns::kernel<192, double, true> : nns::kernel<192, double, false>)<<<grid, nns::THREADS, nns::Cfg<192>::SMEM, s>>>(
+          m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt,
+          DX, dldx, kdot, dws);
     }
     POD_CHECK_LAUNCH("nn streamed");
     return POD_OK;
   }
+}
+
+extern "C" size_t pod_gemm_nn_dots_ws_bytes(int64_t kdot) {
+  return (size_t)std::max<int64_t>(kdot, 1) * 2 * 148 * sizeof(double);
+}
+
+extern "C" int pod_gemm_nn_dots(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
+                                int64_t ldx, const double* T, int64_t ldt, double* Y, int64_t ldy,
+                                int64_t kdot, double* dots, void* ws, size_t ws_bytes,
+                                const int32_t* gate, void* stream) {
+  POD_REQUIRE(m >= 1 && p >= 1 && q >= 1 && ldx >= m && ldy >= m,
+              "pod_gemm_nn_dots: bad shape");
+  POD_REQUIRE(kdot >= 1 && kdot <= p && kdot <= q, "pod_gemm_nn_dots: need 1 <= kdot <= min(p, q)");
+  POD_REQUIRE(gate == nullptr, "pod_gemm_nn_dots: not gateable");
+  POD_REQUIRE(ws_bytes >= pod_gemm_nn_dots_ws_bytes(kdot), "pod_gemm_nn_dots: workspace too small");
+  const char* y0 = (const char*)Y;
+  const char* y1 = (const char*)(Y + (q - 1) * ldy + m);
+  const char* x0 = (const char*)X;
+  const char* x1 = (const char*)(X + (p - 1) * ldx + m);
+  POD_REQUIRE(!(x0 < y1 && y0 < x1), "pod_gemm_nn_dots: Y must not alias X");
+  int st = ensure_attrs();
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t nchunk = 0;
+  st = nn_streamed(m, p, q, alpha, X, ldx, nullptr, T, ldt, 0.0, nullptr, 1, Y, ldy, gate, s, X, ldx,
+                   (int)kdot, (double*)ws, &nchunk);
+  if (st) return st;
+  POD_REQUIRE(nchunk <= 2 * 148, "pod_gemm_nn_dots: grid larger than the workspace");
+  nns::dots_final_kernel<<<(unsigned)ceil_div(kdot, 128), 128, 0, s>>>((const double*)ws,
+                                                                     (int)nchunk, (int)kdot, dots);
+  POD_CHECK_LAUNCH("nn dots final");
+  return POD_OK;
+}
+
+// T-resident NN with the Gram epilogue: q <= 64 output columns, p >= q,
+// T in shared memory at 2 CTAs per SM
+extern "C" int pod_gemm_nn_gram_ok(int64_t p, int64_t q) {
+  return (q >= 1 && q <= 64 && p >= q && nnp::smem_bytes((int)p, 64) <= 110 * 1024) ? 1 : 0;
+}
+
+static int64_t nn_gram_grid(int64_t m) {
+  return std::min<int64_t>(ceil_div(m, nnp::BM), capped(2 * 148));
+}
+
+extern "C" size_t pod_gemm_nn_gram_ws_bytes(int64_t m, int64_t q) {
+  if (m <= 0 || q <= 0) return 256;
+  return (size_t)(2 * 148) * q * q * sizeof(double);  // >= any capped grid
+}
+
+extern "C" int pod_gemm_nn_gram(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
+                                int64_t ldx, const double* T, int64_t ldt, double beta,
+                                const double* Z, int64_t ldz, double* Y, int64_t ldy, double* G,
+                                int64_t ldg, void* ws, size_t ws_bytes, const int32_t* gate,
+                                void* stream) {
+  POD_REQUIRE(m >= 1 && pod_gemm_nn_gram_ok(p, q), "pod_gemm_nn_gram: shape not supported");
+  POD_REQUIRE(ldy >= m && ldx >= m && ldg >= q, "pod_gemm_nn_gram: bad leading dimension");
+  POD_REQUIRE(beta == 0.0 || Z != nullptr, "pod_gemm_nn_gram: beta != 0 needs Z");
+  POD_REQUIRE(ws_bytes >= pod_gemm_nn_gram_ws_bytes(m, q), "pod_gemm_nn_gram: workspace too small");
+  int st = ensure_attrs();
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = nnp::smem_bytes((int)p, 64);
+  const int vec16 = ((reinterpret_cast<uintptr_t>(X) & 15) == 0) && (ldx % 2 == 0);
+  const unsigned grid = (unsigned)nn_gram_grid(m);
+  nnp::kernel<64, true><<<grid, nnp::THREADS, bytes, s>>>(m, (int)p, (int)q, alpha, X, ldx, nullptr,
+                                                         T, ldt, beta, Z, ldz, Y, ldy, gate, vec16,
+                                                         (double*)ws);
+  POD_CHECK_LAUNCH("nn gram");
+  const int64_t tot = q * q;
+  const int blocks = (int)std::min<int64_t>(ceil_div(tot, 8), 16 * 148);
+  tn::reduce_kernel<<<blocks, 256, 0, s>>>((int)grid, (int)q, (int)q, 1.0, (const double*)ws, G,
+                                           ldg, gate, 1);
+  POD_CHECK_LAUNCH("nn gram reduce");
+  return POD_OK;
 }
 
 extern "C" int pod_set_grid_cap(int ctas) {

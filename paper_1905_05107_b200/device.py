@@ -226,6 +226,31 @@ class Ctx:
                    ldt, float(beta), Z.ptr if Z is not None else ctypes.c_void_p(0),
                    Z.ld if Z is not None else 1, Y.ptr, Y.ld, _gp(gate), self.stream)
 
+    def nn_dots(self, p, q, alpha, X, T, ldt, Y, kdot, dots, tag="gemm_nn"):
+        """Y = alpha X T and dots[j] = Y[:, j] . X[:, j] for j < kdot in the
+        same pass (pod_gemm_nn_dots)."""
+        m = X.m
+        ws = self.ws("nn_dots", _lib.load().pod_gemm_nn_dots_ws_bytes(kdot))
+        self._call(tag + "+dots", 2, 2.0 * m * p * q, float(m) * 8.0 * (p + q + kdot),
+                   "pod_gemm_nn_dots", m, p, q, float(alpha), X.ptr, X.ld, T, ldt, Y.ptr, Y.ld,
+                   kdot, _ptr(dots), _ptr(ws), ws.numel(), None, self.stream)
+
+    def nn_gram_ok(self, p, q):
+        return bool(_lib.load().pod_gemm_nn_gram_ok(p, q))
+
+    def nn_gram(self, p, q, alpha, X, T, ldt, Y, G, ldg, beta=0.0, Z=None, gate=None,
+                tag="gemm_nn"):
+        """Y = alpha X T + beta Z (nn) and G = Y^T Y from the output tiles
+        (pod_gemm_nn_gram; shapes with nn_gram_ok)."""
+        m = X.m
+        ws = self.ws("nn_gram", _lib.load().pod_gemm_nn_gram_ws_bytes(m, q))
+        nbytes = float(m) * 8.0 * (p + q + (q if beta != 0.0 else 0))
+        self._call((tag + "+gram") if gate is None else tag + "+gram[gated]", 2,
+                   2.0 * m * p * q + 1.0 * m * q * q, nbytes, "pod_gemm_nn_gram", m, p, q,
+                   float(alpha), X.ptr, X.ld, T, ldt, float(beta),
+                   Z.ptr if Z is not None else ctypes.c_void_p(0), Z.ld if Z is not None else 1,
+                   Y.ptr, Y.ld, G, ldg, _ptr(ws), ws.numel(), _gp(gate), self.stream)
+
     def small_ws(self, n):
         return self.ws("small", _lib.load().pod_small_ws_bytes(n))
 

@@ -104,6 +104,19 @@ SPEC_MAX_N = 256
 #: 32-64: 51.2-51.4 ms vs 52.3 serial)
 LEAK_GRID_CAP = int(__import__("os").environ.get("POD_LEAK_GRID_CAP", "64"))
 
+#: NN GEMMs whose output a CholeskyQR pass consumes next form its Gram in
+#: their epilogue (pod_gemm_nn_gram, q <= 64) instead of a TN pass over the
+#: output.  POD_NN_GRAM=0 disables.
+NN_GRAM = __import__("os").environ.get("POD_NN_GRAM", "1") != "0"
+
+#: POD_FUSED_COSINES=1: the merge's rotation GEMM also forms the convergence
+#: cosines (criterion "modes") in its epilogue (pod_gemm_nn_dots) instead of
+#: the separate coldots pass.  Off by default -- measured slower (config 2
+#: 49.13 -> 49.37 ms, config 3 2.905 -> 2.942 s): the epilogue re-reads
+#: U_old's k columns from L2 on the rotation's critical path and loads only
+#: the first column group's CTAs, which costs more than the 2-kernel pass.
+FUSED_COSINES = __import__("os").environ.get("POD_FUSED_COSINES", "0") == "1"
+
 #: debug/parity switch: when set, every run copies each round's drawn index
 #: set and counts (the draw slot's idx/cnt, still intact when the round's
 #: record is read) to the host -> IsmaEngine.draw_log, isma.LAST_DRAWS.
@@ -193,14 +206,17 @@ class MergeWorkspace:
         return l
 
     # ------------------------------------------------------- launch pieces --
-    def cholqr_ops(self, Wsrc, Q, l, Rout, gate_base, first_gate=None, sharded=True):
+    def cholqr_ops(self, Wsrc, Q, l, Rout, gate_base, first_gate=None, sharded=True,
+                   gram_ready=False):
         """Q = orthonormal factor of Wsrc (m x l) with Wsrc = Q Rout (the
         Householder QR of merge.py:70/76, matcore.py:209 replaced by
         CholeskyQR passes).  Passes 0 and 1 (CholeskyQR2) run when first_gate
         is null or set -- pass 0 into a scratch block, pass 1 from it into Q,
         so both GEMMs are out of place (column-group parallel); further
         passes run in place when the previous pass asked for them (slot
-        gate_base + p)."""
+        gate_base + p).  gram_ready: self.Gq already holds Wsrc^T Wsrc (from
+        the producing GEMM's Gram epilogue); pass 0's apply forms pass 1's
+        Gram the same way when the shape allows (nn_gram)."""
         ctx, r = self.ctx, self.r
         g0 = first_gate
         tmp = self._scratch_like(Q)
@@ -208,9 +224,12 @@ class MergeWorkspace:
         # the running R: pass 0 writes it, later passes fold R_p R into it
         # inside the factor kernel (pod_cholqr_factor2)
         rk = None if l <= 64 else dptr(self.Rk)
+        fuse = NN_GRAM and ctx.nn_gram_ok(l, l)
+        have_gram = gram_ready
         for p in range(2):  # CholeskyQR2: Wsrc -> tmp -> Q
             dst = tmp if p == 0 else Q
-            ctx.tn(l, l, 1.0, src, src, dptr(self.Gq), r, gate=g0, tag="tn_cholqr_gram")
+            if not have_gram:
+                ctx.tn(l, l, 1.0, src, src, dptr(self.Gq), r, gate=g0, tag="tn_cholqr_gram")
             if sharded:
                 self.comm.allreduce_sum_(self.Gq)
             ctx.cholqr_factor_acc(dptr(self.Gq), r, l, src.m, dptr(self.Rinv), r,
@@ -218,7 +237,13 @@ class MergeWorkspace:
                                   None if p == 0 else dptr(Rout), r,
                                   gate_in=g0, gate_out=self.gate(gate_base + p + 1),
                                   first_pass=1 if p == 0 else 0)
-            ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, dst, gate=g0, tag="nn_cholqr_apply")
+            if p == 0 and fuse:  # the apply also forms pass 1's Gram
+                ctx.nn_gram(l, l, 1.0, src, dptr(self.Rinv), r, dst, dptr(self.Gq), r, gate=g0,
+                            tag="nn_cholqr_apply")
+                have_gram = True
+            else:
+                ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, dst, gate=g0, tag="nn_cholqr_apply")
+                have_gram = False
             src = dst
         for p in range(2, CHOLQR_PASSES):
             gp = self.gate(gate_base + p)
@@ -243,10 +268,12 @@ class MergeWorkspace:
             self._qscratch[key] = buf
         return buf
 
-    def merge_ops(self, cur, ub=0, before_core=None):
+    def merge_ops(self, cur, ub=0, before_core=None, cos_out=None):
         """block_merge (merge.py:37-91) of stack `cur` (U1, sig[cur]) with
         update slot `ub` (Uupd, sig_upd) into stack 1 - cur, at capacity r.
-        `before_core` is issued after the GEMM phase, before the E-SVD."""
+        `before_core` is issued after the GEMM phase, before the E-SVD.
+        cos_out: the rotation also writes the raw convergence cosines
+        u_old_j . u_new_j, j < k (isma.py:195-198, criterion "modes")."""
         ctx, r = self.ctx, self.r
         S, Snext = self.S[cur], self.S[1 - cur]
         U1 = S.cols(0, r)
@@ -258,9 +285,14 @@ class MergeWorkspace:
         info = self.rec[0, REC_KEEP:]
         ctx.tn(r, r, 1.0, U1, U2, dptr(self.M), r, tag="tn_merge_proj")       # merge.py:65
         self.comm.allreduce_sum_(self.M)
-        ctx.nn(r, r, -1.0, U1, dptr(self.M), r, self.W, beta=1.0, Z=U2,
-               tag="nn_merge_resid")                                         # merge.py:69
-        self.cholqr_ops(self.W, Q, r, self.Rt, G_QR)                         # merge.py:70
+        if NN_GRAM and ctx.nn_gram_ok(r, r):  # the residual's Gram in the same pass
+            ctx.nn_gram(r, r, -1.0, U1, dptr(self.M), r, self.W, dptr(self.Gq), r, beta=1.0,
+                        Z=U2, tag="nn_merge_resid")                          # merge.py:69
+            self.cholqr_ops(self.W, Q, r, self.Rt, G_QR, gram_ready=True)    # merge.py:70
+        else:
+            ctx.nn(r, r, -1.0, U1, dptr(self.M), r, self.W, beta=1.0, Z=U2,
+                   tag="nn_merge_resid")                                     # merge.py:69
+            self.cholqr_ops(self.W, Q, r, self.Rt, G_QR)                     # merge.py:70
         spec = self.speculative_core()
         if spec:
             # the E-SVD on the first-pass (M, R) starts now; the leak check
@@ -300,8 +332,12 @@ class MergeWorkspace:
             if before_core is not None:
                 before_core()
             ctx.merge_core(*core, info=info)                                 # merge.py:80-85
-        ctx.nn(2 * r, r, 1.0, S, dptr(self.Tm), 2 * r, Snext.cols(0, r),
-               tag="nn_merge_rotate")                                        # merge.py:86-88
+        if cos_out is not None:  # rotation + cosines in one pass (isma.py:195-198)
+            ctx.nn_dots(2 * r, r, 1.0, S, dptr(self.Tm), 2 * r, Snext.cols(0, r), self.k, cos_out,
+                        tag="nn_merge_rotate")                               # merge.py:86-88
+        else:
+            ctx.nn(2 * r, r, 1.0, S, dptr(self.Tm), 2 * r, Snext.cols(0, r),
+                   tag="nn_merge_rotate")                                    # merge.py:86-88
 
     def leak_check_ops(self, U1, Q):
         """C = U1^T Q and the gate max|C| > REORTH_TOL (merge.py:72-73)."""
@@ -323,13 +359,19 @@ class MergeWorkspace:
                 self._leak_stream = torch.cuda.Stream(self.ctx.device)
         return self._spec
 
-    def cosines_ops(self, old, new):
+    def fused_cosines(self):
+        """Whether the merge's rotation forms the cosines (criterion modes)."""
+        return FUSED_COSINES and self.criterion == "modes" and 1 <= self.k <= self.r
+
+    def cosines_ops(self, old, new, fused=False):
         """convergence_cosines (isma.py:181-201) into self.xi (length k);
-        padded (missing) modes are zero columns and contribute 0."""
+        padded (missing) modes are zero columns and contribute 0.  fused:
+        the rotation already wrote the raw dots (only the shard sum is left)."""
         ctx, k = self.ctx, self.k
         P, Qn = self.S[old].cols(0, k), self.S[new].cols(0, k)
         if self.criterion == "modes":
-            ctx.coldots(P, Qn, k, k, False, self.xi)  # raw dots; |.| and clip on the host
+            if not fused:
+                ctx.coldots(P, Qn, k, k, False, self.xi)  # raw dots; |.| and clip on the host
             self.comm.allreduce_sum_(self.xi)
         else:
             ctx.tn(k, k, 1.0, P, Qn, dptr(self.Ck), k, tag="tn_cosines")
@@ -676,17 +718,20 @@ class IsmaEngine(MergeWorkspace):
                 self.side_ops(lambda: (self.lift_ops(u1, self.Uupd_b[u1].cols(0, self.r)),
                                        self.draw_gram_ops(mode, u2)), join=False)
 
+            fc = self.fused_cosines()
             try:
-                self.merge_ops(cur, ub, before_core=before_core)
+                self.merge_ops(cur, ub, before_core=before_core,
+                               cos_out=self.xi if fc else None)
             finally:
                 lib.pod_set_grid_cap(0)
-            self.cosines_ops(cur, 1 - cur)
+            self.cosines_ops(cur, 1 - cur, fused=fc)
             torch.cuda.current_stream(self.ctx.device).wait_stream(self.side)
             self.readback()
             return
         self.update_ops(mode, ub, self.Uupd_b[ub].cols(0, self.r), cur=cur, rowsrc=rowsrc)
-        self.merge_ops(cur, ub)
-        self.cosines_ops(cur, 1 - cur)
+        fc = self.fused_cosines()
+        self.merge_ops(cur, ub, cos_out=self.xi if fc else None)
+        self.cosines_ops(cur, 1 - cur, fused=fc)
         self.readback()
 
     def launch_round(self, mode, cur, ub, pipelined, rowsrc=None):

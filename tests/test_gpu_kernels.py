@@ -155,6 +155,61 @@ def test_gemm_nn(ctx, m, p, q):
     np.testing.assert_allclose(Y.to_numpy(), ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("m,p,q", [(1, 1, 1), (100, 7, 7), (4099, 20, 20), (262144 + 5, 60, 60),
+                                   (70001, 64, 64), (5000, 48, 40)])
+@pytest.mark.parametrize("beta", [0.0, 0.5])
+def test_gemm_nn_gram_epilogue(ctx, m, p, q, beta):
+    """pod_gemm_nn_gram: Y as pod_gemm_nn and G = Y^T Y from the output
+    tiles (exactly symmetric); a zero gate leaves Y and G untouched."""
+    rng = np.random.default_rng(m + 3 * p + q)
+    x = rng.standard_normal((m, p))
+    t = rng.standard_normal((p, q))
+    z = rng.standard_normal((m, q))
+    X, Z = dev_mat(x, ctx), dev_mat(z, ctx)
+    T = torch.as_tensor(np.asfortranarray(t).T.copy().reshape(-1), device=ctx.device)
+    Y = ColMat.zeros(m, q, ctx.device)
+    ldg = q + 3
+    G = torch.full((q * ldg,), 7.0, dtype=torch.float64, device=ctx.device)
+    assert ctx.nn_gram_ok(p, q)
+    ctx.nn_gram(p, q, -1.5, X, dptr(T), p, Y, dptr(G), ldg, beta=beta, Z=Z if beta else None)
+    ref = -1.5 * x @ t + beta * z
+    y = Y.to_numpy()
+    np.testing.assert_allclose(y, ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
+    g = G.cpu().numpy().reshape(q, ldg).T[:q, :]  # column-major q x q, ld = ldg
+    gref = y.T @ y
+    np.testing.assert_allclose(g, gref, rtol=1e-12, atol=1e-13 * np.abs(gref).max())
+    assert np.array_equal(g, g.T)
+    gate = torch.zeros(1, dtype=torch.int32, device=ctx.device)
+    Y.t.zero_()
+    ctx.nn_gram(p, q, 1.0, X, dptr(T), p, Y, dptr(G), ldg, gate=gate)
+    assert not Y.to_numpy().any() and np.array_equal(G.cpu().numpy().reshape(q, ldg).T[:q], g)
+
+
+@pytest.mark.parametrize("m,p,q,k", [(77, 8, 8, 8), (1000, 60, 30, 10), (262144 + 3, 120, 60, 20),
+                                     (100003, 300, 150, 50), (5001, 400, 200, 64)])
+def test_gemm_nn_dots_rotation_cosines(ctx, m, p, q, k):
+    """pod_gemm_nn_dots: the rotation Y = X T and the raw cosines
+    dots[j] = Y[:, j] . X[:, j] (j < k) formed in its epilogue."""
+    rng = np.random.default_rng(m + p + q + k)
+    x = rng.standard_normal((m, p))
+    t = rng.standard_normal((p, q))
+    X = dev_mat(x, ctx)
+    T = torch.as_tensor(np.asfortranarray(t).T.copy().reshape(-1), device=ctx.device)
+    Y = ColMat.zeros(m, q, ctx.device)
+    dots = torch.full((k,), 3.0, dtype=torch.float64, device=ctx.device)
+    ctx.nn_dots(p, q, 0.75, X, dptr(T), p, Y, k, dots)
+    ref = 0.75 * x @ t
+    np.testing.assert_allclose(Y.to_numpy(), ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
+    y = Y.to_numpy()
+    dref = np.einsum("ij,ij->j", y[:, :k], x[:, :k])
+    np.testing.assert_allclose(dots.cpu().numpy(), dref, rtol=1e-11,
+                               atol=1e-13 * np.sqrt((y[:, :k] ** 2).sum() * (x[:, :k] ** 2).sum()))
+
+
+def test_gemm_nn_gram_shape_limits(ctx):
+    assert not ctx.nn_gram_ok(60, 65) and not ctx.nn_gram_ok(30, 40) and ctx.nn_gram_ok(64, 64)
+
+
 def test_gemm_nn_inplace_and_gather(ctx):
     rng = np.random.default_rng(11)
     a = rng.standard_normal((10000, 30))
