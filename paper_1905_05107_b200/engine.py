@@ -978,6 +978,12 @@ class IsmaEngine(MergeWorkspace):
         return u, s, vv
 
 
+def eng_input_is_staged(A):
+    from .device import _STAGING
+
+    return any(A.t is b.t for b in _STAGING.values())
+
+
 _ENGINE_CACHE = {}
 ENGINE_CACHE_SIZE = 2  # per device: e.g. the two block widths of a column-block stream
 
@@ -1008,6 +1014,12 @@ def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=
                          precision=precision)
     except torch.OutOfMemoryError:
         lru.clear()  # cached engines hold their buffers: drop them and retry once
+        from .device import release_staging
+
+        if eng_input_is_staged(A):
+            pass  # the run's own matrix lives in the staging buffer: keep it
+        else:
+            release_staging()
         torch.cuda.empty_cache()
         eng = IsmaEngine(ctx, A, k=k, r=r, c=c, criterion=criterion, use_graphs=use_graphs,
                          comm=comm, row_offset=row_offset, m_total=m_total, w=w,

@@ -154,7 +154,7 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
     """
     import torch
 
-    from .device import ColMat, HostResident, get_ctx, to_device_colmajor
+    from .device import ColMat, HostResident, get_ctx, upload_matrix
     from .parallel import Comm, shard_rows
 
     a, m, n = _validate_shape(a)
@@ -198,7 +198,7 @@ def isma_run(a, config, rng=None, keep=None, *, device=None, return_device=False
         with HostResident(a) as A:
             return _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m,
                                return_device, precision)
-    A = to_device_colmajor(a, ctx.device)
+    A = upload_matrix(a, ctx.device)
     return _run_engine(ctx, A, config, rng, k, keep, use_graphs, comm, row_offset, m,
                        return_device, precision)
 
