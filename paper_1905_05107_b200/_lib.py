@@ -18,7 +18,8 @@ from .errors import (
 )
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpodsketch_b200.so")
+# POD_LIB_PATH: an alternative build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("POD_LIB_PATH") or os.path.join(_HERE, "libpodsketch_b200.so")
 
 POD_OK, POD_EPARAM, POD_EFORMAT, POD_EDEGENERATE, POD_ENOCONVERGE, POD_ECUDA, POD_ENCCL = (
     0, 2, 3, 4, 5, 6, 7)
