@@ -128,7 +128,7 @@ class ClockSampler:
 
 # ncu `--set full` DRAM traffic per call of the hot kernels (committed
 # summary of tools/profile_targets.py): "name | dram_rd [unit] | dram_wr [unit]"
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r02_ncu_traffic.txt")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r02b_ncu_traffic.txt")
 
 
 def _profiled_traffic():
@@ -669,8 +669,20 @@ def gpu_arm(args):
                 e2e.append(time.perf_counter() - t0)
         h2d = m * n * 8 + len(tr_h) * w["c"] * 8
         d2h = (f_h.u.size + f_h.sigma.size + (f_h.v.size if f_h.v is not None else 0)) * 8
+        # this box's pinned H2D rate for the same bytes (the e2e floor's main term)
+        dst = torch.empty_like(host, device=dev)
+        h2d_t = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dst.copy_(host, non_blocking=True)
+            torch.cuda.synchronize()
+            h2d_t.append(time.perf_counter() - t0)
+        del dst
         line["e2e"] = {"value": _max_over_ranks(statistics.mean(e2e), comm, torch, dev),
-                       "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+                       "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "runs_s": e2e, "h2d_matrix_s": min(h2d_t),
+                       "h2d_gbs": m * n * 8 / min(h2d_t) / 1e9}
         del host, a_pinned
     if not args.no_north_star:
         line["north_star"] = north_star_block(args, pod, torch, dev, comm, ws, rank)

@@ -7,7 +7,8 @@ import csv, subprocess, sys
 # kernels per call of each op, in tools/profile_targets.py order
 OPS = [("colnorms2", 1), ("draw", 1), ("tn_gram_gather", 2), ("tn_merge_proj", 2),
        ("tn_cholqr_gram", 2), ("nn_lift_gather", 1), ("nn_merge_resid", 1),
-       ("nn_merge_rotate", 1), ("gram_eigh", 2), ("merge_core", 1), ("cholqr_factor", 1)]
+       ("nn_merge_rotate", 1), ("gram_eigh", 2), ("merge_core", 1), ("cholqr_factor", 1),
+       ("nn_merge_resid+gram", 2), ("wedin_k20", 3)]
 rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
@@ -18,7 +19,7 @@ it = hdr.index("gpu__time_duration.sum")
 ki = hdr.index("Kernel Name")
 data = rows[2:]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
-print("# ncu --set full --clock-control none, tools/profile_targets.py on one B200 (round 2):")
+print("# ncu --set full --clock-control none, tools/profile_targets.py on one B200 (round 2, session 2):")
 print("# DRAM traffic per call of each hot op (its second, warm call), config-2 shapes")
 print(f"op | dram_rd | unit | dram_wr | unit | dur [{units[it]}] | kernels")
 pos = 0

@@ -34,6 +34,11 @@ Gq = (Wt @ Wt.T).T.contiguous().reshape(-1)
 Rinv = torch.empty(r * r, dtype=torch.float64, device=dev)
 Rk = torch.empty(r * r, dtype=torch.float64, device=dev)
 live = torch.ones(n, dtype=torch.uint8, device=dev)
+Gq2 = torch.empty(r * r, dtype=torch.float64, device=dev)
+Uw = ColMat(torch.randn((20, m), dtype=torch.float64, device=dev), m)
+Vw = ColMat(torch.randn((20, n), dtype=torch.float64, device=dev), n)
+sw = torch.linspace(5.0, 1.0, 20, dtype=torch.float64, device=dev)
+w2 = torch.empty(2, dtype=torch.float64, device=dev)
 uni = torch.rand(c := 100, dtype=torch.float64, device=dev)
 didx = torch.empty(g, dtype=torch.int32, device=dev)
 dcnt = torch.empty(g, dtype=torch.int64, device=dev)
@@ -50,6 +55,9 @@ ops = [
     ("merge_core", lambda: ctx.merge_core(dptr(sig1), r, dptr(M), r, dptr(R), r, dptr(sig1), r, r, r,
                                           dptr(Tm), 2 * r, r, dptr(sn))),
     ("cholqr_factor", lambda: ctx.cholqr_factor(dptr(Gq), r, r, m, dptr(Rinv), r, dptr(Rk), r)),
+    ("nn_merge_resid+gram", lambda: ctx.nn_gram(r, r, -1.0, S.cols(0, r), dptr(T), r, W, dptr(Gq2), r,
+                                                beta=1.0, Z=U2)),
+    ("wedin_k20", lambda: ctx.wedin(A, Uw, Vw, sw, 20, w2)),
 ]
 import sys as _s
 only = _s.argv[1:]  # optional subset of op names
