@@ -350,6 +350,145 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
   }
 }
 
+// cholqr_kernel for 104 < l <= CQI_MAX_L (config 3: l = 150), where the
+// three l x l buffers no longer fit shared memory and the global-memory path
+// runs every elimination step through L2 (~0.74 ms at l = 150): here only the
+// factor C lives in shared memory -- the scaled Gram is rebuilt from G for a
+// shifted retry, R is written out before the triangular inverse, and the
+// inverse overwrites C in place (column r of Rh is copied aside before step
+// r updates it).  Same operation order as cholqr_kernel, so the same bits.
+constexpr int CQI_MAX_L = 158;
+static size_t cqi_bytes(int64_t l) { return (size_t)l * l * 8 + (size_t)3 * l * 8; }
+
+__global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
+    const double* __restrict__ G, int64_t ldg, int l, double nrows, double* __restrict__ Rinv,
+    int64_t ldri, double* __restrict__ R, int64_t ldr, double* __restrict__ dinfo,
+    const int32_t* __restrict__ gate_in, int32_t* __restrict__ gate_out, int first_pass) {
+  if (gate_in && *gate_in == 0) {
+    if (gate_out && threadIdx.x == 0) *gate_out = 0;
+    return;
+  }
+  extern __shared__ __align__(16) double sm[];
+  double* C = sm;                      // factor, then its inverse (l x l)
+  double* d = C + (size_t)l * l;       // column scales
+  double* dr = d + l;                  // their reciprocals (0 for dead columns)
+  double* dr2 = dr + l;                // 1 / Rh[j][j]
+  __shared__ int s_fail;
+  __shared__ double s_defect;
+  __shared__ double s_row[CQI_MAX_L], s_col[CQI_MAX_L];
+  for (int i = threadIdx.x; i < l; i += blockDim.x) {
+    const double gii = G[i + (int64_t)i * ldg];
+    d[i] = (gii > 0.0) ? sqrt(gii) : 0.0;
+    dr[i] = d[i] > 0.0 ? 1.0 / d[i] : 0.0;
+  }
+  if (threadIdx.x == 0) s_defect = 0.0;
+  __syncthreads();
+  // scaled Gram H (+ shift on the diagonal), rebuilt from G for every attempt
+  auto build = [&](double shift, bool defect) {
+    double loc = 0.0;
+    for (int t = threadIdx.x; t < l * l; t += blockDim.x) {
+      const int j = t / l, i = t - j * l;
+      double h;
+      if (d[i] == 0.0 || d[j] == 0.0) {
+        h = (i == j) ? 1.0 : 0.0;
+      } else {
+        h = G[i + (int64_t)j * ldg] * dr[i] * dr[j];
+        loc = fmax(loc, fabs(h - (i == j ? 1.0 : 0.0)));
+      }
+      C[t] = h + ((i == j) ? shift : 0.0);
+    }
+    if (defect) {
+      __shared__ double red[32];
+      double v = warp_max(loc);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
+        v = warp_max(v);
+        if (threadIdx.x == 0) s_defect = v;
+      }
+    }
+  };
+  build(0.0, true);
+  double shift = 0.0;
+  int attempt = 0;
+  for (;;) {
+    if (attempt > 0) build(shift, false);
+    if (threadIdx.x == 0) s_fail = 0;
+    __syncthreads();
+    for (int j = 0; j < l; ++j) {
+      const double piv = C[j + j * l];
+      if (!(piv > 0.0)) {  // uniform decision
+        if (threadIdx.x == 0) s_fail = 1;
+        __syncthreads();
+        break;
+      }
+      const double rjj = sqrt(piv);
+      const double rinv = 1.0 / rjj;
+      __syncthreads();
+      if (threadIdx.x == 0) dr2[j] = rinv;
+      for (int k = j + threadIdx.x; k < l; k += blockDim.x)
+        C[j + k * l] = (k == j) ? rjj : C[j + k * l] * rinv;
+      __syncthreads();
+      const int rem = l - j - 1;
+      for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
+        const int kk = j + 1 + t / rem, ii = j + 1 + t % rem;
+        if (ii <= kk) C[ii + kk * l] -= C[j + ii * l] * C[j + kk * l];
+      }
+      __syncthreads();
+    }
+    if (!s_fail) break;
+    __syncthreads();
+    ++attempt;
+    const double base = 11.0 * (nrows * l + (double)l * (l + 1)) * 1.1102230246251565e-16 * l;
+    shift = (attempt == 1) ? base : shift * 100.0;
+    if (attempt > 8) break;
+  }
+  // strict lower part -> 0; R = Rh D (dead columns -> zero) before C is inverted
+  for (int t = threadIdx.x; t < l * l; t += blockDim.x) {
+    const int j = t / l, i = t - j * l;
+    if (i > j) C[t] = 0.0;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < l * l; t += blockDim.x) {
+    const int j = t / l, i = t - j * l;
+    const bool dead = d[i] == 0.0 || d[j] == 0.0;
+    R[i + (int64_t)j * ldr] = dead ? 0.0 : C[t] * d[j];
+  }
+  __syncthreads();
+  // Rh^-1 in place, right-looking back substitution (cholqr_kernel's steps)
+  for (int r = l - 1; r >= 0; --r) {
+    for (int i = threadIdx.x; i < r; i += blockDim.x) s_col[i] = C[i + r * l];
+    for (int c = r + threadIdx.x; c < l; c += blockDim.x) {
+      const double v = ((c == r) ? 1.0 : C[r + c * l]) * dr2[r];
+      C[r + c * l] = v;
+      s_row[c] = v;
+    }
+    __syncthreads();
+    const int w = l - r;
+    for (int t = threadIdx.x; t < r * w; t += blockDim.x) {
+      const int c = r + t / r, i = t % r;
+      C[i + c * l] = fma(-s_col[i], s_row[c], (c == r) ? 0.0 : C[i + c * l]);
+    }
+    __syncthreads();
+  }
+  int ndead = 0;
+  for (int t = threadIdx.x; t < l * l; t += blockDim.x) {
+    const int j = t / l, i = t - j * l;
+    const bool dead = d[i] == 0.0 || d[j] == 0.0;
+    Rinv[i + (int64_t)j * ldri] = dead ? 0.0 : C[t] * dr[i];
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < l; ++i) ndead += d[i] == 0.0;
+    dinfo[0] = s_defect;
+    dinfo[1] = (double)attempt;
+    dinfo[2] = (double)ndead;
+    dinfo[3] = shift;
+    if (s_fail) dinfo[POD_DINFO_BREAKDOWN] = 1.0;
+    if (gate_out) *gate_out = first_pass ? 1 : ((s_defect > 1e-4 || attempt > 0) ? 1 : 0);
+  }
+}
+
 // Register-resident CholeskyQR factor for l <= 64 (the merge rank of
 // BASELINE configs 1-2): same contract as cholqr_kernel.  256 threads: thread
 // (i = t % 64, q = t / 64) holds row i of the scaled Gram H at columns
@@ -630,6 +769,15 @@ static bool cqs_enabled() {
 }
 
 static size_t cholqr_bytes(int64_t l) { return (size_t)3 * l * l * 8 + (size_t)3 * l * 8 + 64; }
+// POD_CHOLQR_INPLACE=0: the global-memory factor for 104 < l <= 158 too (A/B)
+static bool cqi_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_CHOLQR_INPLACE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 int bj_merge_core(const double* sig1, int64_t l1, const double* M, int64_t ldm, const double* R,
                   int64_t ldr, const double* sig2, int64_t l2, int64_t r, int64_t rcap, double* T,
@@ -805,6 +953,13 @@ extern "C" int pod_cholqr_factor2(const double* G, int64_t ldg, int64_t l, int64
   POD_REQUIRE(l <= 1024, "pod_cholqr_factor: l = %lld exceeds 1024", (long long)l);
   const size_t bytes = cholqr_bytes(l);
   const int use_smem = bytes <= SMALL_SMEM_CAP;
+  if (!use_smem && l <= CQI_MAX_L && cqi_enabled()) {  // factor alone in shared memory
+    int e = set_smem((const void*)cholqr_inplace_kernel, cqi_bytes(l));
+    if (e) return e;
+    cholqr_inplace_kernel<<<1, SMALL_THREADS, cqi_bytes(l), st>>>(
+        G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr, dinfo, gate_in, gate_out, first_pass);
+    POD_CHECK_LAUNCH("cholqr in place");
+  } else {
   POD_REQUIRE(use_smem || ws_bytes >= bytes, "pod_cholqr_factor: workspace too small");
   if (use_smem) { int st = set_smem((const void*)cholqr_kernel<true>, bytes); if (st) return st; }
   if (use_smem)
@@ -816,6 +971,7 @@ extern "C" int pod_cholqr_factor2(const double* G, int64_t ldg, int64_t l, int64
       G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr, dinfo, (double*)ws, use_smem, gate_in,
       gate_out, first_pass);
   POD_CHECK_LAUNCH("cholqr");
+  }
   if (Racc) {  // Racc <- R Racc through the workspace's tail (general path)
     POD_REQUIRE(ws_bytes >= cholqr_bytes(l) + (size_t)l * l * 8, "pod_cholqr_factor: workspace");
     double* tmp = (double*)((char*)ws + cholqr_bytes(l));

@@ -282,7 +282,8 @@ def test_svd_small(ctx, nr, nc):
 
 
 @pytest.mark.parametrize("m,l,cond", [(1000, 10, 1e2), (50000, 60, 1e6), (3000, 130, 1e3),
-                                      (20000, 60, 1e12)])
+                                      (20000, 60, 1e12), (200000, 150, 1e6), (5000, 158, 1e10),
+                                      (4000, 105, 1e3), (3000, 159, 1e3)])
 def test_cholqr_orthonormal(ctx, m, l, cond):
     from paper_1905_05107_b200.engine import G_QR, MergeWorkspace
     rng = np.random.default_rng(l)
@@ -297,6 +298,50 @@ def test_cholqr_orthonormal(ctx, m, l, cond):
     rr = R.cpu().numpy().reshape(l, l).T
     assert np.abs(q.T @ q - np.eye(l)).max() < 1e-12
     np.testing.assert_allclose(q @ rr, w, atol=1e-13 * np.abs(w).max())
+
+
+_CQ_SCRIPT = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_1905_05107_b200.device import get_ctx, dptr
+ctx = get_ctx()
+rng = np.random.default_rng(4)
+l = {l}
+w = rng.standard_normal((3000, l)) * np.logspace(0, -5, l)
+w[:, 7] = 0.0  # a dead column
+g = w.T @ w
+G = torch.as_tensor(np.asfortranarray(g).T.copy().reshape(-1), device=ctx.device)
+Ri = torch.zeros(l * l, dtype=torch.float64, device=ctx.device)
+R = torch.zeros(l * l, dtype=torch.float64, device=ctx.device)
+ctx.cholqr_factor(dptr(G), l, l, 3000, dptr(Ri), l, dptr(R), l)
+torch.cuda.synchronize()
+np.save({out!r}, np.concatenate([R.cpu().numpy(), Ri.cpu().numpy()]))
+"""
+
+
+@pytest.mark.parametrize("l", [120, 150])
+def test_cholqr_inplace_factor_bitwise_equals_global_path(tmp_path, l):
+    """The shared-memory in-place factor (104 < l <= 158) reproduces the
+    global-memory kernel bit for bit, dead column included."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        out = str(tmp_path / f"cq{flag}.npy")
+        env = dict(os.environ, POD_CHOLQR_INPLACE=flag)
+        subprocess.run([sys.executable, "-c", _CQ_SCRIPT.format(root=root, l=l, out=out)],
+                       env=env, check=True)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
+    rr = outs[0][:l * l].reshape(l, l).T
+    ri = outs[0][l * l:].reshape(l, l).T
+    live = np.ones(l, bool)
+    live[7] = False
+    np.testing.assert_allclose((ri @ rr)[np.ix_(live, live)], np.eye(l - 1), atol=1e-9)
+    assert not rr[7].any() and not rr[:, 7].any() and not ri[7].any() and not ri[:, 7].any()
 
 
 def test_fix_signs_and_coldots(ctx):
