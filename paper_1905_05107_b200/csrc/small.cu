@@ -350,15 +350,18 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_kernel(
   }
 }
 
-// cholqr_kernel for 104 < l <= CQI_MAX_L (config 3: l = 150), where the
-// three l x l buffers no longer fit shared memory and the global-memory path
-// runs every elimination step through L2 (~0.74 ms at l = 150): here only the
-// factor C lives in shared memory -- the scaled Gram is rebuilt from G for a
-// shifted retry, R is written out before the triangular inverse, and the
-// inverse overwrites C in place (column r of Rh is copied aside before step
-// r updates it).  Same operation order as cholqr_kernel, so the same bits.
-constexpr int CQI_MAX_L = 158;
-static size_t cqi_bytes(int64_t l) { return (size_t)l * l * 8 + (size_t)3 * l * 8; }
+// cholqr_kernel for 104 < l <= CQI_MAX_L (configs 3 and 4: l = 150, 192),
+// where the three l x l buffers no longer fit shared memory and the
+// global-memory path runs every elimination step through L2 (~0.74 ms at
+// l = 150): here only the factor lives in shared memory, as a packed upper
+// triangle (column j holds rows 0..j at j (j + 1) / 2) -- the scaled Gram is
+// rebuilt from G for a shifted retry, R is written out before the triangular
+// inverse, and the inverse overwrites the factor in place (column r of Rh is
+// copied aside before step r updates it).  Same operations in the same
+// order as cholqr_kernel, so the same bits.
+constexpr int CQI_MAX_L = 230;
+static size_t cqi_bytes(int64_t l) { return (size_t)(l * (l + 1) / 2) * 8 + (size_t)3 * l * 8; }
+__device__ __forceinline__ int pk(int i, int j) { return (j * (j + 1) >> 1) + i; }  // i <= j
 
 __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
     const double* __restrict__ G, int64_t ldg, int l, double nrows, double* __restrict__ Rinv,
@@ -369,8 +372,9 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
     return;
   }
   extern __shared__ __align__(16) double sm[];
-  double* C = sm;                      // factor, then its inverse (l x l)
-  double* d = C + (size_t)l * l;       // column scales
+  const int np = l * (l + 1) / 2;
+  double* C = sm;                      // packed upper factor, then its inverse
+  double* d = C + np;                  // column scales
   double* dr = d + l;                  // their reciprocals (0 for dead columns)
   double* dr2 = dr + l;                // 1 / Rh[j][j]
   __shared__ int s_fail;
@@ -383,11 +387,17 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
   }
   if (threadIdx.x == 0) s_defect = 0.0;
   __syncthreads();
-  // scaled Gram H (+ shift on the diagonal), rebuilt from G for every attempt
+  // scaled Gram H (+ shift on the diagonal), upper triangle, rebuilt from G
+  // for every attempt (G is exactly symmetric: the defect over the upper
+  // triangle is the defect over all of H)
   auto build = [&](double shift, bool defect) {
     double loc = 0.0;
-    for (int t = threadIdx.x; t < l * l; t += blockDim.x) {
-      const int j = t / l, i = t - j * l;
+#pragma unroll 4
+    for (int t = threadIdx.x; t < np; t += blockDim.x) {
+      int j = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+      while (j * (j + 1) / 2 > t) --j;
+      while ((j + 1) * (j + 2) / 2 <= t) ++j;
+      const int i = t - j * (j + 1) / 2;
       double h;
       if (d[i] == 0.0 || d[j] == 0.0) {
         h = (i == j) ? 1.0 : 0.0;
@@ -395,7 +405,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
         h = G[i + (int64_t)j * ldg] * dr[i] * dr[j];
         loc = fmax(loc, fabs(h - (i == j ? 1.0 : 0.0)));
       }
-      C[t] = h + ((i == j) ? shift : 0.0);
+      C[pk(i, j)] = h + ((i == j) ? shift : 0.0);
     }
     if (defect) {
       __shared__ double red[32];
@@ -417,7 +427,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
     if (threadIdx.x == 0) s_fail = 0;
     __syncthreads();
     for (int j = 0; j < l; ++j) {
-      const double piv = C[j + j * l];
+      const double piv = C[pk(j, j)];
       if (!(piv > 0.0)) {  // uniform decision
         if (threadIdx.x == 0) s_fail = 1;
         __syncthreads();
@@ -428,12 +438,12 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
       __syncthreads();
       if (threadIdx.x == 0) dr2[j] = rinv;
       for (int k = j + threadIdx.x; k < l; k += blockDim.x)
-        C[j + k * l] = (k == j) ? rjj : C[j + k * l] * rinv;
+        C[pk(j, k)] = (k == j) ? rjj : C[pk(j, k)] * rinv;
       __syncthreads();
       const int rem = l - j - 1;
       for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
         const int kk = j + 1 + t / rem, ii = j + 1 + t % rem;
-        if (ii <= kk) C[ii + kk * l] -= C[j + ii * l] * C[j + kk * l];
+        if (ii <= kk) C[pk(ii, kk)] -= C[pk(j, ii)] * C[pk(j, kk)];
       }
       __syncthreads();
     }
@@ -444,31 +454,26 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
     shift = (attempt == 1) ? base : shift * 100.0;
     if (attempt > 8) break;
   }
-  // strict lower part -> 0; R = Rh D (dead columns -> zero) before C is inverted
-  for (int t = threadIdx.x; t < l * l; t += blockDim.x) {
-    const int j = t / l, i = t - j * l;
-    if (i > j) C[t] = 0.0;
-  }
-  __syncthreads();
+  // R = Rh D (dead columns -> zero, strict lower part zero) before Rh is inverted
   for (int t = threadIdx.x; t < l * l; t += blockDim.x) {
     const int j = t / l, i = t - j * l;
     const bool dead = d[i] == 0.0 || d[j] == 0.0;
-    R[i + (int64_t)j * ldr] = dead ? 0.0 : C[t] * d[j];
+    R[i + (int64_t)j * ldr] = (dead || i > j) ? 0.0 : C[pk(i, j)] * d[j];
   }
   __syncthreads();
   // Rh^-1 in place, right-looking back substitution (cholqr_kernel's steps)
   for (int r = l - 1; r >= 0; --r) {
-    for (int i = threadIdx.x; i < r; i += blockDim.x) s_col[i] = C[i + r * l];
+    for (int i = threadIdx.x; i < r; i += blockDim.x) s_col[i] = C[pk(i, r)];
     for (int c = r + threadIdx.x; c < l; c += blockDim.x) {
-      const double v = ((c == r) ? 1.0 : C[r + c * l]) * dr2[r];
-      C[r + c * l] = v;
+      const double v = ((c == r) ? 1.0 : C[pk(r, c)]) * dr2[r];
+      C[pk(r, c)] = v;
       s_row[c] = v;
     }
     __syncthreads();
     const int w = l - r;
     for (int t = threadIdx.x; t < r * w; t += blockDim.x) {
       const int c = r + t / r, i = t % r;
-      C[i + c * l] = fma(-s_col[i], s_row[c], (c == r) ? 0.0 : C[i + c * l]);
+      C[pk(i, c)] = fma(-s_col[i], s_row[c], (c == r) ? 0.0 : C[pk(i, c)]);
     }
     __syncthreads();
   }
@@ -476,7 +481,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
   for (int t = threadIdx.x; t < l * l; t += blockDim.x) {
     const int j = t / l, i = t - j * l;
     const bool dead = d[i] == 0.0 || d[j] == 0.0;
-    Rinv[i + (int64_t)j * ldri] = dead ? 0.0 : C[t] * dr[i];
+    Rinv[i + (int64_t)j * ldri] = (dead || i > j) ? 0.0 : C[pk(i, j)] * dr[i];
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < l; ++i) ndead += d[i] == 0.0;
@@ -769,7 +774,7 @@ static bool cqs_enabled() {
 }
 
 static size_t cholqr_bytes(int64_t l) { return (size_t)3 * l * l * 8 + (size_t)3 * l * 8 + 64; }
-// POD_CHOLQR_INPLACE=0: the global-memory factor for 104 < l <= 158 too (A/B)
+// POD_CHOLQR_INPLACE=0: the global-memory factor for 104 < l <= 230 too (A/B)
 static bool cqi_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -954,8 +959,14 @@ extern "C" int pod_cholqr_factor2(const double* G, int64_t ldg, int64_t l, int64
   const size_t bytes = cholqr_bytes(l);
   const int use_smem = bytes <= SMALL_SMEM_CAP;
   if (!use_smem && l <= CQI_MAX_L && cqi_enabled()) {  // factor alone in shared memory
-    int e = set_smem((const void*)cholqr_inplace_kernel, cqi_bytes(l));
-    if (e) return e;
+    static bool attr = false;  // up to 218 KB: above set_smem's 200 KB cap
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute((const void*)cholqr_inplace_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)cqi_bytes(CQI_MAX_L));
+      if (e != cudaSuccess) return cuda_status(e, "cholqr in place smem attr");
+      attr = true;
+    }
     cholqr_inplace_kernel<<<1, SMALL_THREADS, cqi_bytes(l), st>>>(
         G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr, dinfo, gate_in, gate_out, first_pass);
     POD_CHECK_LAUNCH("cholqr in place");

@@ -283,7 +283,8 @@ def test_svd_small(ctx, nr, nc):
 
 @pytest.mark.parametrize("m,l,cond", [(1000, 10, 1e2), (50000, 60, 1e6), (3000, 130, 1e3),
                                       (20000, 60, 1e12), (200000, 150, 1e6), (5000, 158, 1e10),
-                                      (4000, 105, 1e3), (3000, 159, 1e3)])
+                                      (4000, 105, 1e3), (3000, 159, 1e3), (30000, 192, 1e8), (3000, 230, 1e3),
+                                      (3000, 231, 1e3)])
 def test_cholqr_orthonormal(ctx, m, l, cond):
     from paper_1905_05107_b200.engine import G_QR, MergeWorkspace
     rng = np.random.default_rng(l)
@@ -319,7 +320,7 @@ np.save({out!r}, np.concatenate([R.cpu().numpy(), Ri.cpu().numpy()]))
 """
 
 
-@pytest.mark.parametrize("l", [120, 150])
+@pytest.mark.parametrize("l", [120, 150, 192, 230])
 def test_cholqr_inplace_factor_bitwise_equals_global_path(tmp_path, l):
     """The shared-memory in-place factor (104 < l <= 158) reproduces the
     global-memory kernel bit for bit, dead column included."""
