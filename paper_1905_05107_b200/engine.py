@@ -104,6 +104,11 @@ SPEC_MAX_N = 256
 #: 32-64: 51.2-51.4 ms vs 52.3 serial)
 LEAK_GRID_CAP = int(__import__("os").environ.get("POD_LEAK_GRID_CAP", "64"))
 
+#: the merge's second projection (merge.py:73-79) factors its nearly
+#: orthonormal W2 with one CholeskyQR pass, the second only when the first
+#: reports a defect > 1e-4 or a shift.  POD_SECOND_PROJ_ONE_PASS=0: always two.
+SECOND_PROJ_ONE_PASS = __import__("os").environ.get("POD_SECOND_PROJ_ONE_PASS", "1") != "0"
+
 #: NN GEMMs whose output a CholeskyQR pass consumes next form its Gram in
 #: their epilogue (pod_gemm_nn_gram, q <= 64) instead of a TN pass over the
 #: output.  POD_NN_GRAM=0 disables.
@@ -226,23 +231,33 @@ class MergeWorkspace:
         rk = None if l <= 64 else dptr(self.Rk)
         fuse = NN_GRAM and ctx.nn_gram_ok(l, l)
         have_gram = gram_ready
+        # second projection (first_gate set, merge.py:76): W2 = Q - U1 C is
+        # orthonormal to ~1e-8, where ONE CholeskyQR pass is already exact to
+        # working precision (error ~ kappa^2 u) -- pass 0 writes Q directly and
+        # pass 1 runs (in place) only when pass 0's scaled Gram was off the
+        # identity by more than 1e-4 or needed a shift, like passes >= 2
+        one = first_gate is not None and SECOND_PROJ_ONE_PASS
         for p in range(2):  # CholeskyQR2: Wsrc -> tmp -> Q
-            dst = tmp if p == 0 else Q
+            dst = (Q if one else tmp) if p == 0 else Q
+            gp = g0 if (p == 0 or not one) else self.gate(gate_base + 1)
             if not have_gram:
-                ctx.tn(l, l, 1.0, src, src, dptr(self.Gq), r, gate=g0, tag="tn_cholqr_gram")
+                ctx.tn(l, l, 1.0, src, src, dptr(self.Gq), r, gate=gp, tag="tn_cholqr_gram")
             if sharded:
                 self.comm.allreduce_sum_(self.Gq)
             ctx.cholqr_factor_acc(dptr(self.Gq), r, l, src.m, dptr(self.Rinv), r,
                                   dptr(Rout) if p == 0 else rk, r,
                                   None if p == 0 else dptr(Rout), r,
-                                  gate_in=g0, gate_out=self.gate(gate_base + p + 1),
-                                  first_pass=1 if p == 0 else 0)
-            if p == 0 and fuse:  # the apply also forms pass 1's Gram
-                ctx.nn_gram(l, l, 1.0, src, dptr(self.Rinv), r, dst, dptr(self.Gq), r, gate=g0,
+                                  gate_in=gp, gate_out=self.gate(gate_base + p + 1),
+                                  first_pass=1 if (p == 0 and not one) else 0)
+            if p == 1 and one and l > NN_INPLACE_MAX_Q:  # in place through the scratch block
+                ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, tmp, gate=gp, tag="nn_cholqr_apply")
+                ctx.small_copy(Q.m, l, tmp.ptr, tmp.ld, Q.ptr, Q.ld, gate=gp)
+            elif p == 0 and fuse:  # the apply also forms pass 1's Gram
+                ctx.nn_gram(l, l, 1.0, src, dptr(self.Rinv), r, dst, dptr(self.Gq), r, gate=gp,
                             tag="nn_cholqr_apply")
                 have_gram = True
             else:
-                ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, dst, gate=g0, tag="nn_cholqr_apply")
+                ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, dst, gate=gp, tag="nn_cholqr_apply")
                 have_gram = False
             src = dst
         for p in range(2, CHOLQR_PASSES):
