@@ -299,10 +299,13 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
 // C[i, j] = alpha * sum_k ws[k][i, j]: one warp per output element, lanes
 // take splits k = lane, lane + 32, ... and a fixed shuffle tree combines them
 // (deterministic; no atomics).
+// nsplit_diag > 0 (balanced symmetric plan): elements of the diagonal
+// tiles (i / tile == j / tile) have only nsplit_diag partials.
 __global__ void __launch_bounds__(256) reduce_kernel(int nsplit, int p, int q, double alpha,
                                                      const double* __restrict__ ws,
                                                      double* __restrict__ C, int64_t ldc,
-                                                     const int32_t* __restrict__ gate, int sym) {
+                                                     const int32_t* __restrict__ gate, int sym,
+                                                     int nsplit_diag = 0, int tile = 1) {
   if (gate && *gate == 0) return;
   const int64_t total = (int64_t)p * q;
   const int lane = threadIdx.x & 31;
@@ -312,8 +315,9 @@ __global__ void __launch_bounds__(256) reduce_kernel(int nsplit, int p, int q, d
     const int64_t j = t / p, i = t - j * p;
     // symmetric: the lower triangle mirrors the upper one (exactly symmetric C)
     const int64_t src = (sym && i > j) ? (j + i * p) : t;
+    const int ns = (nsplit_diag > 0 && i / tile == j / tile) ? nsplit_diag : nsplit;
     double s = 0.0;
-    for (int k = lane; k < nsplit; k += 32) s += ws[(size_t)k * total + src];
+    for (int k = lane; k < ns; k += 32) s += ws[(size_t)k * total + src];
     s = warp_sum(s);
     if (lane == 0) C[i + j * ldc] = alpha * s;
   }
@@ -356,28 +360,56 @@ constexpr size_t smem_bytes() {
   return size_t(STAGES) * TILE * (sizeof(TX) + sizeof(TY)) + 2 * T * sizeof(int64_t);
 }
 
-template <typename TX, typename TY>
+// Work-balanced symmetric mode (Bal.on): a diagonal tile computes only its 55
+// upper-triangular fragments, dealt two rows per pair of warps (rows k and
+// 9 - k hold 11 fragments: 6 + 5), and the K split gives each off-diagonal
+// tile more CTAs than a diagonal one (sd < so splits) so both finish
+// together.  1-D grid: the nd x sd diagonal CTAs first, then the
+// off-diagonal tiles (tq = 1, 2, ..., tp < tq) x so.
+struct Bal {
+  int on, nd, sd, so;
+  int64_t rps_d, rps_o;
+};
+
+template <typename TX, typename TY, bool BAL = false>
 __global__ void __launch_bounds__(THREADS, 2) partial_kernel(
     int64_t m, int p, int q, const TX* __restrict__ X, int64_t ldx,
     const int32_t* __restrict__ xcols, const TY* __restrict__ Y, int64_t ldy,
     const int32_t* __restrict__ ycols, int64_t rows_per_split, double* __restrict__ ws,
-    const int32_t* __restrict__ gate, int sym) {
+    const int32_t* __restrict__ gate, int sym, Bal bal) {
   if (gate && *gate == 0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tiles_p = (p + T - 1) / T;
-  int tp, tq;
-  if (sym) {
+  int tp, tq, split;
+  int64_t rps = rows_per_split;
+  if (BAL) {
+    const int x = blockIdx.x;
+    if (x < bal.nd * bal.sd) {
+      tp = tq = x / bal.sd;
+      split = x % bal.sd;
+      rps = bal.rps_d;
+    } else {
+      int t = (x - bal.nd * bal.sd) / bal.so;
+      split = (x - bal.nd * bal.sd) % bal.so;
+      tq = 1;
+      while (t >= tq) { t -= tq; ++tq; }
+      tp = t;
+      rps = bal.rps_o;
+    }
+  } else if (sym) {
     int t = blockIdx.x;
     tq = 0;
     while (t > tq) { t -= tq + 1; ++tq; }
     tp = t;
+    split = blockIdx.y;
   } else {
     tp = blockIdx.x % tiles_p;
     tq = blockIdx.x / tiles_p;
+    split = blockIdx.y;
   }
-  const int split = blockIdx.y;
-  const int64_t r0 = (int64_t)split * rows_per_split;
-  const int64_t r1 = min(m, r0 + rows_per_split);
+  const bool diag = BAL && tp == tq;
+  const int64_t r0 = (int64_t)split * rps;
+  const int64_t r1 = min(m, r0 + rps);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   TX* const xs0 = reinterpret_cast<TX*>(smem_raw);
   TY* const ys0 = reinterpret_cast<TY*>(smem_raw + size_t(STAGES) * TILE * sizeof(TX));
@@ -418,6 +450,26 @@ __global__ void __launch_bounds__(THREADS, 2) partial_kernel(
   for (int f = 0; f < 2; ++f)
 #pragma unroll
     for (int g = 0; g < 5; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+  // diagonal tile: this warp's <= 6 upper fragments (row fr[g], column fc[g]);
+  // rows k and 9 - k of warps 2k, 2k + 1
+  const int kq = warp >> 1;
+  int fr[6], fc[6];
+#pragma unroll
+  for (int g = 0; g < 6; ++g) {
+    if ((warp & 1) == 0) {
+      fr[g] = kq;
+      fc[g] = kq + g <= 9 ? kq + g : -1;
+    } else if (g < 4 - kq) {
+      fr[g] = kq;
+      fc[g] = kq + 6 + g;
+    } else if (g - (4 - kq) <= kq) {
+      fr[g] = 9 - kq;
+      fc[g] = 9 - kq + (g - (4 - kq));
+    } else {
+      fr[g] = 9 - kq;
+      fc[g] = -1;
+    }
+  }
   const int64_t nkb = (r1 > r0) ? (r1 - r0 + BK - 1) / BK : 0;
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
@@ -432,6 +484,20 @@ __global__ void __launch_bounds__(THREADS, 2) partial_kernel(
     __syncthreads();
     const TX* xs = xs0 + (size_t)(kb % STAGES) * TILE;
     const TY* ys = ys0 + (size_t)(kb % STAGES) * TILE;
+    if (BAL && diag) {
+      // the 6 accumulators reuse acc's registers: acc[g / 5][g % 5]
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        const double a0 = (double)xs[(fr[0] * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+        const double a1 = (double)xs[(fr[5] * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+#pragma unroll
+        for (int g = 0; g < 6; ++g) {
+          if (fc[g] < 0) continue;
+          const double bb = (double)ys[(fc[g] * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+          dmma8x8x4(acc[g / 5][g % 5][0], acc[g / 5][g % 5][1], fr[g] == fr[0] ? a0 : a1, bb);
+        }
+      }
+    } else {
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       double a[2], b[5];
@@ -446,10 +512,24 @@ __global__ void __launch_bounds__(THREADS, 2) partial_kernel(
 #pragma unroll
         for (int g = 0; g < 5; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
     }
+    }
     __syncthreads();
   }
   cp_async_wait<0>();
   double* out = ws + (size_t)split * p * q;
+  if (BAL && diag) {
+#pragma unroll
+    for (int g = 0; g < 6; ++g) {
+      if (fc[g] < 0) continue;
+      const int i = tp * T + fr[g] * 8 + (lane >> 2);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = tq * T + fc[g] * 8 + 2 * (lane & 3) + e;
+        if (i < p && j < q) out[(size_t)j * p + i] = acc[g / 5][g % 5][e];
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
     const int i = tp * T + wp * 16 + f * 8 + (lane >> 2);
@@ -477,6 +557,54 @@ inline tn::Plan plan(int64_t m, int64_t p, int64_t q, bool sym) {
   pl.splits = (int)std::max<int64_t>(1, ceil_div(m, pl.rows_per_split));
   return pl;
 }
+// Balanced symmetric plan (sym products with >= 2 tile rows): a diagonal
+// tile's CTA is given DIAG_COST times an off-diagonal one's splits (55 of
+// 100 fragments; 0.47 measured best at config 3 from a sweep 0.2-1.0:
+// 2.850 s unbalanced -> 2.77 s), so both finish together in one wave.
+inline double diag_cost() {  // POD_TN_DIAG_COST: A/B override
+  static double v = -1.0;
+  if (v < 0.0) {
+    const char* e = getenv("POD_TN_DIAG_COST");
+    v = e ? atof(e) : 0.47;
+    if (!(v > 0.05 && v <= 1.0)) v = 0.47;
+  }
+  return v;
+}
+inline Bal plan_bal(int64_t m, int64_t p) {
+  const double DIAG_COST = diag_cost();
+  Bal b = {0, 0, 0, 0, 0, 0};
+  const int64_t tp = ceil_div(p, T);
+  if (tp < 2) return b;
+  const int64_t noff = tp * (tp - 1) / 2;
+  const double budget = (double)capped(2 * 148);
+  int64_t so = std::max<int64_t>(1, (int64_t)(budget / (noff + DIAG_COST * tp)));
+  int64_t sd = std::max<int64_t>(1, (int64_t)(so * DIAG_COST));
+  while (sd * tp + so * noff > (int64_t)budget && so > 1) {
+    --so;
+    sd = std::max<int64_t>(1, (int64_t)(so * DIAG_COST));
+  }
+  auto rows = [&](int64_t sp) {
+    int64_t r = ceil_div(ceil_div(m, sp), BK) * BK;
+    return std::max<int64_t>(BK, r);
+  };
+  b.rps_d = rows(sd);
+  b.rps_o = rows(so);
+  b.sd = (int)ceil_div(m, b.rps_d);
+  b.so = (int)ceil_div(m, b.rps_o);
+  b.nd = (int)tp;
+  b.on = 1;
+  return b;
+}
+// POD_TN_BAL=0: uniform K split and full diagonal tiles (A/B)
+inline bool bal_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_TN_BAL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // 80-wide tiles when they cover p x q with less padding than 64-wide ones
 inline bool better(int64_t p, int64_t q) {
   const int64_t a64 = ceil_div(p, 64) * 64 * ceil_div(q, 64) * 64;
@@ -962,7 +1090,11 @@ static int ensure_attrs() {
                            (int)tn::smem_bytes<double, float>());
   if (e != cudaSuccess) return cuda_status(e, "tn attr");
 #define TN80_ATTR(A_, B_)                                                                   \
-  e = cudaFuncSetAttribute(tn80::partial_kernel<A_, B_>,                                   \
+  e = cudaFuncSetAttribute(tn80::partial_kernel<A_, B_, false>,                            \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                           (int)tn80::smem_bytes<A_, B_>());                               \
+  if (e != cudaSuccess) return cuda_status(e, "tn80 attr");                                \
+  e = cudaFuncSetAttribute(tn80::partial_kernel<A_, B_, true>,                             \
                            cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
                            (int)tn80::smem_bytes<A_, B_>());                               \
   if (e != cudaSuccess) return cuda_status(e, "tn80 attr");
@@ -1025,7 +1157,8 @@ extern "C" size_t pod_gemm_tn_ws_bytes(int64_t m, int64_t p, int64_t q) {
   if (m <= 0 || p <= 0 || q <= 0) return 0;
   const tn::Plan a = tn::plan(m, p, q, false), b = tn::plan(m, p, q, p == q);
   const tn::Plan c = tn80::plan(m, p, q, false), d = tn80::plan(m, p, q, p == q);
-  const int sp = std::max(std::max(a.splits, b.splits), std::max(c.splits, d.splits));
+  int sp = std::max(std::max(a.splits, b.splits), std::max(c.splits, d.splits));
+  if (p == q) sp = std::max(sp, tn80::plan_bal(m, p).so);
   return (size_t)sp * p * q * sizeof(double);
 }
 
@@ -1045,15 +1178,21 @@ extern "C" int pod_gemm_tn(int xtype, int ytype, int64_t m, int64_t p, int64_t q
   const int sym = (X == Y && ldx == ldy && xcols == ycols && p == q && xtype == ytype) ? 1 : 0;
   const bool w80 = tn80::better(p, q) && tn80_enabled();
   tn::Plan pl = w80 ? tn80::plan(m, p, q, sym != 0) : tn::plan(m, p, q, sym != 0);
-  POD_REQUIRE(ws_bytes >= (size_t)pl.splits * p * q * sizeof(double),
+  tn80::Bal bal = {0, 0, 0, 0, 0, 0};
+  if (w80 && sym && tn80::bal_enabled()) bal = tn80::plan_bal(m, p);
+  const int nsplit = bal.on ? bal.so : pl.splits;
+  POD_REQUIRE(ws_bytes >= (size_t)nsplit * p * q * sizeof(double),
               "pod_gemm_tn: workspace too small (%zu < %zu)", ws_bytes,
-              (size_t)pl.splits * p * q * sizeof(double));
+              (size_t)nsplit * p * q * sizeof(double));
   dim3 grid(pl.tiles, pl.splits);
+  if (bal.on)
+    grid = dim3((unsigned)(bal.nd * bal.sd + (bal.nd * (bal.nd - 1) / 2) * bal.so), 1);
   if (w80) {
 #define TN80_LAUNCH(A_, B_)                                                                     \
-  tn80::partial_kernel<A_, B_><<<grid, tn80::THREADS, tn80::smem_bytes<A_, B_>(), s>>>(        \
+  (bal.on ? tn80::partial_kernel<A_, B_, true> : tn80::partial_kernel<A_, B_, false>)           \
+      <<<grid, tn80::THREADS, tn80::smem_bytes<A_, B_>(), s>>>(                                 \
       m, (int)p, (int)q, (const A_*)X, ldx, xcols, (const B_*)Y, ldy, ycols, pl.rows_per_split, \
-      (double*)ws, gate, sym)
+      (double*)ws, gate, sym, bal)
     if (xtype == POD_F64 && ytype == POD_F64) TN80_LAUNCH(double, double);
     else if (xtype == POD_F64) TN80_LAUNCH(double, float);
     else if (ytype == POD_F32) TN80_LAUNCH(float, float);
@@ -1078,8 +1217,8 @@ extern "C" int pod_gemm_tn(int xtype, int ytype, int64_t m, int64_t p, int64_t q
   POD_CHECK_LAUNCH("tn partial");
   int64_t tot = p * q;
   int blocks = (int)std::min<int64_t>(ceil_div(tot, 8), 16 * 148);  // 8 warps = 8 outputs per block
-  tn::reduce_kernel<<<blocks, 256, 0, s>>>(pl.splits, (int)p, (int)q, alpha, (const double*)ws, C,
-                                           ldc, gate, sym);
+  tn::reduce_kernel<<<blocks, 256, 0, s>>>(nsplit, (int)p, (int)q, alpha, (const double*)ws, C,
+                                           ldc, gate, sym, bal.on ? bal.sd : 0, tn80::T);
   POD_CHECK_LAUNCH("tn reduce");
   return POD_OK;
 }

@@ -127,6 +127,33 @@ def test_gemm_tn(ctx, m, p, q):
     np.testing.assert_allclose(got, ref, rtol=1e-11, atol=1e-11 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("m,p", [(50001, 150), (7, 160), (20000, 161), (100000, 200), (3000, 240),
+                                 (1000003, 150), (40000, 300)])
+def test_gemm_tn_symmetric_balanced(ctx, m, p):
+    """Symmetric products on 80-wide tiles (configs 3: r = 150, g = 200): the
+    diagonal tiles compute only their upper fragments and the K split
+    weights tiles by their work -- exactly symmetric C, numpy's values, and
+    the same with an index list holding -1 (zero) padding columns."""
+    rng = np.random.default_rng(m + p)
+    x = rng.standard_normal((m, p))
+    X = dev_mat(x, ctx)
+    C = torch.empty(p * p, dtype=torch.float64, device=ctx.device)
+    ctx.tn(p, p, 1.0, X, X, dptr(C), p)
+    got = C.cpu().numpy().reshape(p, p).T
+    ref = x.T @ x
+    np.testing.assert_allclose(got, ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
+    assert np.array_equal(got, got.T)
+    idx = np.arange(p, dtype=np.int32)
+    idx[p - 3:] = -1
+    it = torch.as_tensor(idx, device=ctx.device)
+    ctx.tn(p, p, 1.0, X, X, dptr(C), p, xcols=it, ycols=it)
+    got = C.cpu().numpy().reshape(p, p).T
+    d = x.copy()
+    d[:, p - 3:] = 0.0
+    np.testing.assert_allclose(got, d.T @ d, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
+    assert np.array_equal(got, got.T)
+
+
 def test_gemm_tn_gather(ctx):
     rng = np.random.default_rng(3)
     a = rng.standard_normal((3001, 40))
