@@ -143,6 +143,12 @@ static inline int64_t capped(int64_t ctas) {
 
 // ---------------------------------------------------------------- TN ------
 namespace tn {
+// balanced symmetric launch (see tn80): nd diagonal tiles x sd splits, then
+// the off-diagonal tiles x so splits, with their own rows per split
+struct Bal {
+  int on, nd, sd, so;
+  int64_t rps_d, rps_o;
+};
 constexpr int BP = 64, BQ = 64, BK = 32, LDS = BK + 4;  // LDS % 16 == 4: conflict-free frags
 constexpr int THREADS = 256;
 constexpr int STAGES = 3;
@@ -160,28 +166,45 @@ __device__ __forceinline__ const T* colptr(const T* base, int64_t ld, const int3
   return base + (cols ? (int64_t)cols[c] : (int64_t)c) * ld;
 }
 
-template <typename TX, typename TY>
+template <typename TX, typename TY, bool BAL = false>
 __global__ void __launch_bounds__(THREADS) partial_kernel(
     int64_t m, int p, int q, const TX* __restrict__ X, int64_t ldx,
     const int32_t* __restrict__ xcols, const TY* __restrict__ Y, int64_t ldy,
     const int32_t* __restrict__ ycols, int64_t rows_per_split, double* __restrict__ ws,
-    const int32_t* __restrict__ gate, int sym) {
+    const int32_t* __restrict__ gate, int sym, Bal bal = Bal{0, 0, 0, 0, 0, 0}) {
   if (gate && *gate == 0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tiles_p = (p + BP - 1) / BP;
-  int tp, tq;
-  if (sym) {  // symmetric product (X == Y): upper-triangular tiles tp <= tq only
+  int tp, tq, split;
+  int64_t rps = rows_per_split;
+  if (BAL) {
+    const int x = blockIdx.x;
+    if (x < bal.nd * bal.sd) {
+      tp = tq = x / bal.sd;
+      split = x % bal.sd;
+      rps = bal.rps_d;
+    } else {
+      int t = (x - bal.nd * bal.sd) / bal.so;
+      split = (x - bal.nd * bal.sd) % bal.so;
+      tq = 1;
+      while (t >= tq) { t -= tq; ++tq; }
+      tp = t;
+      rps = bal.rps_o;
+    }
+  } else if (sym) {  // symmetric product (X == Y): upper-triangular tiles tp <= tq only
     int t = blockIdx.x;
     tq = 0;
     while (t > tq) { t -= tq + 1; ++tq; }
     tp = t;
+    split = blockIdx.y;
   } else {
     tp = blockIdx.x % tiles_p;
     tq = blockIdx.x / tiles_p;
+    split = blockIdx.y;
   }
-  const int split = blockIdx.y;
-  const int64_t r0 = (int64_t)split * rows_per_split;
-  const int64_t r1 = min(m, r0 + rows_per_split);
+  const bool diag = BAL && tp == tq;
+  const int64_t r0 = (int64_t)split * rps;
+  const int64_t r1 = min(m, r0 + rps);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   // fp64 operands move row PAIRS with 16-byte copies: thread -> columns
@@ -249,6 +272,26 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
   for (int f = 0; f < 4; ++f)
 #pragma unroll
     for (int g = 0; g < 2; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+  // diagonal tile (BAL): this warp's <= 5 of the 36 upper fragments, rows k
+  // and 7 - k (9 fragments) dealt over warps 2k (5) and 2k + 1 (4)
+  const int kq = warp >> 1;
+  int fr[5], fc[5];
+#pragma unroll
+  for (int g = 0; g < 5; ++g) {
+    if ((warp & 1) == 0) {
+      fr[g] = kq;
+      fc[g] = kq + g;
+    } else if (g < 3 - kq) {
+      fr[g] = kq;
+      fc[g] = kq + 5 + g;
+    } else if (g - (3 - kq) <= kq) {
+      fr[g] = 7 - kq;
+      fc[g] = 7 - kq + (g - (3 - kq));
+    } else {
+      fr[g] = 7 - kq;
+      fc[g] = -1;
+    }
+  }
 
   const int64_t nkb = (r1 > r0) ? (r1 - r0 + BK - 1) / BK : 0;
 #pragma unroll
@@ -264,6 +307,19 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
     __syncthreads();
     const TX* xs = xs0 + (size_t)(kb % STAGES) * TILE_DBL;
     const TY* ys = ys0 + (size_t)(kb % STAGES) * TILE_DBL;
+    if (BAL && diag) {  // accumulators acc[g / 2][g % 2], g < 5
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        const double a0 = (double)xs[(fr[0] * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+        const double a1 = (double)xs[(fr[4] * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+#pragma unroll
+        for (int g = 0; g < 5; ++g) {
+          if (fc[g] < 0) continue;
+          const double bb = (double)ys[(fc[g] * 8 + (lane >> 2)) * LDS + kk * 4 + (lane & 3)];
+          dmma8x8x4(acc[g / 2][g % 2][0], acc[g / 2][g % 2][1], fr[g] == fr[0] ? a0 : a1, bb);
+        }
+      }
+    } else {
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       double a[4], b[2];
@@ -278,11 +334,25 @@ __global__ void __launch_bounds__(THREADS) partial_kernel(
 #pragma unroll
         for (int g = 0; g < 2; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
     }
+    }
     __syncthreads();
   }
   cp_async_wait<0>();
 
   double* out = ws + (size_t)split * p * q;
+  if (BAL && diag) {
+#pragma unroll
+    for (int g = 0; g < 5; ++g) {
+      if (fc[g] < 0) continue;
+      const int i = tp * BP + fr[g] * 8 + (lane >> 2);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int j = tq * BQ + fc[g] * 8 + 2 * (lane & 3) + e;
+        if (i < p && j < q) out[(size_t)j * p + i] = acc[g / 2][g % 2][e];
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int f = 0; f < 4; ++f) {
     const int i = tp * BP + wp * 32 + f * 8 + (lane >> 2);
@@ -366,10 +436,7 @@ constexpr size_t smem_bytes() {
 // tile more CTAs than a diagonal one (sd < so splits) so both finish
 // together.  1-D grid: the nd x sd diagonal CTAs first, then the
 // off-diagonal tiles (tq = 1, 2, ..., tp < tq) x so.
-struct Bal {
-  int on, nd, sd, so;
-  int64_t rps_d, rps_o;
-};
+using Bal = tn::Bal;
 
 template <typename TX, typename TY, bool BAL = false>
 __global__ void __launch_bounds__(THREADS, 2) partial_kernel(
@@ -561,17 +628,17 @@ inline tn::Plan plan(int64_t m, int64_t p, int64_t q, bool sym) {
 // tile's CTA is given DIAG_COST times an off-diagonal one's splits (55 of
 // 100 fragments; 0.47 measured best at config 3 from a sweep 0.2-1.0:
 // 2.850 s unbalanced -> 2.77 s), so both finish together in one wave.
+inline double env_cost(const char* name, double dflt) {
+  const char* e = getenv(name);
+  const double v = e ? atof(e) : dflt;
+  return (v > 0.05 && v <= 1.0) ? v : dflt;
+}
 inline double diag_cost() {  // POD_TN_DIAG_COST: A/B override
   static double v = -1.0;
-  if (v < 0.0) {
-    const char* e = getenv("POD_TN_DIAG_COST");
-    v = e ? atof(e) : 0.47;
-    if (!(v > 0.05 && v <= 1.0)) v = 0.47;
-  }
+  if (v < 0.0) v = env_cost("POD_TN_DIAG_COST", 0.47);
   return v;
 }
-inline Bal plan_bal(int64_t m, int64_t p) {
-  const double DIAG_COST = diag_cost();
+inline Bal plan_bal_t(int64_t m, int64_t p, int T, int BK, double DIAG_COST) {
   Bal b = {0, 0, 0, 0, 0, 0};
   const int64_t tp = ceil_div(p, T);
   if (tp < 2) return b;
@@ -594,6 +661,24 @@ inline Bal plan_bal(int64_t m, int64_t p) {
   b.nd = (int)tp;
   b.on = 1;
   return b;
+}
+inline Bal plan_bal(int64_t m, int64_t p) { return plan_bal_t(m, p, T, BK, diag_cost()); }
+// the 64-wide kernel's diagonal tiles (36 of 64 fragments): opt-in
+// (POD_TN_BAL64=1, weight POD_TN_DIAG_COST64).  Measured at config 4
+// (r = 192, g = 256): weights 0.75-0.9 tie the unbalanced 1.377 s, 0.6 and
+// 1.0 lose -- its leak check sits at the 1e-8 threshold, so the summation
+// order of the Grams moves the second-projection count more than the
+// balancing saves.
+inline Bal plan_bal64(int64_t m, int64_t p) {
+  static int on = -1;
+  static double v = -1.0;
+  if (on < 0) {
+    const char* e = getenv("POD_TN_BAL64");
+    on = (e && e[0] == '1') ? 1 : 0;
+    v = env_cost("POD_TN_DIAG_COST64", 0.9);
+  }
+  if (!on) return Bal{0, 0, 0, 0, 0, 0};
+  return plan_bal_t(m, p, tn::BP, tn::BK, v);
 }
 // POD_TN_BAL=0: uniform K split and full diagonal tiles (A/B)
 inline bool bal_enabled() {
@@ -1089,6 +1174,16 @@ static int ensure_attrs() {
                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tn::smem_bytes<double, float>());
   if (e != cudaSuccess) return cuda_status(e, "tn attr");
+#define TN64_BAL_ATTR(A_, B_)                                                              \
+  e = cudaFuncSetAttribute(tn::partial_kernel<A_, B_, true>,                               \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                           (int)tn::smem_bytes<A_, B_>());                                 \
+  if (e != cudaSuccess) return cuda_status(e, "tn bal attr");
+  TN64_BAL_ATTR(double, double)
+  TN64_BAL_ATTR(float, float)
+  TN64_BAL_ATTR(float, double)
+  TN64_BAL_ATTR(double, float)
+#undef TN64_BAL_ATTR
 #define TN80_ATTR(A_, B_)                                                                   \
   e = cudaFuncSetAttribute(tn80::partial_kernel<A_, B_, false>,                            \
                            cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
@@ -1158,7 +1253,7 @@ extern "C" size_t pod_gemm_tn_ws_bytes(int64_t m, int64_t p, int64_t q) {
   const tn::Plan a = tn::plan(m, p, q, false), b = tn::plan(m, p, q, p == q);
   const tn::Plan c = tn80::plan(m, p, q, false), d = tn80::plan(m, p, q, p == q);
   int sp = std::max(std::max(a.splits, b.splits), std::max(c.splits, d.splits));
-  if (p == q) sp = std::max(sp, tn80::plan_bal(m, p).so);
+  if (p == q) sp = std::max(sp, std::max(tn80::plan_bal(m, p).so, tn80::plan_bal64(m, p).so));
   return (size_t)sp * p * q * sizeof(double);
 }
 
@@ -1179,7 +1274,7 @@ extern "C" int pod_gemm_tn(int xtype, int ytype, int64_t m, int64_t p, int64_t q
   const bool w80 = tn80::better(p, q) && tn80_enabled();
   tn::Plan pl = w80 ? tn80::plan(m, p, q, sym != 0) : tn::plan(m, p, q, sym != 0);
   tn80::Bal bal = {0, 0, 0, 0, 0, 0};
-  if (w80 && sym && tn80::bal_enabled()) bal = tn80::plan_bal(m, p);
+  if (sym && tn80::bal_enabled()) bal = w80 ? tn80::plan_bal(m, p) : tn80::plan_bal64(m, p);
   const int nsplit = bal.on ? bal.so : pl.splits;
   POD_REQUIRE(ws_bytes >= (size_t)nsplit * p * q * sizeof(double),
               "pod_gemm_tn: workspace too small (%zu < %zu)", ws_bytes,
@@ -1198,27 +1293,24 @@ extern "C" int pod_gemm_tn(int xtype, int ytype, int64_t m, int64_t p, int64_t q
     else if (ytype == POD_F32) TN80_LAUNCH(float, float);
     else TN80_LAUNCH(float, double);
 #undef TN80_LAUNCH
-  } else if (xtype == POD_F64 && ytype == POD_F64)
-    tn::partial_kernel<double, double><<<grid, tn::THREADS, tn::SMEM, s>>>(
-        m, (int)p, (int)q, (const double*)X, ldx, xcols, (const double*)Y, ldy, ycols,
-        pl.rows_per_split, (double*)ws, gate, sym);
-  else if (xtype == POD_F64)
-    tn::partial_kernel<double, float><<<grid, tn::THREADS, tn::smem_bytes<double, float>(), s>>>(
-        m, (int)p, (int)q, (const double*)X, ldx, xcols, (const float*)Y, ldy, ycols,
-        pl.rows_per_split, (double*)ws, gate, sym);
-  else if (ytype == POD_F32)
-    tn::partial_kernel<float, float><<<grid, tn::THREADS, tn::smem_bytes<float, float>(), s>>>(
-        m, (int)p, (int)q, (const float*)X, ldx, xcols, (const float*)Y, ldy, ycols,
-        pl.rows_per_split, (double*)ws, gate, sym);
-  else
-    tn::partial_kernel<float, double><<<grid, tn::THREADS, tn::smem_bytes<float, double>(), s>>>(
-        m, (int)p, (int)q, (const float*)X, ldx, xcols, (const double*)Y, ldy, ycols,
-        pl.rows_per_split, (double*)ws, gate, sym);
+  } else {
+#define TN64_LAUNCH(A_, B_)                                                                     \
+  (bal.on ? tn::partial_kernel<A_, B_, true> : tn::partial_kernel<A_, B_, false>)               \
+      <<<grid, tn::THREADS, tn::smem_bytes<A_, B_>(), s>>>(                                     \
+      m, (int)p, (int)q, (const A_*)X, ldx, xcols, (const B_*)Y, ldy, ycols, pl.rows_per_split, \
+      (double*)ws, gate, sym, bal)
+    if (xtype == POD_F64 && ytype == POD_F64) TN64_LAUNCH(double, double);
+    else if (xtype == POD_F64) TN64_LAUNCH(double, float);
+    else if (ytype == POD_F32) TN64_LAUNCH(float, float);
+    else TN64_LAUNCH(float, double);
+#undef TN64_LAUNCH
+  }
   POD_CHECK_LAUNCH("tn partial");
   int64_t tot = p * q;
   int blocks = (int)std::min<int64_t>(ceil_div(tot, 8), 16 * 148);  // 8 warps = 8 outputs per block
   tn::reduce_kernel<<<blocks, 256, 0, s>>>(nsplit, (int)p, (int)q, alpha, (const double*)ws, C,
-                                           ldc, gate, sym, bal.on ? bal.sd : 0, tn80::T);
+                                           ldc, gate, sym, bal.on ? bal.sd : 0,
+                                           w80 ? tn80::T : tn::BP);
   POD_CHECK_LAUNCH("tn reduce");
   return POD_OK;
 }

@@ -128,12 +128,14 @@ def test_gemm_tn(ctx, m, p, q):
 
 
 @pytest.mark.parametrize("m,p", [(50001, 150), (7, 160), (20000, 161), (100000, 200), (3000, 240),
-                                 (1000003, 150), (40000, 300)])
+                                 (1000003, 150), (40000, 300), (60001, 192), (20000, 256),
+                                 (5000, 100), (3000, 129), (200000, 128)])
 def test_gemm_tn_symmetric_balanced(ctx, m, p):
-    """Symmetric products on 80-wide tiles (configs 3: r = 150, g = 200): the
-    diagonal tiles compute only their upper fragments and the K split
-    weights tiles by their work -- exactly symmetric C, numpy's values, and
-    the same with an index list holding -1 (zero) padding columns."""
+    """Symmetric products on 80- and 64-wide tiles (config 3: r = 150,
+    g = 200; config 4: 192, 256; config 2: g = 100): the diagonal tiles
+    compute only their upper fragments and the K split weights tiles by
+    their work -- exactly symmetric C, numpy's values, and the same with an
+    index list holding -1 (zero) padding columns."""
     rng = np.random.default_rng(m + p)
     x = rng.standard_normal((m, p))
     X = dev_mat(x, ctx)
