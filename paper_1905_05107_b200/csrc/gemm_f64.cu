@@ -910,8 +910,15 @@ __global__ void __launch_bounds__(THREADS) kernel(int64_t m, int p, int q, doubl
 // so Y may alias X or Z.
 namespace nns {
 constexpr int THREADS = 256;
-constexpr int BK = 16;
-constexpr int LDT = BK + 4;  // T chunk stored [j][k]
+#ifndef POD_NNS_BK80
+#define POD_NNS_BK80 16
+#endif
+#ifndef POD_NNS_MINB
+#define POD_NNS_MINB 1
+#endif
+#ifndef POD_NNS_ST80
+#define POD_NNS_ST80 4
+#endif
 
 #ifndef POD_NN80_WIDE
 #define POD_NN80_WIDE 0
@@ -923,8 +930,10 @@ struct Cfg {
   // 128-row blocks (20 DMMAs per 9 fragment loads instead of 8 per 6)
   static constexpr bool W80 = (BN == 80) && POD_NN80_WIDE;
   static constexpr int NWARP = (BN == 80 && !W80) ? 10 : 8;
+  static constexpr int BK = BN == 80 ? POD_NNS_BK80 : 16;  // k-chunk per pipeline stage
+  static constexpr int LDT = BK + 4;                         // T chunk stored [j][k]
   static constexpr int NTHREADS = NWARP * 32;
-  static constexpr int STAGES = (BN == 128 || W80) ? 3 : 4;
+  static constexpr int STAGES = (BN == 128 || W80) ? 3 : (BN == 80 ? POD_NNS_ST80 : 4);
   static constexpr int BM = (BN == 64 || W80) ? 128 : 64;  // rows per block (T reuse)
   // X chunk stored [k][row] in X's own type (fp32 storage converted exactly
   // at the fragment loads); padding keeps the fragment loads conflict-free
@@ -942,7 +951,7 @@ struct Cfg {
 // columns of a row block while another group may still be reading X there).
 
 template <int BN, typename TX = double, bool DOTS = false>
-__global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p, int q,
+__global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS, POD_NNS_MINB) kernel(int64_t m, int p, int q,
                                                                  double alpha,
                                                   const TX* X, int64_t ldx,
                                                   const int32_t* __restrict__ xcols,
@@ -975,7 +984,7 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p
     q = min(BN, q - q0);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nkb = (p + BK - 1) / BK;
+  const int nkb = (p + C::BK - 1) / C::BK;
   const int64_t nblk = (m + C::BM - 1) / C::BM;
   const int64_t G = gridDim.x;
   if ((int64_t)blockIdx.x >= nblk) {
@@ -993,14 +1002,14 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p
   auto load_stage = [&](int st) {
     TX* xs = stage_x(st);
     double* ts = stage_t(st);
-    const int k0 = l_kb * BK;
+    const int k0 = l_kb * C::BK;
     const int64_t r0 = l_r0;
     if (++l_kb == nkb) {
       l_kb = 0;
       l_r0 += G * C::BM;
     }
-    // X: C::BM rows x BK cols as row pairs (2 x 8 B)
-    for (int e = threadIdx.x; e < BK * (C::BM / 2); e += C::NTHREADS) {
+    // X: C::BM rows x C::BK cols as row pairs (2 x 8 B)
+    for (int e = threadIdx.x; e < C::BK * (C::BM / 2); e += C::NTHREADS) {
       const int cl = e / (C::BM / 2), i2 = (e - cl * (C::BM / 2)) * 2;
       const int c = k0 + cl;
       const int64_t row = r0 + i2;
@@ -1020,12 +1029,12 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p
         cp_async_elem(dst + 1, cv && row + 1 < m ? src + 1 : X, cv && row + 1 < m);
       }
     }
-    // T: rows k0..k0+BK, all BN cols, k pairs
-    for (int e = threadIdx.x; e < BN * (BK / 2); e += C::NTHREADS) {
-      const int j = e / (BK / 2), k2 = (e - j * (BK / 2)) * 2;
+    // T: rows k0..k0+C::BK, all BN cols, k pairs
+    for (int e = threadIdx.x; e < BN * (C::BK / 2); e += C::NTHREADS) {
+      const int j = e / (C::BK / 2), k2 = (e - j * (C::BK / 2)) * 2;
       const int k = k0 + k2;
       const bool jv = j < q;
-      double* dst = ts + j * LDT + k2;
+      double* dst = ts + j * C::LDT + k2;
       const double* src = T + k + (int64_t)j * ldT;
       if (jv && vt && k + 1 < p) {
         cp_async16(dst, src, true);
@@ -1068,14 +1077,14 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS) kernel(int64_t m, int p
     if (++st_c == ST) st_c = 0;
 
 #pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
+    for (int kk = 0; kk < C::BK / 4; ++kk) {
       double a[4], b[C::FN];
 #pragma unroll
       for (int f = 0; f < 4; ++f)
         a[f] = (double)xs[(kk * 4 + (lane & 3)) * C::LDX + wm * 32 + f * 8 + (lane >> 2)];
 #pragma unroll
       for (int g = 0; g < C::FN; ++g)
-        b[g] = ts[(wn * (BN / C::WN) + g * 8 + (lane >> 2)) * LDT + kk * 4 + (lane & 3)];
+        b[g] = ts[(wn * (BN / C::WN) + g * 8 + (lane >> 2)) * C::LDT + kk * 4 + (lane & 3)];
 #pragma unroll
       for (int f = 0; f < 4; ++f)
 #pragma unroll
