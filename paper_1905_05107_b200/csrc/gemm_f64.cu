@@ -141,6 +141,30 @@ static inline int64_t capped(int64_t ctas) {
   return g_grid_cap > 0 ? std::max<int64_t>(1, std::min<int64_t>(ctas, g_grid_cap)) : ctas;
 }
 
+// mbarrier helpers of the warp-specialized GEMMs (producer warp -> consumers)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(uint64_t* mb, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(mb)), "r"(count));
+}
+__device__ __forceinline__ void mb_wait(uint64_t* mb, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_addr(mb)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* mb) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(mb)) : "memory");
+}
+__device__ __forceinline__ void mb_cp_async_arrive(uint64_t* mb) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_addr(mb))
+               : "memory");
+}
+
 // ---------------------------------------------------------------- TN ------
 namespace tn {
 // balanced symmetric launch (see tn80): nd diagonal tiles x sd splits, then
@@ -420,14 +444,20 @@ inline Plan plan(int64_t m, int64_t p, int64_t q, bool sym) {
 // (5 along p x 2 along q), warp tile 16 x 40 (2 x 5 fragments), BK = 16 so two
 // CTAs fit an SM; gathered column offsets live in shared memory instead of
 // per-thread pointer registers.
+#ifndef POD_TN_WS_MINB
+#define POD_TN_WS_MINB 2
+#endif
 namespace tn80 {
 constexpr int T = 80, NW = 10, THREADS = NW * 32;
+constexpr int NPROD = 2;  // producer warps of the warp-specialized variant
 constexpr int BK = 16, LDS = BK + 4;  // % 16 == 4: conflict-free fragments
 constexpr int STAGES = 4;
 constexpr int TILE = T * LDS;
 template <typename TX, typename TY>
 constexpr size_t smem_bytes() {
-  return size_t(STAGES) * TILE * (sizeof(TX) + sizeof(TY)) + 2 * T * sizeof(int64_t);
+  // + the warp-specialized variant's full / empty mbarriers
+  return size_t(STAGES) * TILE * (sizeof(TX) + sizeof(TY)) + 2 * T * sizeof(int64_t) +
+         2 * STAGES * sizeof(uint64_t);
 }
 
 // Work-balanced symmetric mode (Bal.on): a diagonal tile computes only its 55
@@ -438,8 +468,8 @@ constexpr size_t smem_bytes() {
 // off-diagonal tiles (tq = 1, 2, ..., tp < tq) x so.
 using Bal = tn::Bal;
 
-template <typename TX, typename TY, bool BAL = false>
-__global__ void __launch_bounds__(THREADS, 2) partial_kernel(
+template <typename TX, typename TY, bool BAL = false, bool WS = false>
+__global__ void __launch_bounds__(WS ? THREADS + NPROD * 32 : THREADS, WS ? POD_TN_WS_MINB : 2) partial_kernel(
     int64_t m, int p, int q, const TX* __restrict__ X, int64_t ldx,
     const int32_t* __restrict__ xcols, const TY* __restrict__ Y, int64_t ldy,
     const int32_t* __restrict__ ycols, int64_t rows_per_split, double* __restrict__ ws,
@@ -495,6 +525,15 @@ __global__ void __launch_bounds__(THREADS, 2) partial_kernel(
     }
     (isx ? xoff : yoff)[cc] = off;
   }
+  uint64_t* const full = reinterpret_cast<uint64_t*>(yoff + T);
+  uint64_t* const empty = full + STAGES;
+  if (WS && threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mb_init(&full[s], NPROD * 32);
+      mb_init(&empty[s], NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
   // loader: warp w moves rows rb + lane of columns w, w + 10, ... (8 each)
   auto load_stage = [&](int st, int64_t rb) {
@@ -538,17 +577,81 @@ __global__ void __launch_bounds__(THREADS, 2) partial_kernel(
     }
   }
   const int64_t nkb = (r1 > r0) ? (r1 - r0 + BK - 1) / BK : 0;
+  if constexpr (WS) {
+    if (warp >= NW) {
+      // NPROD producer warps: thread t owns row pair t % 8 of columns
+      // t / 8 + (NPT * i), i < 80 / NPT, of both tiles, their offsets held in
+      // registers; 16-byte copies for fp64 on full aligned stages, each
+      // thread's copies completing on the stage's full barrier
+      constexpr int NPT = NPROD * 32 / (BK / 2);  // columns covered per sweep
+      constexpr int CPT = T / NPT;                // columns per thread
+      const int t = threadIdx.x - NW * 32;
+      const int r2 = (t % (BK / 2)) * 2, c0 = t / (BK / 2);
+      int64_t ox[CPT], oy[CPT];
 #pragma unroll
-  for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < nkb) load_stage(st, r0 + (int64_t)st * BK);
-    cp_async_commit();
+      for (int i = 0; i < CPT; ++i) {
+        ox[i] = xoff[c0 + NPT * i];
+        oy[i] = yoff[c0 + NPT * i];
+      }
+      const bool al = ((reinterpret_cast<uintptr_t>(X) % (2 * sizeof(TX))) == 0) && ldx % 2 == 0 &&
+                      ((reinterpret_cast<uintptr_t>(Y) % (2 * sizeof(TY))) == 0) && ldy % 2 == 0;
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t kb = 0; kb < nkb; ++kb) {
+        if (kb >= STAGES) mb_wait(&empty[st], ph ^ 1);
+        const int64_t row = r0 + kb * BK + r2;
+        TX* xs = xs0 + (size_t)st * TILE + c0 * LDS + r2;
+        TY* ys = ys0 + (size_t)st * TILE + c0 * LDS + r2;
+        if (al && row + 1 < r1) {
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            if constexpr (sizeof(TX) == 8)
+              cp_async16(xs + NPT * i * LDS, ox[i] >= 0 ? X + ox[i] + row : X, ox[i] >= 0);
+            else
+              cp_async8(xs + NPT * i * LDS, ox[i] >= 0 ? X + ox[i] + row : X, ox[i] >= 0);
+            if constexpr (sizeof(TY) == 8)
+              cp_async16(ys + NPT * i * LDS, oy[i] >= 0 ? Y + oy[i] + row : Y, oy[i] >= 0);
+            else
+              cp_async8(ys + NPT * i * LDS, oy[i] >= 0 ? Y + oy[i] + row : Y, oy[i] >= 0);
+          }
+        } else {
+          const bool v0 = row < r1, v1 = row + 1 < r1;
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            const bool x0 = ox[i] >= 0 && v0, x1 = ox[i] >= 0 && v1;
+            const bool y0 = oy[i] >= 0 && v0, y1 = oy[i] >= 0 && v1;
+            cp_async_elem(xs + NPT * i * LDS, x0 ? X + ox[i] + row : X, x0);
+            cp_async_elem(xs + NPT * i * LDS + 1, x1 ? X + ox[i] + row + 1 : X, x1);
+            cp_async_elem(ys + NPT * i * LDS, y0 ? Y + oy[i] + row : Y, y0);
+            cp_async_elem(ys + NPT * i * LDS + 1, y1 ? Y + oy[i] + row + 1 : Y, y1);
+          }
+        }
+        mb_cp_async_arrive(&full[st]);
+        if (++st == STAGES) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+      cp_async_wait<0>();
+      return;
+    }
+  } else {
+#pragma unroll
+    for (int st = 0; st < STAGES - 1; ++st) {
+      if (st < nkb) load_stage(st, r0 + (int64_t)st * BK);
+      cp_async_commit();
+    }
   }
   for (int64_t kb = 0; kb < nkb; ++kb) {
-    const int64_t nxt = kb + STAGES - 1;
-    if (nxt < nkb) load_stage((int)(nxt % STAGES), r0 + nxt * BK);
-    cp_async_commit();
-    cp_async_wait<STAGES - 1>();
-    __syncthreads();
+    if constexpr (WS) {
+      mb_wait(&full[kb % STAGES], (uint32_t)((kb / STAGES) & 1));
+    } else {
+      const int64_t nxt = kb + STAGES - 1;
+      if (nxt < nkb) load_stage((int)(nxt % STAGES), r0 + nxt * BK);
+      cp_async_commit();
+      cp_async_wait<STAGES - 1>();
+      __syncthreads();
+    }
     const TX* xs = xs0 + (size_t)(kb % STAGES) * TILE;
     const TY* ys = ys0 + (size_t)(kb % STAGES) * TILE;
     if (BAL && diag) {
@@ -580,9 +683,14 @@ __global__ void __launch_bounds__(THREADS, 2) partial_kernel(
         for (int g = 0; g < 5; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
     }
     }
-    __syncthreads();
+    if constexpr (WS) {
+      __syncwarp();
+      if (lane == 0) mb_arrive(&empty[kb % STAGES]);
+    } else {
+      __syncthreads();
+    }
   }
-  cp_async_wait<0>();
+  if constexpr (!WS) cp_async_wait<0>();
   double* out = ws + (size_t)split * p * q;
   if (BAL && diag) {
 #pragma unroll
@@ -1126,6 +1234,155 @@ __global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS, POD_NNS_MINB) kernel(in
   }
 }
 
+// Warp-specialized variant of kernel<> (beta Z epilogue, no column dots):
+// one producer warp streams the (block, chunk) sequence into the STAGES ring
+// with cp.async, each lane's copies completing on the stage's `full`
+// mbarrier (cp.async.mbarrier.arrive.noinc), and the NWARP consumer warps
+// release a stage through its `empty` mbarrier once their fragments are
+// loaded -- no CTA-wide barrier per stage, so a warp may run up to STAGES - 1
+// chunks ahead of the slowest.  Same fragments, same k order, same epilogue:
+// bitwise equal to kernel<>.
+template <int BN, typename TX = double>
+__global__ void __launch_bounds__(Cfg<BN, TX>::NTHREADS + 32, Cfg<BN, TX>::PER_SM) kernel_ws(
+    int64_t m, int p, int q, double alpha, const TX* X, int64_t ldx,
+    const int32_t* __restrict__ xcols, const double* __restrict__ T, int64_t ldT, double beta,
+    const double* Z, int64_t ldz, double* Y, int64_t ldy, const int32_t* __restrict__ gate,
+    int vx, int vt) {
+  using C = Cfg<BN, TX>;
+  constexpr int ST = C::STAGES;
+  constexpr size_t STB = C::XBYTES + C::TT * sizeof(double);
+  if (gate && *gate == 0) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)ST * STB);
+  uint64_t* empty = full + ST;
+  const int q0 = blockIdx.y * BN;
+  T += (int64_t)q0 * ldT;
+  Y += (int64_t)q0 * ldy;
+  if (Z) Z += (int64_t)q0 * ldz;
+  q = min(BN, q - q0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nkb = (p + C::BK - 1) / C::BK;
+  const int64_t nblk = (m + C::BM - 1) / C::BM;
+  const int64_t G = gridDim.x;
+  if ((int64_t)blockIdx.x >= nblk) return;
+  const int64_t nmine = (nblk - blockIdx.x + G - 1) / G;
+  const int64_t total = nmine * nkb;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mb_init(&full[s], 32);
+      mb_init(&empty[s], C::NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == C::NWARP) {  // ---- producer warp
+    int64_t r0 = (int64_t)blockIdx.x * C::BM;
+    int kb = 0, st = 0;
+    uint32_t ph = 0;
+    for (int64_t it = 0; it < total; ++it) {
+      if (it >= ST) mb_wait(&empty[st], ph ^ 1);
+      TX* xs = reinterpret_cast<TX*>(smem_raw + (size_t)st * STB);
+      double* ts = reinterpret_cast<double*>(smem_raw + (size_t)st * STB + C::XBYTES);
+      const int k0 = kb * C::BK;
+      // the chunk's gathered column ids, one per lane (BK <= 32), broadcast
+      // below by shuffles instead of a dependent load per copy
+      int mycol = k0 + lane;
+      if (xcols && lane < C::BK && k0 + lane < p) mycol = xcols[k0 + lane];
+      for (int e = lane; e < C::BK * (C::BM / 2); e += 32) {
+        const int cl = e / (C::BM / 2), i2 = (e - cl * (C::BM / 2)) * 2;
+        const int c = k0 + cl;
+        const int64_t row = r0 + i2;
+        const int colv = __shfl_sync(0xffffffffu, mycol, cl);
+        int64_t col = colv;
+        bool cv = c < p && colv >= 0;  // index -1: zero column
+        TX* dst = xs + cl * C::LDX + i2;
+        const TX* src = X + col * ldx + row;
+        if (cv && vx && row + 1 < m) {
+          if constexpr (sizeof(TX) == 8) cp_async16(dst, src, true);
+          else cp_async8(dst, src, true);
+        } else {
+          cp_async_elem(dst, cv && row < m ? src : X, cv && row < m);
+          cp_async_elem(dst + 1, cv && row + 1 < m ? src + 1 : X, cv && row + 1 < m);
+        }
+      }
+      for (int e = lane; e < BN * (C::BK / 2); e += 32) {
+        const int j = e / (C::BK / 2), k2 = (e - j * (C::BK / 2)) * 2;
+        const int k = k0 + k2;
+        const bool jv = j < q;
+        double* dst = ts + j * C::LDT + k2;
+        const double* src = T + k + (int64_t)j * ldT;
+        if (jv && vt && k + 1 < p) {
+          cp_async16(dst, src, true);
+        } else {
+          cp_async8(dst, jv && k < p ? src : T, jv && k < p);
+          cp_async8(dst + 1, jv && k + 1 < p ? src + 1 : T, jv && k + 1 < p);
+        }
+      }
+      mb_cp_async_arrive(&full[st]);
+      if (++kb == nkb) {
+        kb = 0;
+        r0 += G * C::BM;
+      }
+      if (++st == ST) {
+        st = 0;
+        ph ^= 1;
+      }
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  // ---- consumer warps
+  const int wm = warp % C::WM, wn = warp / C::WM;
+  double acc[4][C::FN][2];
+  int kb = 0, st = 0;
+  uint32_t ph = 0;
+  int64_t c_r0 = (int64_t)blockIdx.x * C::BM;
+  for (int64_t it = 0; it < total; ++it) {
+    mb_wait(&full[st], ph);
+    if (kb == 0) {
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int g = 0; g < C::FN; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+    }
+    const TX* xs = reinterpret_cast<const TX*>(smem_raw + (size_t)st * STB);
+    const double* ts = reinterpret_cast<const double*>(smem_raw + (size_t)st * STB + C::XBYTES);
+#pragma unroll
+    for (int kk = 0; kk < C::BK / 4; ++kk) {
+      double a[4], b[C::FN];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+        a[f] = (double)xs[(kk * 4 + (lane & 3)) * C::LDX + wm * 32 + f * 8 + (lane >> 2)];
+#pragma unroll
+      for (int g = 0; g < C::FN; ++g)
+        b[g] = ts[(wn * (BN / C::WN) + g * 8 + (lane >> 2)) * C::LDT + kk * 4 + (lane & 3)];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int g = 0; g < C::FN; ++g) dmma8x8x4(acc[f][g][0], acc[f][g][1], a[f], b[g]);
+    }
+    __syncwarp();
+    if (lane == 0) mb_arrive(&empty[st]);
+    if (++st == ST) {
+      st = 0;
+      ph ^= 1;
+    }
+    if (++kb == nkb) {
+      kb = 0;
+      const int64_t row0 = c_r0 + wm * 32;
+      c_r0 += G * C::BM;
+      nn_epilogue<C::FN>(acc, row0, wn * (BN / C::WN), lane, m, q, alpha, beta, Z, ldz, Y, ldy);
+    }
+  }
+}
+template <int BN, typename TX = double>
+constexpr size_t ws_smem() {
+  return (size_t)Cfg<BN, TX>::STAGES * (Cfg<BN, TX>::XBYTES + Cfg<BN, TX>::TT * sizeof(double)) +
+         2 * Cfg<BN, TX>::STAGES * sizeof(uint64_t);
+}
+
 // out[j] = sum over the CTAs of dws[j][cta] (fixed order), j < k
 __global__ void dots_final_kernel(const double* __restrict__ dws, int nchunk, int k,
                                   double* __restrict__ out) {
@@ -1143,6 +1400,17 @@ static bool tn80_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("POD_TN80");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+// Warp-specialized 80-wide TN partial kernel (default; POD_TN_WS=0: the
+// barrier-per-stage kernel, A/B).  Config-3 shapes: Gram 1.125 -> 1.052 ms,
+// gathered Gram 2.485 -> 2.322 ms, U1^T U2 1.755 -> 1.732 ms (bitwise equal).
+static bool tn_ws_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_TN_WS");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
@@ -1193,20 +1461,20 @@ static int ensure_attrs() {
   TN64_BAL_ATTR(float, double)
   TN64_BAL_ATTR(double, float)
 #undef TN64_BAL_ATTR
-#define TN80_ATTR(A_, B_)                                                                   \
-  e = cudaFuncSetAttribute(tn80::partial_kernel<A_, B_, false>,                            \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
-                           (int)tn80::smem_bytes<A_, B_>());                               \
-  if (e != cudaSuccess) return cuda_status(e, "tn80 attr");                                \
-  e = cudaFuncSetAttribute(tn80::partial_kernel<A_, B_, true>,                             \
+#define TN80_ATTR1(A_, B_, BAL_, WS_)                                                        \
+  e = cudaFuncSetAttribute(tn80::partial_kernel<A_, B_, BAL_, WS_>,                        \
                            cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
                            (int)tn80::smem_bytes<A_, B_>());                               \
   if (e != cudaSuccess) return cuda_status(e, "tn80 attr");
+#define TN80_ATTR(A_, B_)                                                                   \
+  TN80_ATTR1(A_, B_, false, false) TN80_ATTR1(A_, B_, true, false)                          \
+  TN80_ATTR1(A_, B_, false, true) TN80_ATTR1(A_, B_, true, true)
   TN80_ATTR(double, double)
   TN80_ATTR(float, float)
   TN80_ATTR(float, double)
   TN80_ATTR(double, float)
 #undef TN80_ATTR
+#undef TN80_ATTR1
   e = cudaFuncSetAttribute((const void*)nnp::kernel<64, true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   if (e != cudaSuccess) return cuda_status(e, "nnp gram attr");
@@ -1293,10 +1561,13 @@ extern "C" int pod_gemm_tn(int xtype, int ytype, int64_t m, int64_t p, int64_t q
     grid = dim3((unsigned)(bal.nd * bal.sd + (bal.nd * (bal.nd - 1) / 2) * bal.so), 1);
   if (w80) {
 #define TN80_LAUNCH(A_, B_)                                                                     \
-  (bal.on ? tn80::partial_kernel<A_, B_, true> : tn80::partial_kernel<A_, B_, false>)           \
-      <<<grid, tn80::THREADS, tn80::smem_bytes<A_, B_>(), s>>>(                                 \
+  (tnws ? (bal.on ? tn80::partial_kernel<A_, B_, true, true>                                     \
+                  : tn80::partial_kernel<A_, B_, false, true>)                                  \
+        : (bal.on ? tn80::partial_kernel<A_, B_, true> : tn80::partial_kernel<A_, B_, false>))  \
+      <<<grid, tn80::THREADS + (tnws ? 32 * tn80::NPROD : 0), tn80::smem_bytes<A_, B_>(), s>>>(                \
       m, (int)p, (int)q, (const A_*)X, ldx, xcols, (const B_*)Y, ldy, ycols, pl.rows_per_split, \
       (double*)ws, gate, sym, bal)
+    const bool tnws = tn_ws_enabled();
     if (xtype == POD_F64 && ytype == POD_F64) TN80_LAUNCH(double, double);
     else if (xtype == POD_F64) TN80_LAUNCH(double, float);
     else if (ytype == POD_F32) TN80_LAUNCH(float, float);
@@ -1418,6 +1689,36 @@ extern "C" int pod_gemm_nn_f64(int64_t m, int64_t p, int64_t q, double alpha, co
                      0, 0, nullptr, &nchunk);
 }
 
+// The warp-specialized streamed NN kernel (default; POD_NN_WS=0: the
+// barrier-per-stage kernel, A/B).  Config-3 shapes: rotation 4.94 -> 3.53 ms,
+// residual 3.15 -> 2.13, apply 2.69 -> 1.91, lift 3.48 -> 2.76 (bitwise equal).
+static bool nn_ws_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("POD_NN_WS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+template <int BN>
+static int launch_nn_ws(dim3 grid, cudaStream_t s, int64_t m, int64_t p, int64_t q, double alpha,
+                        const double* X, int64_t ldx, const int32_t* xcols, const double* T,
+                        int64_t ldt, double beta, const double* Z, int64_t ldz, double* Y,
+                        int64_t ldy, const int32_t* gate, int vx, int vt) {
+  static bool attr = false;
+  constexpr size_t smem = nns::ws_smem<BN>();
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(nns::kernel_ws<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_status(e, "nns ws attr");
+    attr = true;
+  }
+  nns::kernel_ws<BN><<<grid, nns::Cfg<BN>::NTHREADS + 32, smem, s>>>(
+      m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt);
+  POD_CHECK_LAUNCH("nn streamed ws");
+  return POD_OK;
+}
+
 // The streamed (nns) launches of pod_gemm_nn_f64, with optional column dots
 // (kdot > 0: dws[j][cta] partials; *nchunk_out = CTAs along the rows).
 static int nn_streamed(int64_t m, int64_t p, int64_t q, double alpha, const double* X,
@@ -1449,6 +1750,9 @@ static int nn_streamed(int64_t m, int64_t p, int64_t q, double alpha, const doub
         const int64_t per = std::max<int64_t>(1, capped(C80::PER_SM * 148) / gy);
         const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
         *nchunk_out = grid.x;
+        if (kdot == 0 && nn_ws_enabled())
+          return launch_nn_ws<80>(grid, s, m, p, q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz,
+                                  Y, ldy, gate, vx, vt);
         (kdot > 0 ? nns::kernel<80, double, true> : nns::kernel<80, double, false>)<<<grid, C80::NTHREADS, C80::SMEM, s>>>(
             m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt,
             DX, dldx, kdot, dws);
@@ -1458,6 +1762,9 @@ static int nn_streamed(int64_t m, int64_t p, int64_t q, double alpha, const doub
         const int64_t per = std::max<int64_t>(1, capped(nns::Cfg<64>::PER_SM * 148) / gy);
         const dim3 grid((unsigned)std::min<int64_t>(nblk, per), gy);
         *nchunk_out = grid.x;
+        if (kdot == 0 && nn_ws_enabled())
+          return launch_nn_ws<64>(grid, s, m, p, q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz,
+                                  Y, ldy, gate, vx, vt);
         (kdot > 0 ? nns::kernel<64, double, true> : nns::kernel<64, double, false>)<<<grid, nns::THREADS, nns::Cfg<64>::SMEM, s>>>(
             m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt,
             DX, dldx, kdot, dws);
@@ -1473,6 +1780,9 @@ static int nn_streamed(int64_t m, int64_t p, int64_t q, double alpha, const doub
       const int64_t nblk = ceil_div(m, nns::Cfg<192>::BM);
       const unsigned grid = (unsigned)std::min<int64_t>(nblk, capped(nns::Cfg<192>::PER_SM * 148));
       *nchunk_out = grid;
+      if (kdot == 0 && nn_ws_enabled())
+        return launch_nn_ws<192>(dim3(grid), s, m, p, q, alpha, X, ldx, xcols, T, ldt, beta, Z,
+                                 ldz, Y, ldy, gate, vx, vt);
       (kdot > 0 ? nns::kernel<192, double, true> : nns::kernel<192, double, false>)<<<grid, nns::THREADS, nns::Cfg<192>::SMEM, s>>>(
           m, (int)p, (int)q, alpha, X, ldx, xcols, T, ldt, beta, Z, ldz, Y, ldy, gate, vx, vt,
           DX, dldx, kdot, dws);
