@@ -109,6 +109,14 @@ LEAK_GRID_CAP = int(__import__("os").environ.get("POD_LEAK_GRID_CAP", "64"))
 #: reports a defect > 1e-4 or a shift.  POD_SECOND_PROJ_ONE_PASS=0: always two.
 SECOND_PROJ_ONE_PASS = __import__("os").environ.get("POD_SECOND_PROJ_ONE_PASS", "1") != "0"
 
+#: the merge's CholeskyQR2 (merge.py:70) skips its second m x r apply: the
+#: pass-1 factor's R^-1 stays a small r x r matrix ("fold") that multiplies
+#: the leak matrix U1^T Q (merge.py:72) and the lower half of the rotation
+#: (merge.py:86-88) instead -- [U1 Q1 R^-1] T = [U1 Q1] [T_top; R^-1 T_bot].
+#: Q is materialized (gated) only when a further CholeskyQR pass or the
+#: second projection needs it.  POD_FOLD_QR=0 disables.
+FOLD_QR = __import__("os").environ.get("POD_FOLD_QR", "1") != "0"
+
 #: NN GEMMs whose output a CholeskyQR pass consumes next form its Gram in
 #: their epilogue (pod_gemm_nn_gram, q <= 64) instead of a TN pass over the
 #: output.  POD_NN_GRAM=0 disables.
@@ -170,6 +178,11 @@ class MergeWorkspace:
         self.Rt = torch.zeros(sq, **f64)
         self.Rt2 = torch.zeros(sq, **f64)
         self.Rtmp = torch.zeros(sq, **f64)
+        # folded CholeskyQR pass (FOLD_QR): the unapplied R^-1, the raw leak
+        # matrix U1^T Q1 and an identity to reset the fold with
+        self.Rfold = torch.eye(r, **f64).reshape(-1).contiguous()
+        self.Ident = torch.eye(r, **f64).reshape(-1).contiguous()
+        self.C1 = torch.zeros(sq, **f64)
         self.Tm = torch.zeros(2 * r * r, **f64)
         self.sig = [torch.zeros(r, **f64), torch.zeros(r, **f64)]
         kk = max(self.k, 1)
@@ -212,7 +225,7 @@ class MergeWorkspace:
 
     # ------------------------------------------------------- launch pieces --
     def cholqr_ops(self, Wsrc, Q, l, Rout, gate_base, first_gate=None, sharded=True,
-                   gram_ready=False):
+                   gram_ready=False, fold=False):
         """Q = orthonormal factor of Wsrc (m x l) with Wsrc = Q Rout (the
         Householder QR of merge.py:70/76, matcore.py:209 replaced by
         CholeskyQR passes).  Passes 0 and 1 (CholeskyQR2) run when first_gate
@@ -221,8 +234,12 @@ class MergeWorkspace:
         passes run in place when the previous pass asked for them (slot
         gate_base + p).  gram_ready: self.Gq already holds Wsrc^T Wsrc (from
         the producing GEMM's Gram epilogue); pass 0's apply forms pass 1's
-        Gram the same way when the shape allows (nn_gram)."""
+        Gram the same way when the shape allows (nn_gram).  fold: pass 0
+        writes Q directly and pass 1 only factors -- its R^-1 is left in
+        self.Rfold for the caller to apply to the small matrices (FOLD_QR);
+        `materialize_q` turns Q into the true factor when someone needs it."""
         ctx, r = self.ctx, self.r
+        assert not fold or (first_gate is None and l == r)
         g0 = first_gate
         tmp = self._scratch_like(Q)
         src = Wsrc
@@ -238,7 +255,7 @@ class MergeWorkspace:
         # identity by more than 1e-4 or needed a shift, like passes >= 2
         one = first_gate is not None and SECOND_PROJ_ONE_PASS
         for p in range(2):  # CholeskyQR2: Wsrc -> tmp -> Q
-            dst = (Q if one else tmp) if p == 0 else Q
+            dst = (Q if (one or fold) else tmp) if p == 0 else Q
             gp = g0 if (p == 0 or not one) else self.gate(gate_base + 1)
             if not have_gram:
                 ctx.tn(l, l, 1.0, src, src, dptr(self.Gq), r, gate=gp, tag="tn_cholqr_gram")
@@ -249,6 +266,9 @@ class MergeWorkspace:
                                   None if p == 0 else dptr(Rout), r,
                                   gate_in=gp, gate_out=self.gate(gate_base + p + 1),
                                   first_pass=1 if (p == 0 and not one) else 0)
+            if p == 1 and fold:  # the apply is folded into the small matrices
+                ctx.small_copy(l, l, dptr(self.Rinv), r, dptr(self.Rfold), r)
+                break
             if p == 1 and one and l > NN_INPLACE_MAX_Q:  # in place through the scratch block
                 ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, tmp, gate=gp, tag="nn_cholqr_apply")
                 ctx.small_copy(Q.m, l, tmp.ptr, tmp.ld, Q.ptr, Q.ld, gate=gp)
@@ -262,6 +282,8 @@ class MergeWorkspace:
             src = dst
         for p in range(2, CHOLQR_PASSES):
             gp = self.gate(gate_base + p)
+            if fold and p == 2:
+                self.materialize_q(Q, gp)
             ctx.tn(l, l, 1.0, Q, Q, dptr(self.Gq), r, gate=gp, tag="tn_cholqr_gram")
             if sharded:
                 self.comm.allreduce_sum_(self.Gq)
@@ -273,6 +295,18 @@ class MergeWorkspace:
             else:  # wider than the in-place NN kernel: through the scratch block
                 ctx.nn(l, l, 1.0, Q, dptr(self.Rinv), r, tmp, gate=gp, tag="nn_cholqr_apply")
                 ctx.small_copy(Q.m, l, tmp.ptr, tmp.ld, Q.ptr, Q.ld, gate=gp)
+
+    def materialize_q(self, Q, gate):
+        """Folded CholeskyQR (FOLD_QR): Q <- Q Rfold, Rfold <- I, when `gate`
+        is set (a further pass or the second projection reads the true Q)."""
+        ctx, r = self.ctx, self.r
+        if r <= NN_INPLACE_MAX_Q:
+            ctx.nn(r, r, 1.0, Q, dptr(self.Rfold), r, Q, gate=gate, tag="nn_cholqr_apply")
+        else:
+            tmp = self._scratch_like(Q)
+            ctx.nn(r, r, 1.0, Q, dptr(self.Rfold), r, tmp, gate=gate, tag="nn_cholqr_apply")
+            ctx.small_copy(Q.m, r, tmp.ptr, tmp.ld, Q.ptr, Q.ld, gate=gate)
+        ctx.small_copy(r, r, dptr(self.Ident), r, dptr(self.Rfold), r, gate=gate)
 
     def _scratch_like(self, Q):
         """m x r scratch block for the first CholeskyQR pass (one per row count)."""
@@ -303,11 +337,12 @@ class MergeWorkspace:
         if NN_GRAM and ctx.nn_gram_ok(r, r):  # the residual's Gram in the same pass
             ctx.nn_gram(r, r, -1.0, U1, dptr(self.M), r, self.W, dptr(self.Gq), r, beta=1.0,
                         Z=U2, tag="nn_merge_resid")                          # merge.py:69
-            self.cholqr_ops(self.W, Q, r, self.Rt, G_QR, gram_ready=True)    # merge.py:70
+            self.cholqr_ops(self.W, Q, r, self.Rt, G_QR, gram_ready=True,
+                            fold=FOLD_QR)                                    # merge.py:70
         else:
             ctx.nn(r, r, -1.0, U1, dptr(self.M), r, self.W, beta=1.0, Z=U2,
                    tag="nn_merge_resid")                                     # merge.py:69
-            self.cholqr_ops(self.W, Q, r, self.Rt, G_QR)                     # merge.py:70
+            self.cholqr_ops(self.W, Q, r, self.Rt, G_QR, fold=FOLD_QR)       # merge.py:70
         spec = self.speculative_core()
         if spec:
             # the E-SVD on the first-pass (M, R) starts now; the leak check
@@ -333,6 +368,8 @@ class MergeWorkspace:
         else:
             self.leak_check_ops(U1, Q)
         gl = self.gate(G_LEAK)                                               # merge.py:73-79
+        if FOLD_QR:
+            self.materialize_q(Q, gl)
         ctx.nn(r, r, -1.0, U1, dptr(self.C), r, self.W, beta=1.0, Z=Q, gate=gl,
                tag="nn_merge_resid")
         self.cholqr_ops(self.W, Q, r, self.Rt2, G_RQR, first_gate=gl)
@@ -347,6 +384,11 @@ class MergeWorkspace:
             if before_core is not None:
                 before_core()
             ctx.merge_core(*core, info=info)                                 # merge.py:80-85
+        if FOLD_QR:  # T_bot <- Rfold T_bot: the rotation reads Q1, not Q1 R^-1
+            tbot = dptr(self.Tm, r)
+            ctx.small_gemm(r, r, r, 1.0, dptr(self.Rfold), r, 0, tbot, 2 * r, 0.0,
+                           dptr(self.Rtmp), r)
+            ctx.small_copy(r, r, dptr(self.Rtmp), r, tbot, 2 * r)
         if cos_out is not None:  # rotation + cosines in one pass (isma.py:195-198)
             ctx.nn_dots(2 * r, r, 1.0, S, dptr(self.Tm), 2 * r, Snext.cols(0, r), self.k, cos_out,
                         tag="nn_merge_rotate")                               # merge.py:86-88
@@ -357,8 +399,14 @@ class MergeWorkspace:
     def leak_check_ops(self, U1, Q):
         """C = U1^T Q and the gate max|C| > REORTH_TOL (merge.py:72-73)."""
         ctx, r = self.ctx, self.r
-        ctx.tn(r, r, 1.0, U1, Q, dptr(self.C), r, tag="tn_merge_leak")
-        self.comm.allreduce_sum_(self.C)
+        if FOLD_QR:  # Q holds Q1: U1^T Q = (U1^T Q1) Rfold
+            ctx.tn(r, r, 1.0, U1, Q, dptr(self.C1), r, tag="tn_merge_leak")
+            self.comm.allreduce_sum_(self.C1)
+            ctx.small_gemm(r, r, r, 1.0, dptr(self.C1), r, 0, dptr(self.Rfold), r, 0.0,
+                           dptr(self.C), r)
+        else:
+            ctx.tn(r, r, 1.0, U1, Q, dptr(self.C), r, tag="tn_merge_leak")
+            self.comm.allreduce_sum_(self.C)
         ctx.maxabs(dptr(self.C), r, r, r, dptr(self.leak), thr=REORTH_TOL,
                    gate_out=self.gate(G_LEAK))
 

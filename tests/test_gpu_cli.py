@@ -138,3 +138,53 @@ def test_module_invocation_end_to_end(mat, tmp_path):
                          timeout=600)
     assert res.returncode == 0, res.stderr
     reporting.validate_report(json.load(open(out)))
+
+
+# ---- the reference CLI's own reports (tests/golden/make_cli_golden.py) ------
+def _cli_golden():
+    with open(os.path.join(ROOT, "tests", "golden", "cli_reports.json")) as f:
+        return json.load(f)["cases"]
+
+
+def _close(x, y, rtol, atol):
+    np.testing.assert_allclose(np.asarray(x, dtype=float), np.asarray(y, dtype=float),
+                               rtol=rtol, atol=atol)
+
+
+@pytest.mark.parametrize("name", sorted(_cli_golden()))
+def test_report_matches_reference_cli(capsys, tmp_path, name):
+    """The drop-in's `run` report equals the report the reference's command
+    line printed for the same matrix and arguments (reference cli.py run
+    command + reporting.build_report): config echo, pass count and per-round
+    bookkeeping exactly; sigma, cosines, angles and the Wedin block to fp64
+    tolerance."""
+    from golden.make_cli_golden import case_matrix, strip_timing
+
+    case = _cli_golden()[name]
+    path = str(tmp_path / "d.podm")
+    pod.write_matrix(path, case_matrix())
+    argv = [path if x == "MATRIX" else x for x in case["argv"]]
+    got = strip_timing(_run(capsys, "run", *argv))
+    ref = case["report"]
+    assert sorted(got) == sorted(ref)
+    assert got["config"] == ref["config"]
+    assert got["passes"] == ref["passes"]
+    _close(got["sigma"], ref["sigma"], 1e-10, 0)
+    assert len(got["traces"]) == len(ref["traces"])
+    for tg, tr in zip(got["traces"], ref["traces"]):
+        assert sorted(tg) == sorted(tr)
+        for key in ("iteration", "remaining", "columns_sampled", "rows_sampled"):
+            assert tg[key] == tr[key], (key, tg, tr)
+        assert len(tg["cosines"]) == len(tr["cosines"])
+        _close(tg["cosines"], tr["cosines"], 0, 1e-9)
+    if "angles" in ref:
+        for key in ref["angles"]:
+            # degrees; arccos near 1 resolves angles only to ~sqrt(eps) rad
+            # (1e-6 deg), so an exact-reference run (gram) reads 0 .. 1e-5
+            _close(got["angles"][key], ref["angles"][key], 0, 2e-5)
+    if "wedin" in ref:
+        for key, val in ref["wedin"].items():
+            if isinstance(val, float):
+                _close(got["wedin"][key], val, 1e-8, 1e-10)
+            else:
+                assert got["wedin"][key] == val, key
