@@ -117,6 +117,11 @@ SECOND_PROJ_ONE_PASS = __import__("os").environ.get("POD_SECOND_PROJ_ONE_PASS", 
 #: second projection needs it.  POD_FOLD_QR=0 disables.
 FOLD_QR = __import__("os").environ.get("POD_FOLD_QR", "1") != "0"
 
+#: with the folded pass, the leak GEMM U1^T Q1 (merge.py:72) no longer waits
+#: for the pass-1 factor: it runs on its own stream beside that single-CTA
+#: kernel (non-speculative, unsharded merges).  POD_EARLY_LEAK=0 disables.
+EARLY_LEAK = __import__("os").environ.get("POD_EARLY_LEAK", "1") != "0"
+
 #: NN GEMMs whose output a CholeskyQR pass consumes next form its Gram in
 #: their epilogue (pod_gemm_nn_gram, q <= 64) instead of a TN pass over the
 #: output.  POD_NN_GRAM=0 disables.
@@ -225,7 +230,7 @@ class MergeWorkspace:
 
     # ------------------------------------------------------- launch pieces --
     def cholqr_ops(self, Wsrc, Q, l, Rout, gate_base, first_gate=None, sharded=True,
-                   gram_ready=False, fold=False):
+                   gram_ready=False, fold=False, after_gram1=None):
         """Q = orthonormal factor of Wsrc (m x l) with Wsrc = Q Rout (the
         Householder QR of merge.py:70/76, matcore.py:209 replaced by
         CholeskyQR passes).  Passes 0 and 1 (CholeskyQR2) run when first_gate
@@ -261,6 +266,8 @@ class MergeWorkspace:
                 ctx.tn(l, l, 1.0, src, src, dptr(self.Gq), r, gate=gp, tag="tn_cholqr_gram")
             if sharded:
                 self.comm.allreduce_sum_(self.Gq)
+            if p == 1 and after_gram1 is not None:
+                after_gram1()
             ctx.cholqr_factor_acc(dptr(self.Gq), r, l, src.m, dptr(self.Rinv), r,
                                   dptr(Rout) if p == 0 else rk, r,
                                   None if p == 0 else dptr(Rout), r,
@@ -334,16 +341,33 @@ class MergeWorkspace:
         info = self.rec[0, REC_KEEP:]
         ctx.tn(r, r, 1.0, U1, U2, dptr(self.M), r, tag="tn_merge_proj")       # merge.py:65
         self.comm.allreduce_sum_(self.M)
+        spec = self.speculative_core()
+        early = FOLD_QR and EARLY_LEAK and not spec and not self.comm.active
+        hook = None
+        if early:
+            if self._leak_stream is None:
+                self._leak_stream = torch.cuda.Stream(ctx.device)
+
+            def hook():  # Q1 and its Gram are out: U1^T Q1 beside the pass-1 factor
+                ev = torch.cuda.Event()
+                ev.record(torch.cuda.current_stream(ctx.device))
+                self._leak_stream.wait_event(ev)
+                ctx.ws_suffix = "_leak"
+                try:
+                    with torch.cuda.stream(self._leak_stream):
+                        ctx.tn(r, r, 1.0, U1, Q, dptr(self.C1), r, tag="tn_merge_leak")
+                finally:
+                    ctx.ws_suffix = ""
         if NN_GRAM and ctx.nn_gram_ok(r, r):  # the residual's Gram in the same pass
             ctx.nn_gram(r, r, -1.0, U1, dptr(self.M), r, self.W, dptr(self.Gq), r, beta=1.0,
                         Z=U2, tag="nn_merge_resid")                          # merge.py:69
             self.cholqr_ops(self.W, Q, r, self.Rt, G_QR, gram_ready=True,
-                            fold=FOLD_QR)                                    # merge.py:70
+                            fold=FOLD_QR, after_gram1=hook)                  # merge.py:70
         else:
             ctx.nn(r, r, -1.0, U1, dptr(self.M), r, self.W, beta=1.0, Z=U2,
                    tag="nn_merge_resid")                                     # merge.py:69
-            self.cholqr_ops(self.W, Q, r, self.Rt, G_QR, fold=FOLD_QR)       # merge.py:70
-        spec = self.speculative_core()
+            self.cholqr_ops(self.W, Q, r, self.Rt, G_QR, fold=FOLD_QR,
+                            after_gram1=hook)                                # merge.py:70
         if spec:
             # the E-SVD on the first-pass (M, R) starts now; the leak check
             # (merge.py:72-73) runs beside it on its own stream, and the
@@ -365,6 +389,10 @@ class MergeWorkspace:
                 lib.pod_set_grid_cap(0)
                 ctx.ws_suffix = ""
             main.wait_stream(self._leak_stream)
+        elif early:
+            torch.cuda.current_stream(ctx.device).wait_stream(self._leak_stream)
+            # a further CholeskyQR pass materialized Q after the early product
+            self.leak_check_ops(U1, Q, tn_gate=self.gate(G_QR + 2))
         else:
             self.leak_check_ops(U1, Q)
         gl = self.gate(G_LEAK)                                               # merge.py:73-79
@@ -396,11 +424,11 @@ class MergeWorkspace:
             ctx.nn(2 * r, r, 1.0, S, dptr(self.Tm), 2 * r, Snext.cols(0, r),
                    tag="nn_merge_rotate")                                    # merge.py:86-88
 
-    def leak_check_ops(self, U1, Q):
+    def leak_check_ops(self, U1, Q, tn_gate=None):
         """C = U1^T Q and the gate max|C| > REORTH_TOL (merge.py:72-73)."""
         ctx, r = self.ctx, self.r
         if FOLD_QR:  # Q holds Q1: U1^T Q = (U1^T Q1) Rfold
-            ctx.tn(r, r, 1.0, U1, Q, dptr(self.C1), r, tag="tn_merge_leak")
+            ctx.tn(r, r, 1.0, U1, Q, dptr(self.C1), r, gate=tn_gate, tag="tn_merge_leak")
             self.comm.allreduce_sum_(self.C1)
             ctx.small_gemm(r, r, r, 1.0, dptr(self.C1), r, 0, dptr(self.Rfold), r, 0.0,
                            dptr(self.C), r)
