@@ -117,6 +117,26 @@ SECOND_PROJ_ONE_PASS = __import__("os").environ.get("POD_SECOND_PROJ_ONE_PASS", 
 #: second projection needs it.  POD_FOLD_QR=0 disables.
 FOLD_QR = __import__("os").environ.get("POD_FOLD_QR", "1") != "0"
 
+#: out-of-place CholeskyQR applies Q = W R^-1 skip the zero half of the upper
+#: triangular R^-1: column chunk [c0, c1) multiplies only W's first c1
+#: columns (bitwise equal to the full product; tools/trmm_split_probe.py:
+#: l = 150 split at 80: 1.92 -> 1.48 ms, l = 192 in 64-wide chunks: 3.11 ->
+#: 2.12 ms at m = 1M; l <= 96 loses).  POD_TRI_APPLY=0 disables.
+TRI_APPLY = __import__("os").environ.get("POD_TRI_APPLY", "1") != "0"
+
+
+def tri_apply_bounds(l):
+    """Column chunk boundaries of the triangular apply for width l."""
+    if not TRI_APPLY or l < 120:
+        return [0, l]
+    if l <= 160:
+        return [0, 80, l]
+    b = list(range(0, l, 64))
+    if l - b[-1] < 32:  # fold a thin last chunk into its neighbour
+        b.pop()
+    return b + [l]
+
+
 #: with the folded pass, the leak GEMM U1^T Q1 (merge.py:72) no longer waits
 #: for the pass-1 factor: it runs on its own stream beside that single-CTA
 #: kernel (non-speculative, unsharded merges).  POD_EARLY_LEAK=0 disables.
@@ -277,14 +297,14 @@ class MergeWorkspace:
                 ctx.small_copy(l, l, dptr(self.Rinv), r, dptr(self.Rfold), r)
                 break
             if p == 1 and one and l > NN_INPLACE_MAX_Q:  # in place through the scratch block
-                ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, tmp, gate=gp, tag="nn_cholqr_apply")
+                self.apply_upper(src, self.Rinv, l, tmp, gate=gp)
                 ctx.small_copy(Q.m, l, tmp.ptr, tmp.ld, Q.ptr, Q.ld, gate=gp)
             elif p == 0 and fuse:  # the apply also forms pass 1's Gram
                 ctx.nn_gram(l, l, 1.0, src, dptr(self.Rinv), r, dst, dptr(self.Gq), r, gate=gp,
                             tag="nn_cholqr_apply")
                 have_gram = True
             else:
-                ctx.nn(l, l, 1.0, src, dptr(self.Rinv), r, dst, gate=gp, tag="nn_cholqr_apply")
+                self.apply_upper(src, self.Rinv, l, dst, gate=gp)
                 have_gram = False
             src = dst
         for p in range(2, CHOLQR_PASSES):
@@ -300,8 +320,16 @@ class MergeWorkspace:
             if l <= NN_INPLACE_MAX_Q:
                 ctx.nn(l, l, 1.0, Q, dptr(self.Rinv), r, Q, gate=gp, tag="nn_cholqr_apply")
             else:  # wider than the in-place NN kernel: through the scratch block
-                ctx.nn(l, l, 1.0, Q, dptr(self.Rinv), r, tmp, gate=gp, tag="nn_cholqr_apply")
+                self.apply_upper(Q, self.Rinv, l, tmp, gate=gp)
                 ctx.small_copy(Q.m, l, tmp.ptr, tmp.ld, Q.ptr, Q.ld, gate=gp)
+
+    def apply_upper(self, src, T, l, dst, gate=None):
+        """dst = src T for an upper triangular l x l T (leading dimension r),
+        src and dst distinct blocks."""
+        b = tri_apply_bounds(l)
+        for c0, c1 in zip(b[:-1], b[1:]):
+            self.ctx.nn(c1, c1 - c0, 1.0, src.cols(0, c1), dptr(T, c0 * self.r), self.r,
+                        dst.cols(c0, c1), gate=gate, tag="nn_cholqr_apply")
 
     def materialize_q(self, Q, gate):
         """Folded CholeskyQR (FOLD_QR): Q <- Q Rfold, Rfold <- I, when `gate`
@@ -311,7 +339,7 @@ class MergeWorkspace:
             ctx.nn(r, r, 1.0, Q, dptr(self.Rfold), r, Q, gate=gate, tag="nn_cholqr_apply")
         else:
             tmp = self._scratch_like(Q)
-            ctx.nn(r, r, 1.0, Q, dptr(self.Rfold), r, tmp, gate=gate, tag="nn_cholqr_apply")
+            self.apply_upper(Q, self.Rfold, r, tmp, gate=gate)
             ctx.small_copy(Q.m, r, tmp.ptr, tmp.ld, Q.ptr, Q.ld, gate=gate)
         ctx.small_copy(r, r, dptr(self.Ident), r, dptr(self.Rfold), r, gate=gate)
 
