@@ -379,7 +379,8 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
   double* dr2 = dr + l;                // 1 / Rh[j][j]
   __shared__ int s_fail;
   __shared__ double s_defect;
-  __shared__ double s_row[CQI_MAX_L], s_col[CQI_MAX_L];
+  __shared__ double s_row[CQI_MAX_L], s_col[CQI_MAX_L], s_piv[3];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   for (int i = threadIdx.x; i < l; i += blockDim.x) {
     const double gii = G[i + (int64_t)i * ldg];
     d[i] = (gii > 0.0) ? sqrt(gii) : 0.0;
@@ -424,26 +425,62 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
   int attempt = 0;
   for (;;) {
     if (attempt > 0) build(shift, false);
-    if (threadIdx.x == 0) s_fail = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_fail = 0;
+      const double p0 = C[0];
+      s_piv[0] = p0;
+      if (p0 > 0.0) {
+        const double q = sqrt(p0);
+        s_piv[1] = q;
+        s_piv[2] = 1.0 / q;
+      }
+    }
     __syncthreads();
     for (int j = 0; j < l; ++j) {
-      const double piv = C[pk(j, j)];
+      // pivot, its root and reciprocal: formed once (by one lane, beside the
+      // previous step's trailing update) instead of by all 32 warps, whose
+      // redundant fp64 sqrt + divide sequences kept the FP64 pipe busy
+      const double piv = s_piv[0], rjj = s_piv[1], rinv = s_piv[2];
       if (!(piv > 0.0)) {  // uniform decision
         if (threadIdx.x == 0) s_fail = 1;
         __syncthreads();
         break;
       }
-      const double rjj = sqrt(piv);
-      const double rinv = 1.0 / rjj;
+      // row j scaled, with a contiguous copy for the trailing update (the
+      // pivot itself is stored after the barrier: every thread has read it)
+      for (int k = j + 1 + threadIdx.x; k < l; k += blockDim.x) {
+        const double v = C[pk(j, k)] * rinv;
+        C[pk(j, k)] = v;
+        s_row[k] = v;
+      }
       __syncthreads();
-      if (threadIdx.x == 0) dr2[j] = rinv;
-      for (int k = j + threadIdx.x; k < l; k += blockDim.x)
-        C[pk(j, k)] = (k == j) ? rjj : C[pk(j, k)] * rinv;
-      __syncthreads();
-      const int rem = l - j - 1;
-      for (int t = threadIdx.x; t < rem * rem; t += blockDim.x) {
-        const int kk = j + 1 + t / rem, ii = j + 1 + t % rem;
-        if (ii <= kk) C[pk(ii, kk)] -= C[pk(j, ii)] * C[pk(j, kk)];
+      if (threadIdx.x == 32) {
+        dr2[j] = rinv;
+        C[pk(j, j)] = rjj;
+      }
+      // trailing update, one warp per packed column (rows contiguous across
+      // lanes: no index division, no bank conflicts); same operation per
+      // entry.  Warp 0 takes only column j + 1 -- the next pivot -- and roots it.
+      if (wid == 0) {
+        if (lane == 0 && j + 1 < l) {
+          const int kk = j + 1;
+          double* col = C + (kk * (kk + 1) >> 1);
+          col[kk] -= s_row[kk] * s_row[kk];
+          const double pn = col[kk];
+          s_piv[0] = pn;
+          if (pn > 0.0) {
+            const double q = sqrt(pn);
+            s_piv[1] = q;
+            s_piv[2] = 1.0 / q;
+          }
+        }
+      } else {
+        for (int kk = j + 1 + wid; kk < l; kk += nwarp - 1) {
+          const double ckk = s_row[kk];
+          double* col = C + (kk * (kk + 1) >> 1);
+          for (int ii = j + 1 + lane; ii <= kk; ii += 32) col[ii] -= s_row[ii] * ckk;
+        }
       }
       __syncthreads();
     }
@@ -470,10 +507,11 @@ __global__ void __launch_bounds__(SMALL_THREADS) cholqr_inplace_kernel(
       s_row[c] = v;
     }
     __syncthreads();
-    const int w = l - r;
-    for (int t = threadIdx.x; t < r * w; t += blockDim.x) {
-      const int c = r + t / r, i = t % r;
-      C[pk(i, c)] = fma(-s_col[i], s_row[c], (c == r) ? 0.0 : C[pk(i, c)]);
+    for (int c = r + wid; c < l; c += nwarp) {  // one warp per packed column
+      const double src = s_row[c];
+      double* col = C + (c * (c + 1) >> 1);
+      for (int i = lane; i < r; i += 32)
+        col[i] = fma(-s_col[i], src, (c == r) ? 0.0 : col[i]);
     }
     __syncthreads();
   }
