@@ -1005,7 +1005,13 @@ extern "C" int pod_cholqr_factor2(const double* G, int64_t ldg, int64_t l, int64
       if (e != cudaSuccess) return cuda_status(e, "cholqr in place smem attr");
       attr = true;
     }
-    cholqr_inplace_kernel<<<1, SMALL_THREADS, cqi_bytes(l), st>>>(
+    static int cqi_threads = 0;
+    if (!cqi_threads) {  // POD_CQI_THREADS: A/B of the CTA width (multiple of 32, 64..1024)
+      const char* e = getenv("POD_CQI_THREADS");
+      const int v = e ? atoi(e) : 0;
+      cqi_threads = (v >= 64 && v <= SMALL_THREADS && v % 32 == 0) ? v : SMALL_THREADS;
+    }
+    cholqr_inplace_kernel<<<1, cqi_threads, cqi_bytes(l), st>>>(
         G, ldg, (int)l, (double)nrows, Rinv, ldri, R, ldr, dinfo, gate_in, gate_out, first_pass);
     POD_CHECK_LAUNCH("cholqr in place");
   } else {
