@@ -137,6 +137,10 @@ def tri_apply_bounds(l):
     return b + [l]
 
 
+#: row-sharded rounds over NCCL are captured into CUDA graphs like the
+#: single-GPU rounds (POD_SHARDED_GRAPHS=0: eager launches)
+SHARDED_GRAPHS = __import__("os").environ.get("POD_SHARDED_GRAPHS", "1") != "0"
+
 #: with the folded pass, the leak GEMM U1^T Q1 (merge.py:72) no longer waits
 #: for the pass-1 factor: it runs on its own stream beside that single-CTA
 #: kernel (non-speculative, unsharded merges).  POD_EARLY_LEAK=0 disables.
@@ -853,8 +857,16 @@ class IsmaEngine(MergeWorkspace):
         self.cosines_ops(cur, 1 - cur, fused=fc)
         self.readback()
 
+    def sharded_graphs(self):
+        """Row-sharded rounds replay as CUDA graphs when the collectives are
+        NCCL's (stream-ordered, capturable: every rank captures the same
+        launch sequence); gloo's host-mediated collectives cannot be captured
+        and run eagerly.  POD_SHARDED_GRAPHS=0 disables."""
+        return SHARDED_GRAPHS and self.comm.backend == "nccl"
+
     def launch_round(self, mode, cur, ub, pipelined, rowsrc=None):
-        if not self.use_graphs or self.ctx.prof is not None or self.comm.active:
+        if (not self.use_graphs or self.ctx.prof is not None
+                or (self.comm.active and not self.sharded_graphs())):
             self.round_ops(mode, cur, ub, pipelined, rowsrc)
             return
         # graphs bake the matrix pointer into their launches: one set per A buffer
@@ -1117,7 +1129,8 @@ def get_engine(ctx, A, *, k, r, c, criterion, use_graphs, comm=None, row_offset=
     world = 1 if comm is None else comm.world
     key = (A.m, A.ncols, A.ld, A.code, A.t.is_cuda, int(k), int(r), int(c), criterion,
            bool(use_graphs),
-           ctx.device.index, world, int(row_offset), m_total, int(w), precision)
+           ctx.device.index, world, bool(comm is not None and comm.active), int(row_offset),
+           m_total, int(w), precision)
     lru = _ENGINE_CACHE.setdefault(ctx.device.index, [])
     for i, eng in enumerate(lru):
         if eng.key == key:

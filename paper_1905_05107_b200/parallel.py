@@ -49,9 +49,15 @@ def shard_rows(m, world, rank):
 
 
 class Comm:
-    """Collectives over the default process group (no-ops for one rank)."""
+    """Collectives over the default process group (no-ops for one rank).
 
-    def __init__(self, group=None):
+    force (or POD_COMM_FORCE=1): a single-rank group still takes the sharded
+    code path and issues its collectives -- the way to drive the NCCL calls,
+    and their capture into the round graphs, on a one-GPU box."""
+
+    def __init__(self, group=None, force=None):
+        import os
+
         import torch.distributed as dist
 
         self.dist = dist
@@ -61,18 +67,25 @@ class Comm:
             self.rank = dist.get_rank(group)
         else:
             self.world, self.rank = 1, 0
+        if force is None:
+            force = os.environ.get("POD_COMM_FORCE", "0") == "1"
+        self.force = bool(force) and dist.is_available() and dist.is_initialized()
 
     @property
     def active(self):
-        return self.world > 1
+        return self.world > 1 or self.force
+
+    @property
+    def backend(self):
+        return self.dist.get_backend(self.group) if self.dist.is_initialized() else None
 
     def allreduce_sum_(self, t):
-        if self.world > 1:
+        if self.active:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t
 
     def allreduce_max_(self, t):
-        if self.world > 1:
+        if self.active:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return t
 
@@ -93,13 +106,13 @@ class Comm:
         return t
 
     def broadcast_(self, t, src):
-        if self.world > 1:
+        if self.active:
             self.dist.broadcast(t, src, group=self.group)
         return t
 
     def allgather(self, t):
         """Stack of every rank's tensor along a new leading axis."""
-        if self.world == 1:
+        if not self.active:
             return t.unsqueeze(0)
         out = [torch.empty_like(t) for _ in range(self.world)]
         self.dist.all_gather(out, t.contiguous(), group=self.group)

@@ -118,3 +118,61 @@ def test_two_rank_host_resident_config5_matches_oracle():
         assert sigma_relerr(s, o["sigma"]) <= SIGMA_RTOL
         assert principal_angles_sin(u, o["u"]).max() <= ANGLE_TOL_RAD
         assert principal_angles_sin(v, o["v"]).max() <= ANGLE_TOL_RAD
+
+
+# ---- NCCL on the one GPU: a single-rank group on the sharded code path -----
+_NCCL_SCRIPT = r"""
+import os, sys
+sys.path.insert(0, {root!r})
+os.environ["MASTER_ADDR"] = "127.0.0.1"
+os.environ["MASTER_PORT"] = {port!r}
+import numpy as np, torch
+import torch.distributed as dist
+import paper_1905_05107_b200 as pod
+from paper_1905_05107_b200 import engine, workloads
+from paper_1905_05107_b200.parallel import Comm
+
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+try:
+    comm = Comm(force=True)
+    assert comm.active and comm.backend == "nccl"
+    a = workloads.config1(seed=0)
+    cfg = pod.IsmaConfig(k=10, r=30, c=50, tau=0.999, strategy="l2n", criterion={crit!r}, seed=7)
+    f, tr = pod.isma_run(np.asfortranarray(a), cfg, comm=comm, m_total=a.shape[0])
+    engs = [e for lru in engine._ENGINE_CACHE.values() for e in lru]
+    graphs = sum(len(getattr(e, "graphs", ())) for e in engs)
+    np.savez({out!r}, u=f.u, sigma=f.sigma, v=f.v, remaining=[t.remaining for t in tr],
+             graphs=graphs, expect_graphs=int(engine.SHARDED_GRAPHS))
+finally:
+    dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("crit", ["modes", "subspace"])
+def test_single_rank_nccl_group_runs_sharded_path_with_captured_rounds(tmp_path, crit):
+    """The row-sharded code path with its collectives carried by NCCL (a
+    one-rank group, Comm(force=True)): norms chain + broadcast, every
+    allreduce of the round (Gram, M, CholeskyQR Grams, leak, cosines) inside
+    the captured round graphs, the fix_signs allgather and finalize's
+    allreduce -- against the oracle, like the unsharded run."""
+    import subprocess
+    import sys
+
+    from oracle import isma_oracle as orc
+    from paper_1905_05107_b200 import workloads
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "nccl1.npz")
+    subprocess.run([sys.executable, "-c",
+                    _NCCL_SCRIPT.format(root=root, port=str(_port()), crit=crit, out=out)],
+                   check=True, timeout=600)
+    g = np.load(out)
+    a = workloads.config1(seed=0)
+    o = orc.run(a, 10, r=30, c=50, tau=0.999, strategy="l2n", criterion=crit, seed=7)
+    assert list(g["remaining"]) == [t["remaining"] for t in o["trace"]]
+    assert sigma_relerr(g["sigma"], o["sigma"]) <= SIGMA_RTOL
+    assert principal_angles_sin(g["u"], o["u"]).max() <= ANGLE_TOL_RAD
+    assert principal_angles_sin(g["v"], o["v"]).max() <= ANGLE_TOL_RAD
+    if int(g["expect_graphs"]):
+        assert int(g["graphs"]) > 0, "sharded NCCL rounds were not graph-captured"
