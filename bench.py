@@ -128,7 +128,7 @@ class ClockSampler:
 
 # ncu `--set full` DRAM traffic per call of the hot kernels (committed
 # summary of tools/profile_targets.py): "name | dram_rd [unit] | dram_wr [unit]"
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r02b_ncu_traffic.txt")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "r02c_ncu_traffic.txt")
 
 
 def _profiled_traffic():

@@ -1053,6 +1053,15 @@ class IsmaEngine(MergeWorkspace):
         xi = np.zeros(self.k)
         it = 0
         ub = 1
+        if pipelined:
+            # round t's graph draws update(t + 2) from uniform slot (t + 2) % 3.
+            # Its batch is staged while round t - 1 still runs (right after
+            # that round's launch, below), so between two rounds the host only
+            # reads the record and launches; the slot's last reader, round
+            # t - 3, has completed by then.  Round 1's batch goes in now (the
+            # bootstrap's record read synchronized the device).
+            spec[3] = bitgen.state
+            self._stage_uniforms(rng, 0)                                     # round 3
         while rem and (it == 0 or bool(np.any(xi < tau))):
             it += 1
             t0 = time.perf_counter()
@@ -1061,8 +1070,6 @@ class IsmaEngine(MergeWorkspace):
             rowsrc = None
             if pipelined:
                 ub = it % NSLOT
-                spec[it + 2] = bitgen.state
-                self._stage_uniforms(rng, (it + 2) % NSLOT)                  # round it + 2
             else:
                 if rows:
                     state = bitgen.state if bitgen is not None else None
@@ -1071,6 +1078,9 @@ class IsmaEngine(MergeWorkspace):
                 self._stage_uniforms(rng, ub, rows)
             self.launch_round(mode, cur, ub, pipelined, rowsrc)
             ran = it
+            if pipelined:  # the next round's batch, while this round runs
+                spec[it + 3] = bitgen.state
+                self._stage_uniforms(rng, (it + 3) % NSLOT)                  # round it + 3
             rec, xi = self.read_record(ub)
             self._log_draw(ub, rec)
             if rows:
