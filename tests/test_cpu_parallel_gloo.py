@@ -130,3 +130,54 @@ def _chained_norms(comm):
 def test_chained_norm_pass_over_ranks_equals_numpy(world):
     for got, ref in run_world(_chained_norms, world=world):
         assert np.array_equal(got, ref)
+
+
+def _forced_single_rank(comm):
+    """Comm(force=True) on a one-rank group: the sharded path's collectives
+    are issued (identity results) instead of short-circuited."""
+    forced = Comm(force=True)
+    t = torch.arange(6, dtype=torch.float64)
+    out = {
+        "plain_active": comm.active,
+        "forced_active": forced.active,
+        "backend": forced.backend,
+        "sum": forced.allreduce_sum_(t.clone()).tolist(),
+        "max": forced.allreduce_max_(t.clone()).tolist(),
+        "bcast": forced.broadcast_(t.clone(), 0).tolist(),
+        "gather_shape": list(forced.allgather(t).shape),
+    }
+    rows = gather_row_shards(torch.arange(12, dtype=torch.float64).reshape(3, 4), 4, forced)
+    out["rows"] = rows.tolist()
+    return out
+
+
+def test_forced_single_rank_group_issues_collectives():
+    res = run_world(_forced_single_rank, world=1)[0]
+    assert res["plain_active"] is False and res["forced_active"] is True
+    assert res["backend"] == "gloo"
+    assert res["sum"] == res["max"] == res["bcast"] == [0.0, 1.0, 2.0, 3.0, 4.0, 5.0]
+    assert res["gather_shape"] == [1, 6]
+    assert res["rows"] == np.arange(12.0).reshape(3, 4).T.tolist()
+
+
+def test_comm_without_process_group_is_inactive_even_when_forced():
+    c = Comm(force=True)
+    assert not c.active and c.world == 1 and c.backend is None
+
+
+def test_triangular_apply_chunks_cover_the_width():
+    """engine.tri_apply_bounds: contiguous chunks from 0 to l; single call
+    below 120 columns, [0, 80, l] to 160, 64-wide chunks beyond with no thin
+    tail."""
+    from paper_1905_05107_b200.engine import tri_apply_bounds
+
+    for l in list(range(1, 300)) + [384, 512, 1000]:
+        b = tri_apply_bounds(l)
+        assert b[0] == 0 and b[-1] == l and all(x < y for x, y in zip(b[:-1], b[1:]))
+        if l < 120:
+            assert b == [0, l]
+        elif l <= 160:
+            assert b == [0, 80, l]
+        else:
+            assert all(y - x == 64 for x, y in zip(b[:-2], b[1:-1]))
+            assert 32 <= b[-1] - b[-2] < 96
